@@ -1,0 +1,116 @@
+/*
+ * runsort_b200.h -- C ABI of the B200 run-adaptive stable mergesort.
+ *
+ * Drop-in boundary for the reference package's sort entry points
+ * (/root/reference/pkg/src/runsort):
+ *
+ *   powersort(a, cfg, metrics, tags) -> Metrics      sorters.py:430-519
+ *   peeksort(a, cfg, metrics, tags)  -> Metrics      sorters.py:146-361
+ *   SortConfig(min_run_len, merge_kind, record_tree)  sorters.py:63-87
+ *   Metrics(merge_cost, comparisons, runs_detected,
+ *           max_stack_height, merge_tree)            runcore.py:40-55
+ *
+ * The reference is pure Python, so its "FFI" is the Python call itself; a
+ * maintainer binds these symbols with ctypes.  Plain C types
+ * only: device or host pointers, sizes, an opaque cudaStream_t.
+ *
+ * Error codes map onto the reference's exceptions:
+ *   RS_EINVAL      -> ValueError      (sorters.py:81-87 config validation)
+ *   RS_EINVARIANT  -> AssertionError  (sorters.py:481-482, 491-494, 508-509)
+ *   RS_ENOMEM      -> MemoryError     (bench.py:125-133 memory guard)
+ *   RS_ECUDA       -> RuntimeError
+ *   RS_EUNSUPPORTED-> TypeError / NotImplementedError (dtype or size outside
+ *                     the device path; never a silent CPU fallback)
+ */
+#ifndef RUNSORT_B200_H
+#define RUNSORT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RS_OK 0
+#define RS_EINVAL 1
+#define RS_EINVARIANT 2
+#define RS_ENOMEM 3
+#define RS_ECUDA 4
+#define RS_EUNSUPPORTED 5
+
+#define RS_ALGO_POWERSORT 0
+#define RS_ALGO_PEEKSORT 1
+
+#define RS_KEY_I32 1
+#define RS_KEY_I64 2
+
+#define RS_MERGE_BITONIC 0 /* exactly size comparisons per merge (runcore.py:282-301) */
+#define RS_MERGE_CLASSIC 1 /* two-pointer count (runcore.py:304-326) */
+
+/* Per-call counters, same meaning as the reference Metrics fields.  rs_sort
+ * reports the values of THIS call; accumulation into a caller-held Metrics
+ * (+= for counters, max for the stack height, assignment for peeksort's
+ * runs_detected) is the binding's job, as in sorters.py:443-444. */
+typedef struct {
+  uint64_t merge_cost;
+  uint64_t comparisons;
+  uint64_t runs_detected;
+  uint64_t max_stack_height;
+} rs_metrics;
+
+/* Optional merge-tree export for SortConfig.record_tree (opttree.py:60-75).
+ * Host buffers of `capacity` entries; the tree is the min-Cartesian tree of
+ * node_depth (equivalently of node_power for powersort). */
+typedef struct {
+  int64_t capacity;    /* in: entries available in each array */
+  int64_t n_leaves;    /* out: r */
+  int64_t* leaf_len;   /* out: r leaf lengths, left to right */
+  uint8_t* node_power; /* out: r-1 node powers (powersort), boundary order */
+  uint8_t* node_depth; /* out: r-1 node depths (root = 0), boundary order */
+} rs_tree;
+
+/* Device workspace needed by rs_sort (bytes). */
+size_t rs_workspace_bytes(int algo, int key_dtype, int tag_bytes, int64_t n, int32_t min_run_len);
+
+/* Sort `n` keys in place on the device, moving the optional `tags` payload
+ * (tag_bytes = 0, 4 or 8) in lockstep.  keys/tags/workspace are device
+ * pointers; the work is enqueued on `stream` (a cudaStream_t, NULL = legacy
+ * default).  When `out` or `tree` is non-NULL the call synchronizes the stream
+ * and fills them; otherwise it returns without waiting and rs_fetch_metrics
+ * retrieves the counters later. */
+int rs_sort(int algo, int key_dtype, void* keys, int tag_bytes, void* tags, int64_t n,
+            int32_t min_run_len, int32_t merge_kind, void* workspace, size_t ws_bytes,
+            void* stream, rs_metrics* out, rs_tree* tree);
+
+/* Synchronize `stream` and read the counters of the last rs_sort that used
+ * `workspace` (same n / dtypes / min_run_len). */
+int rs_fetch_metrics(int algo, int key_dtype, int tag_bytes, int64_t n, int32_t min_run_len,
+                     void* workspace, void* stream, rs_metrics* out);
+
+/* Host-buffer convenience entry (what a plain ctypes binding of the reference
+ * would call with numpy arrays): allocates device memory, copies in, sorts,
+ * copies back, frees.  Synchronous. */
+int rs_sort_host(int algo, int key_dtype, void* keys, int tag_bytes, void* tags, int64_t n,
+                 int32_t min_run_len, int32_t merge_kind, rs_metrics* out, rs_tree* tree);
+
+/* Per-phase CUDA-event timing of subsequent rs_sort calls on this thread
+ * (phases: leaves, tree, tasks, execute; events recorded on the sort's own
+ * stream).  rs_profile_read waits for the last profiled call and writes up to
+ * `cap` phase durations in milliseconds; returns the number written. */
+int rs_profile(int enable);
+int rs_profile_read(double* ms, int cap);
+
+/* Largest min_run_len the device path accepts for this element type. */
+int32_t rs_max_min_run_len(int key_dtype, int tag_bytes);
+
+/* Thread-local message for the last non-RS_OK return. */
+const char* rs_last_error(void);
+
+/* ABI version (major * 100 + minor). */
+int rs_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RUNSORT_B200_H */

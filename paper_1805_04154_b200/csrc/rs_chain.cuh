@@ -1,0 +1,304 @@
+// rs_chain.cuh -- run detection and the min-run leaf chain (powersort's detect()).
+//
+// Reference: sorters.py:462-470 (detect: natural run from `start`, extended to
+// min_run_len by insertion sort), runcore.py:137-159 (find_run_right: maximal
+// weakly-increasing or strictly-decreasing run).
+//
+// Closed form: with asc_k = a[k] <= a[k+1] and
+// B = {k in [1,n-2] : asc_k != asc_{k-1}} U {n-1}, natEnd(p) = min{k in B, k > p},
+// and the leaf chain is p_0 = 0, p_{i+1} = max(natEnd(p_i)+1, min(p_i+w, n)).
+// The chain is sequential; we make it parallel with per-tile candidate tables:
+// the first chain position >= a tile start t0 is one of {t0..t0+w-1} or
+// natEnd(t0-1)+1 (candidate index w).  Each tile maps candidate -> (exit
+// candidate of the next tile, #leaves in this tile); tables are composed per
+// group, then sequentially across groups, then leaves are emitted per tile.
+#pragma once
+#include "rs_common.cuh"
+
+namespace rs {
+
+// Build the B-words (run-boundary bits), zero word 0 when it holds only
+// positions before the window of interest, and the next-nonzero index array.
+// Executed by one warp over nwords words.  asc[] must hold the window's asc words
+// and `prev0` the asc word just before the window (0 when none).
+__device__ inline void build_bwords_warp(const uint32_t* asc, uint32_t prev0, uint32_t* bw,
+                                         uint16_t* nz, int nwords, pos_t base, pos_t n,
+                                         bool zero_first) {
+  int lane = threadIdx.x & 31;
+  for (int q = lane; q < nwords; q += 32) {
+    uint32_t x = asc[q];
+    uint32_t prev = q > 0 ? asc[q - 1] : prev0;
+    uint32_t b = x ^ ((x << 1) | (prev >> 31));
+    pos_t p0 = base + 32 * pos_t(q);
+    if (p0 == 0) b &= ~1u;  // B_0 undefined (k >= 1)
+    // positions >= n-1: B_{n-1} = 1, beyond: 0
+    pos_t last = n - 1;
+    if (last < p0) b = 0;
+    else if (last < p0 + 32) {
+      int bit = int(last - p0);
+      b &= (bit == 31) ? 0xffffffffu : ((1u << (bit + 1)) - 1);
+      b |= 1u << bit;
+    }
+    if (q == 0 && zero_first) b = 0;
+    bw[q] = b;
+  }
+  __syncwarp();
+  // next-nonzero word index, scanning chunks of 32 from the end
+  int carry = nwords;
+  int nchunks = (nwords + 31) >> 5;
+  for (int c = nchunks - 1; c >= 0; --c) {
+    int q = c * 32 + lane;
+    bool nzb = (q < nwords) && bw[q] != 0;
+    uint32_t bal = __ballot_sync(0xffffffffu, nzb);
+    uint32_t m = bal & (0xffffffffu << lane);
+    if (q < nwords) nz[q] = (uint16_t)(m ? c * 32 + __ffs(m) - 1 : carry);
+    if (bal) carry = c * 32 + __ffs(bal) - 1;
+  }
+  __syncwarp();
+}
+
+// natEnd(p) within the window; kInf when beyond it.
+__device__ __forceinline__ pos_t nat_end_win(const uint32_t* bw, const uint16_t* nz, int nwords,
+                                             pos_t base, pos_t n, pos_t p) {
+  if (p >= n - 1) return n - 1;
+  return next_set_bit(bw, nz, nwords, base, p + 1);
+}
+
+__device__ __forceinline__ pos_t chain_next(pos_t p, pos_t ne, int w, pos_t n) {
+  pos_t b = p + w < n ? p + w : n;
+  pos_t a = ne + 1;
+  return a > b ? a : b;
+}
+
+// Window of words [q0, q1) for chain tile `tile`.
+__device__ __forceinline__ void chain_window(int64_t tile, pos_t n, int w, int64_t* q0, int64_t* q1,
+                                             pos_t* t0, pos_t* t1) {
+  *t0 = tile * (pos_t)kChainT;
+  *t1 = (*t0 + kChainT < n) ? *t0 + kChainT : n;
+  int64_t total_words = (n + 31) >> 5;
+  *q0 = *t0 == 0 ? 0 : ((*t0 - 1) >> 5);
+  int64_t e = ((*t1 + w + 64) >> 5) + 1;
+  *q1 = e < total_words ? e : total_words;
+}
+
+__host__ __device__ constexpr int kMaxWinWords(int w) { return (kChainT + w + 96) / 32 + 4; }
+
+// K1+K2a: pair-type bits for this tile (written to ascw) and the tile's
+// candidate table.  One CTA per chain tile.
+template <typename K>
+__global__ void __launch_bounds__(128) k_scan_tables(const K* __restrict__ a, pos_t n, int w,
+                                                     uint32_t* __restrict__ ascw,
+                                                     uint2* __restrict__ tables) {
+  extern __shared__ uint32_t smem_u32[];
+  int64_t tile = blockIdx.x;
+  pos_t t0, t1;
+  int64_t q0, q1;
+  chain_window(tile, n, w, &q0, &q1, &t0, &t1);
+  int nwords = int(q1 - q0);
+  uint32_t* asc = smem_u32;
+  uint32_t* bw = asc + nwords;
+  uint16_t* nz = reinterpret_cast<uint16_t*>(bw + nwords);
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int64_t own0 = t0 >> 5, own1 = (t1 + 31) >> 5;
+  for (int qi = wid; qi < nwords; qi += nw) {
+    int64_t q = q0 + qi;
+    pos_t k = 32 * q + lane;
+    K v = k < n ? a[k] : K(0);
+    K nx = __shfl_down_sync(0xffffffffu, v, 1);
+    if (lane == 31) nx = (k + 1 < n) ? a[k + 1] : K(0);
+    bool bit = (k < n - 1) && (v <= nx);
+    uint32_t word = __ballot_sync(0xffffffffu, bit);
+    if (lane == 0) {
+      asc[qi] = word;
+      if (q >= own0 && q < own1) ascw[q] = word;
+    }
+  }
+  __syncthreads();
+  pos_t base = 32 * q0;
+  if (wid == 0) build_bwords_warp(asc, 0u, bw, nz, nwords, base, n, q0 > 0 || t0 > 0);
+  __syncthreads();
+  // candidates
+  for (int c = threadIdx.x; c <= w; c += blockDim.x) {
+    pos_t p;
+    if (c < w) p = t0 + c;
+    else if (t0 == 0) p = 0;
+    else {
+      pos_t ne = nat_end_win(bw, nz, nwords, base, n, t0 - 1);
+      p = ne >= kInf ? kInf : ne + 1;
+    }
+    uint32_t cnt = 0;
+    while (p < t1) {
+      ++cnt;
+      pos_t ne = nat_end_win(bw, nz, nwords, base, n, p);
+      if (ne >= kInf) { p = kInf; break; }
+      p = chain_next(p, ne, w, n);
+    }
+    uint32_t ex;
+    if (p >= kInf) ex = (uint32_t)w;
+    else ex = (p - t1 < w) ? (uint32_t)(p - t1) : (uint32_t)w;
+    tables[tile * (w + 1) + c] = make_uint2(ex, cnt);
+  }
+}
+
+// K2b: compose the tables of each group of kChainGroup tiles.
+// out[g*(w+1)+c] = (exit candidate after the group, #leaves) starting at candidate c.
+__global__ void k_group_compose(const uint2* __restrict__ tables, int64_t ntiles, int w, int batch,
+                                uint2* __restrict__ gtab) {
+  extern __shared__ uint2 stab[];
+  int W1 = w + 1;
+  uint32_t* cur = reinterpret_cast<uint32_t*>(stab + (size_t)batch * W1);
+  uint32_t* cnt = cur + W1;
+  int64_t g = blockIdx.x;
+  int64_t k0 = g * kChainGroup, k1 = k0 + kChainGroup < ntiles ? k0 + kChainGroup : ntiles;
+  for (int c = threadIdx.x; c < W1; c += blockDim.x) { cur[c] = c; cnt[c] = 0; }
+  for (int64_t kb = k0; kb < k1; kb += batch) {
+    int nb = int((k1 - kb) < batch ? (k1 - kb) : batch);
+    __syncthreads();
+    for (int x = threadIdx.x; x < nb * W1; x += blockDim.x) stab[x] = tables[kb * W1 + x];
+    __syncthreads();
+    for (int c = threadIdx.x; c < W1; c += blockDim.x) {
+      uint32_t e = cur[c], s = cnt[c];
+      for (int k = 0; k < nb; ++k) {
+        uint2 t = stab[k * W1 + e];
+        s += t.y;
+        e = t.x;
+      }
+      cur[c] = e;
+      cnt[c] = s;
+    }
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < W1; c += blockDim.x) gtab[g * W1 + c] = make_uint2(cur[c], cnt[c]);
+}
+
+// K2c: one CTA walks the group tables from candidate 0 of tile 0, recording each
+// group's entry candidate and leaf offset; writes r and the start sentinel.
+__global__ void k_group_entries(const uint2* __restrict__ gtab, int64_t ngroups, int w, int batch,
+                                uint32_t* __restrict__ gentry, uint64_t* __restrict__ goff,
+                                pos_t* __restrict__ leaf_start, pos_t n, int64_t r_max,
+                                DevMetrics* __restrict__ met) {
+  extern __shared__ uint2 stab[];
+  int W1 = w + 1;
+  __shared__ uint32_t s_e;
+  __shared__ unsigned long long s_off;
+  if (threadIdx.x == 0) { s_e = 0; s_off = 0; }
+  for (int64_t gb = 0; gb < ngroups; gb += batch) {
+    int nb = int((ngroups - gb) < batch ? (ngroups - gb) : batch);
+    __syncthreads();
+    for (int x = threadIdx.x; x < nb * W1; x += blockDim.x) stab[x] = gtab[gb * W1 + x];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t e = s_e;
+      unsigned long long off = s_off;
+      for (int k = 0; k < nb; ++k) {
+        gentry[gb + k] = e;
+        goff[gb + k] = off;
+        uint2 t = stab[k * W1 + e];
+        off += t.y;
+        e = t.x;
+      }
+      s_e = e;
+      s_off = off;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long r = s_off;
+    if ((int64_t)r > r_max) { met->error = 1; r = r_max; }
+    met->n_leaves = r;
+    met->runs_detected = r;
+    leaf_start[r] = n;
+  }
+}
+
+// K2d: per group, walk the tile tables to get each tile's entry and leaf offset
+// (tables staged through shared memory in batches).
+__global__ void k_tile_entries(const uint2* __restrict__ tables, int64_t ntiles, int w, int batch,
+                               const uint32_t* __restrict__ gentry, const uint64_t* __restrict__ goff,
+                               uint32_t* __restrict__ tentry, uint64_t* __restrict__ toff) {
+  extern __shared__ uint2 stab[];
+  __shared__ uint32_t s_e;
+  __shared__ unsigned long long s_off;
+  int W1 = w + 1;
+  int64_t g = blockIdx.x;
+  int64_t k0 = g * kChainGroup, k1 = k0 + kChainGroup < ntiles ? k0 + kChainGroup : ntiles;
+  if (threadIdx.x == 0) { s_e = gentry[g]; s_off = goff[g]; }
+  for (int64_t kb = k0; kb < k1; kb += batch) {
+    int nb = int((k1 - kb) < batch ? (k1 - kb) : batch);
+    __syncthreads();
+    for (int x = threadIdx.x; x < nb * W1; x += blockDim.x) stab[x] = tables[kb * W1 + x];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t e = s_e;
+      unsigned long long off = s_off;
+      for (int k = 0; k < nb; ++k) {
+        tentry[kb + k] = e;
+        toff[kb + k] = off;
+        uint2 t = stab[k * W1 + e];
+        off += t.y;
+        e = t.x;
+      }
+      s_e = e;
+      s_off = off;
+    }
+  }
+}
+
+// K2e: one warp per tile re-walks the chain from the tile's true entry and emits
+// leaves: start position and info = min(natural run length, w) | desc << 31.
+__global__ void __launch_bounds__(256) k_emit_leaves(const uint32_t* __restrict__ ascw, pos_t n, int w,
+                                                     int64_t ntiles, const uint32_t* __restrict__ tentry,
+                                                     const uint64_t* __restrict__ toff, int64_t r_max,
+                                                     pos_t* __restrict__ leaf_start,
+                                                     uint32_t* __restrict__ leaf_info) {
+  extern __shared__ uint32_t smem_u32[];
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int64_t tile = (int64_t)blockIdx.x * (blockDim.x >> 5) + wid;
+  if (tile >= ntiles) return;
+  int maxw = kMaxWinWords(w);
+  uint32_t* asc = smem_u32 + (size_t)wid * (maxw * 2 + (maxw + 1) / 2 + 1);
+  uint32_t* bw = asc + maxw;
+  uint16_t* nz = reinterpret_cast<uint16_t*>(bw + maxw);
+  pos_t t0, t1;
+  int64_t q0, q1;
+  chain_window(tile, n, w, &q0, &q1, &t0, &t1);
+  int nwords = int(q1 - q0);
+  for (int q = lane; q < nwords; q += 32) asc[q] = ascw[q0 + q];
+  uint32_t prev0 = q0 > 0 ? ascw[q0 - 1] : 0u;
+  __syncwarp();
+  pos_t base = 32 * q0;
+  build_bwords_warp(asc, prev0, bw, nz, nwords, base, n, false);
+  if (lane != 0) return;
+  uint32_t e = tentry[tile];
+  uint64_t off = toff[tile];
+  pos_t p;
+  if (e < (uint32_t)w) p = t0 + e;
+  else if (t0 == 0) p = 0;
+  else {
+    pos_t ne = nat_end_win(bw, nz, nwords, base, n, t0 - 1);
+    p = ne >= kInf ? kInf : ne + 1;
+  }
+  while (p < t1) {
+    pos_t ne = nat_end_win(bw, nz, nwords, base, n, p);
+    uint32_t nl;
+    if (ne >= kInf) nl = (uint32_t)w;
+    else {
+      pos_t L = ne - p + 1;
+      nl = L < w ? (uint32_t)L : (uint32_t)w;
+    }
+    uint32_t desc = 0;
+    if (p < n - 1) {
+      pos_t rel = p - base;
+      desc = ((asc[rel >> 5] >> (rel & 31)) & 1u) ? 0u : 1u;
+    }
+    if ((int64_t)off < r_max) {
+      leaf_start[off] = p;
+      leaf_info[off] = nl | (desc << 31);
+    }
+    ++off;
+    if (ne >= kInf) break;
+    p = chain_next(p, ne, w, n);
+  }
+}
+
+}  // namespace rs

@@ -1,0 +1,140 @@
+// rs_common.cuh -- shared types and device helpers for the B200 run-adaptive
+// mergesort (powersort / peeksort of arXiv 1805.04154).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace rs {
+
+using pos_t = int64_t;
+
+constexpr int kWarp = 32;
+constexpr pos_t kInf = INT64_MAX / 4;
+
+// ---- chain (min-run) phase ----
+constexpr int kChainT = 4096;      // positions per chain tile
+constexpr int kChainThreads = 256;
+constexpr int kChainGroup = 64;    // tiles per composition group
+constexpr int kTableBatch = 32;    // tables staged into smem per batch
+
+// ---- executor ----
+constexpr int kExecThreads = 256;
+constexpr int kMaxDepth = 64;      // depth <= max power <= 63
+
+// Task records (u64): [63:62] kind, [61:32] tile index, [31:0] unified node id.
+enum TaskKind : uint32_t { kTaskFuse = 0, kTaskLeaf = 1, kTaskMerge = 2 };
+__host__ __device__ inline uint64_t make_task(uint32_t kind, uint32_t tile, uint32_t id) {
+  return (uint64_t(kind) << 62) | (uint64_t(tile & 0x3fffffffu) << 32) | uint64_t(id);
+}
+__host__ __device__ inline uint32_t task_kind(uint64_t t) { return uint32_t(t >> 62); }
+__host__ __device__ inline uint32_t task_tile(uint64_t t) { return uint32_t(t >> 32) & 0x3fffffffu; }
+__host__ __device__ inline uint32_t task_id(uint64_t t) { return uint32_t(t); }
+
+// Leaf modes for big (non-fused) leaves.
+enum LeafMode : int { kLeafNone = 0, kLeafSwap = 1, kLeafRevCopy = 2, kLeafCopy = 3 };
+
+// Device-resident metrics, accumulated with atomics (reference runcore.py:40-55).
+struct DevMetrics {
+  unsigned long long merge_cost;
+  unsigned long long comparisons;
+  unsigned long long runs_detected;
+  unsigned long long max_stack_height;
+  unsigned long long error;       // nonzero: invariant failure (maps to AssertionError)
+  unsigned long long n_leaves;    // r
+  unsigned long long n_tasks;     // total executor tasks
+  unsigned long long task_ctr;    // executor claim counter
+  unsigned long long phaseA;      // number of phase-A tasks (fuse + leaf tiles)
+  unsigned long long cursorA;     // phase-A slot allocator
+  unsigned long long max_depth;   // deepest internal node
+  unsigned long long n_merge_tasks;
+  unsigned long long depth_tiles[kMaxDepth];
+  unsigned long long depth_base[kMaxDepth];
+  unsigned long long depth_cursor[kMaxDepth];
+};
+
+__device__ __forceinline__ int bitlen64(uint64_t x) { return x ? 64 - __clzll((long long)x) : 0; }
+
+template <typename T>
+__device__ __forceinline__ T ldcg(const T* p) { return __ldcg(p); }
+
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+template <typename T>
+__device__ __forceinline__ T warp_max(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) { T u = __shfl_xor_sync(0xffffffffu, v, o); v = u > v ? u : v; }
+  return v;
+}
+
+// Block-wide sum into thread 0 (all threads must call). smem: >= 32 slots.
+template <typename T>
+__device__ __forceinline__ T block_sum(T v, T* smem) {
+  v = warp_sum(v);
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) smem[wid] = v;
+  __syncthreads();
+  T s = 0;
+  if (threadIdx.x == 0)
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += smem[i];
+  return s;
+}
+
+// Exclusive block scan of u32 counts (all threads call). Returns exclusive prefix;
+// *total gets the block total. smem: >= 33 u32.
+__device__ __forceinline__ uint32_t block_excl_scan_u32(uint32_t v, uint32_t* smem, uint32_t* total) {
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  __syncthreads();
+  if (lane == 31) smem[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    uint32_t s = lane < nw ? smem[lane] : 0, t = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
+    }
+    if (lane < nw) smem[lane] = t - s;
+    if (lane == 31) smem[32] = t;
+  }
+  __syncthreads();
+  uint32_t r = smem[wid] + x - v;
+  *total = smem[32];
+  __syncthreads();
+  return r;
+}
+
+// Next set bit at position >= p inside a window of B-words held in smem.
+// words[q] covers positions base + 32q .. base + 32q + 31; nz[q] = first q' >= q
+// with words[q'] != 0 (nwords when none).  Returns kInf when none in window.
+__device__ __forceinline__ pos_t next_set_bit(const uint32_t* words, const uint16_t* nz, int nwords,
+                                              pos_t base, pos_t p) {
+  pos_t rel = p - base;
+  if (rel < 0) rel = 0;
+  int q = int(rel >> 5);
+  if (q >= nwords) return kInf;
+  uint32_t wv = words[q] & (0xffffffffu << (rel & 31));
+  if (wv) return base + 32 * pos_t(q) + __ffs(wv) - 1;
+  if (q + 1 >= nwords) return kInf;
+  int q2 = nz[q + 1];
+  if (q2 >= nwords) return kInf;
+  return base + 32 * pos_t(q2) + __ffs(words[q2]) - 1;
+}
+
+}  // namespace rs

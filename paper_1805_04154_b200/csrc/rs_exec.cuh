@@ -1,0 +1,646 @@
+// rs_exec.cuh -- leaf formation and dataflow execution of the merge tree.
+//
+// Reference: runcore.py:70-74 (reverse_range), runcore.py:215-248
+// (insertionsort_presorted and its exact comparison count), runcore.py:251-326
+// (stable two-run merge, ties to the left run; bitonic / classic comparison
+// accounting), sorters.py:474-516 (every pending run merged exactly once).
+//
+// Layout: keys/tags live in two HBM buffers, buf[0] = the caller's array and
+// buf[1] = scratch.  A node (or leaf) at tree depth d holds its sorted span in
+// buf[d & 1], so every merge reads buf[(d+1)&1] and writes buf[d&1]; the root
+// (depth 0) lands in the caller's array and no schedule can overwrite data that
+// is still to be read.
+//
+// One persistent kernel claims tasks in list order: first the "phase A" tasks
+// (fused subtrees whose span fits in shared memory -- leaves are formed and all
+// their merges run in SMEM -- and tiles of large leaves), then merge tiles of
+// large nodes, deepest first.  Every task's inputs come from earlier tasks, so
+// waiting on per-node completion counters cannot deadlock while all CTAs are
+// resident.
+#pragma once
+#include "rs_common.cuh"
+
+namespace rs {
+
+template <typename K, int TB>
+struct ExecCfg {
+  static constexpr int kb = sizeof(K);
+  static constexpr int eb = kb + TB;
+  static constexpr int IPT = (kb == 4) ? 15 : 11;  // odd: conflict-free blocked->smem writes
+  static constexpr int TILE = kExecThreads * IPT;
+  static constexpr int FCAP = (eb <= 8) ? 4096 : 2048;  // fused-subtree capacity (elements)
+  static constexpr int IPTF = 8;                        // outputs per fused merge chunk
+  static constexpr int MAXB = FCAP / 2 + 2;             // boundaries inside a fused subtree
+};
+
+template <int TB> struct TagT { using type = uint32_t; };
+template <> struct TagT<8> { using type = uint64_t; };
+
+struct ExecArgs {
+  void* key[2];
+  void* tag[2];
+  pos_t n;
+  int w;
+  int classic;
+  uint32_t leaf_base;
+  const pos_t* leaf_start;
+  const uint32_t* leaf_info;
+  const uint8_t* leaf_depth;
+  const uint8_t* depth;
+  const int32_t* node_a;
+  const int32_t* node_b;
+  const pos_t* node_s;
+  const pos_t* node_e;
+  const uint32_t* child;
+  const uint32_t* need;
+  uint32_t* done;
+  const uint64_t* tasks;
+  DevMetrics* met;
+};
+
+__device__ __forceinline__ int leaf_mode(bool desc, int dpar) {
+  return desc ? (dpar ? kLeafRevCopy : kLeafSwap) : (dpar ? kLeafCopy : kLeafNone);
+}
+__device__ __forceinline__ int64_t leaf_tiles(pos_t len, int mode, int tile) {
+  if (mode == kLeafNone) return 0;
+  if (mode == kLeafSwap) {
+    int64_t half = tile / 2;
+    return ((len / 2) + half - 1) / half;
+  }
+  return (len + tile - 1) / tile;
+}
+
+// ---------------------------------------------------------------- T4: tasks
+struct ClassifyArgs {
+  pos_t n;
+  int w;
+  int classic;
+  int fcap;
+  int tile;
+  uint32_t leaf_base;
+  const pos_t* leaf_start;
+  const uint32_t* leaf_info;
+  const uint8_t* leaf_depth;
+  const uint8_t* depth;
+  const pos_t* node_s;
+  const pos_t* node_e;
+  const int32_t* parent;
+  uint32_t* need;
+  uint64_t* tasks;
+  DevMetrics* met;
+};
+
+__device__ __forceinline__ bool parent_small(const ClassifyArgs& A, int32_t par) {
+  return par >= 0 && (A.node_e[par] - A.node_s[par]) <= A.fcap;
+}
+
+// Per element: 0 = nothing, 1 = fused root, 2 = big (tiles > 0).  *tiles out.
+__device__ __forceinline__ int classify_leaf(const ClassifyArgs& A, int64_t i, int64_t* tiles) {
+  pos_t len = A.leaf_start[i + 1] - A.leaf_start[i];
+  uint32_t lid = A.leaf_base + (uint32_t)i;
+  *tiles = 0;
+  if (len <= A.fcap) return parent_small(A, A.parent[lid]) ? 0 : 1;
+  bool desc = (A.leaf_info[i] >> 31) != 0;
+  int mode = leaf_mode(desc, A.leaf_depth[i] & 1);
+  *tiles = leaf_tiles(len, mode, A.tile);
+  return *tiles > 0 ? 2 : 0;
+}
+__device__ __forceinline__ int classify_node(const ClassifyArgs& A, int64_t j, int64_t* tiles) {
+  pos_t span = A.node_e[j] - A.node_s[j];
+  *tiles = 0;
+  if (span <= A.fcap) return parent_small(A, A.parent[j]) ? 0 : 1;
+  *tiles = (span + A.tile - 1) / A.tile;
+  return 2;
+}
+
+__global__ void k_classify(ClassifyArgs A) {
+  __shared__ unsigned long long sred[32];
+  int64_t r = (int64_t)A.met->n_leaves;
+  unsigned long long comps = 0, mcost = 0, cntA = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < r; i += (int64_t)gridDim.x * blockDim.x) {
+    // leaf: detection comparisons (runcore.py:154/157 closed form)
+    pos_t s0 = A.leaf_start[i], len = A.leaf_start[i + 1] - s0;
+    if (s0 < A.n - 1) {
+      uint32_t nl = A.leaf_info[i] & 0x7fffffffu;
+      pos_t L = (nl >= (uint32_t)A.w) ? len : (pos_t)nl;
+      pos_t ne = s0 + L - 1;
+      comps += (unsigned long long)((ne < A.n - 1) ? L : L - 1);
+    }
+    int64_t tl;
+    int c = classify_leaf(A, i, &tl);
+    uint32_t lid = A.leaf_base + (uint32_t)i;
+    A.need[lid] = c == 1 ? 1u : (uint32_t)tl;
+    cntA += c == 1 ? 1 : (unsigned long long)tl;
+    if (i >= 1) {
+      pos_t span = A.node_e[i] - A.node_s[i];
+      mcost += span;
+      if (!A.classic) comps += span;  // runcore.py:299-301
+      int64_t tn;
+      int cn = classify_node(A, i, &tn);
+      if (cn == 1) { A.need[i] = 1; cntA += 1; }
+      else if (cn == 2) {
+        A.need[i] = (uint32_t)tn;
+        int d = A.depth[i];
+        atomicAdd(&A.met->depth_tiles[d], (unsigned long long)tn);
+        atomicMax(&A.met->max_depth, (unsigned long long)d);
+        atomicAdd(&A.met->n_merge_tasks, (unsigned long long)tn);
+      } else A.need[i] = 0;
+    }
+  }
+  unsigned long long s = block_sum(comps, sred);
+  if (threadIdx.x == 0 && s) atomicAdd(&A.met->comparisons, s);
+  s = block_sum(mcost, sred);
+  if (threadIdx.x == 0 && s) atomicAdd(&A.met->merge_cost, s);
+  s = block_sum(cntA, sred);
+  if (threadIdx.x == 0 && s) atomicAdd(&A.met->phaseA, s);
+}
+
+__global__ void k_task_offsets(DevMetrics* met) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  unsigned long long base = met->phaseA;
+  for (int d = (int)met->max_depth; d >= 0; --d) {
+    met->depth_base[d] = base;
+    met->depth_cursor[d] = base;
+    base += met->depth_tiles[d];
+  }
+  met->n_tasks = base;
+  met->cursorA = 0;
+  met->task_ctr = 0;
+}
+
+__global__ void k_task_fill(ClassifyArgs A) {
+  int64_t r = (int64_t)A.met->n_leaves;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < r; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t tl;
+    int c = classify_leaf(A, i, &tl);
+    uint32_t lid = A.leaf_base + (uint32_t)i;
+    if (c == 1) {
+      unsigned long long slot = atomicAdd(&A.met->cursorA, 1ull);
+      A.tasks[slot] = make_task(kTaskFuse, 0, lid);
+    } else if (c == 2) {
+      unsigned long long slot = atomicAdd(&A.met->cursorA, (unsigned long long)tl);
+      for (int64_t k = 0; k < tl; ++k) A.tasks[slot + k] = make_task(kTaskLeaf, (uint32_t)k, lid);
+    }
+    if (i >= 1) {
+      int64_t tn;
+      int cn = classify_node(A, i, &tn);
+      if (cn == 1) {
+        unsigned long long slot = atomicAdd(&A.met->cursorA, 1ull);
+        A.tasks[slot] = make_task(kTaskFuse, 0, (uint32_t)i);
+      } else if (cn == 2) {
+        unsigned long long slot = atomicAdd(&A.met->depth_cursor[A.depth[i]], (unsigned long long)tn);
+        for (int64_t k = 0; k < tn; ++k) A.tasks[slot + k] = make_task(kTaskMerge, (uint32_t)k, (uint32_t)i);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- searches
+// Number of A elements among the first `diag` outputs of the stable merge of
+// sorted A and B (ties: A first).  Whole warp participates; result in all lanes.
+template <typename K>
+__device__ int64_t warp_merge_path(const K* A, int64_t na, const K* B, int64_t nb, int64_t diag) {
+  int lane = threadIdx.x & 31;
+  int64_t lo = diag - nb > 0 ? diag - nb : 0;
+  int64_t hi = diag < na ? diag : na;
+  while (hi - lo > 32) {
+    int64_t span = hi - lo;
+    int64_t idx = lo + (span * (lane + 1)) / 33;
+    bool pred = ldcg(A + idx) <= ldcg(B + (diag - 1 - idx));
+    uint32_t bal = __ballot_sync(0xffffffffu, pred);
+    int c = __popc(bal);
+    int64_t nlo = c > 0 ? __shfl_sync(0xffffffffu, idx, c - 1) + 1 : lo;
+    int64_t nhi = c < 32 ? __shfl_sync(0xffffffffu, idx, c < 32 ? c : 31) : hi;
+    lo = nlo;
+    hi = nhi;
+  }
+  int64_t idx = lo + lane;
+  bool pred = idx < hi && ldcg(A + idx) <= ldcg(B + (diag - 1 - idx));
+  return lo + __popc(__ballot_sync(0xffffffffu, pred));
+}
+
+// First index in [0, len) where `A[idx] < v` (strict=true) / `A[idx] <= v` fails.
+template <typename K>
+__device__ int64_t warp_count_below(const K* A, int64_t len, K v, bool or_equal) {
+  int lane = threadIdx.x & 31;
+  int64_t lo = 0, hi = len;
+  while (hi - lo > 32) {
+    int64_t span = hi - lo;
+    int64_t idx = lo + (span * (lane + 1)) / 33;
+    K x = ldcg(A + idx);
+    bool pred = or_equal ? (x <= v) : (x < v);
+    uint32_t bal = __ballot_sync(0xffffffffu, pred);
+    int c = __popc(bal);
+    int64_t nlo = c > 0 ? __shfl_sync(0xffffffffu, idx, c - 1) + 1 : lo;
+    int64_t nhi = c < 32 ? __shfl_sync(0xffffffffu, idx, c < 32 ? c : 31) : hi;
+    lo = nlo;
+    hi = nhi;
+  }
+  int64_t idx = lo + lane;
+  bool pred = false;
+  if (idx < hi) {
+    K x = ldcg(A + idx);
+    pred = or_equal ? (x <= v) : (x < v);
+  }
+  return lo + __popc(__ballot_sync(0xffffffffu, pred));
+}
+
+// Thread-level merge path inside shared memory.
+template <typename K>
+__device__ __forceinline__ int smem_merge_path(const K* A, int na, const K* B, int nb, int diag) {
+  int lo = diag - nb > 0 ? diag - nb : 0;
+  int hi = diag < na ? diag : na;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (A[mid] <= B[diag - 1 - mid]) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+template <typename K>
+__device__ __forceinline__ int smem_count(const K* A, int len, K v, bool or_equal) {
+  int lo = 0, hi = len;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    bool p = or_equal ? (A[mid] <= v) : (A[mid] < v);
+    if (p) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// ------------------------------------------------------------- the executor
+template <typename K, int TB>
+struct Exec {
+  using C = ExecCfg<K, TB>;
+  using T = typename TagT<TB>::type;
+  static constexpr bool HAS_TAGS = TB != 0;
+
+  static constexpr size_t smem_merge() { return (size_t)C::TILE * (C::kb + TB) + 64; }
+  static constexpr size_t smem_fuse() {
+    return 2 * (size_t)C::FCAP * (C::kb + TB) + (size_t)C::MAXB * (3 * 2 + 1 + 2 + 2) + 256;
+  }
+  static constexpr size_t smem_bytes() { return smem_merge() > smem_fuse() ? smem_merge() : smem_fuse(); }
+
+  __device__ static void wait_ready(const ExecArgs& E, uint32_t id) {
+    uint32_t need = E.need[id];
+    if (need == 0) return;
+    unsigned ns = 32;
+    while (ld_acquire_u32(E.done + id) < need) {
+      __nanosleep(ns);
+      if (ns < 1024) ns <<= 1;
+    }
+  }
+
+  // --- big-node merge tile ---
+  __device__ static void merge_task(const ExecArgs& E, uint32_t j, uint32_t k, unsigned char* smem,
+                                    unsigned long long& comps) {
+    __shared__ int64_t s_i[2];
+    K* sk = reinterpret_cast<K*>(smem);
+    T* st = reinterpret_cast<T*>(smem + (size_t)C::TILE * C::kb);
+    pos_t s = E.node_s[j], e = E.node_e[j], m = E.leaf_start[j];
+    int d = E.depth[j];
+    const K* src = reinterpret_cast<const K*>(E.key[(d + 1) & 1]);
+    K* dst = reinterpret_cast<K*>(E.key[d & 1]);
+    const T* tsrc = HAS_TAGS ? reinterpret_cast<const T*>(E.tag[(d + 1) & 1]) : nullptr;
+    T* tdst = HAS_TAGS ? reinterpret_cast<T*>(E.tag[d & 1]) : nullptr;
+    if (threadIdx.x == 0) {
+      wait_ready(E, E.child[2 * j]);
+      wait_ready(E, E.child[2 * j + 1]);
+    }
+    __syncthreads();
+    int64_t tot = e - s, na = m - s, nb = e - m;
+    int64_t o0 = (int64_t)k * C::TILE;
+    int64_t o1 = o0 + C::TILE < tot ? o0 + C::TILE : tot;
+    int len = int(o1 - o0);
+    int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (wid == 0) {
+      int64_t v = o0 == 0 ? 0 : warp_merge_path(src + s, na, src + m, nb, o0);
+      if (lane == 0) s_i[0] = v;
+    } else if (wid == 1) {
+      int64_t v = o1 == tot ? na : warp_merge_path(src + s, na, src + m, nb, o1);
+      if (lane == 0) s_i[1] = v;
+    } else if (wid == 2 && E.classic && k == 0) {
+      // runcore.py:321-324
+      K maxL = ldcg(src + m - 1), maxR = ldcg(src + e - 1);
+      int64_t rl = warp_count_below(src + m, nb, maxL, false);
+      int64_t lr = warp_count_below(src + s, na, maxR, true);
+      int64_t pl = na - 1 + rl, pr = nb - 1 + lr;
+      if (lane == 0) comps += (unsigned long long)((pl < pr ? pl : pr) + 1);
+    }
+    __syncthreads();
+    int64_t i0 = s_i[0], i1 = s_i[1];
+    int la = int(i1 - i0), lb = len - la;
+    int64_t j0 = o0 - i0;
+    for (int x = threadIdx.x; x < len; x += blockDim.x) {
+      pos_t g = x < la ? s + i0 + x : m + j0 + (x - la);
+      sk[x] = ldcg(src + g);
+      if (HAS_TAGS) st[x] = ldcg(tsrc + g);
+    }
+    __syncthreads();
+    K rk[C::IPT];
+    T rt[HAS_TAGS ? C::IPT : 1];
+    int d0 = threadIdx.x * C::IPT;
+    int cnt = 0;
+    if (d0 < len) {
+      cnt = len - d0 < C::IPT ? len - d0 : C::IPT;
+      int ai = smem_merge_path(sk, la, sk + la, lb, d0);
+      int bi = d0 - ai;
+#pragma unroll
+      for (int q = 0; q < C::IPT; ++q) {
+        if (q < cnt) {
+          bool takeA = (bi >= lb) || (ai < la && sk[ai] <= sk[la + bi]);
+          int src_i = takeA ? ai : la + bi;
+          rk[q] = sk[src_i];
+          if (HAS_TAGS) rt[q] = st[src_i];
+          ai += takeA;
+          bi += !takeA;
+        }
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < C::IPT; ++q) {
+      if (q < cnt) {
+        sk[d0 + q] = rk[q];
+        if (HAS_TAGS) st[d0 + q] = rt[q];
+      }
+    }
+    __syncthreads();
+    for (int x = threadIdx.x; x < len; x += blockDim.x) {
+      dst[s + o0 + x] = sk[x];
+      if (HAS_TAGS) tdst[s + o0 + x] = st[x];
+    }
+  }
+
+  // --- big-leaf tile: reversal / copy into its depth-parity buffer ---
+  __device__ static void leaf_task(const ExecArgs& E, uint32_t i, uint32_t k) {
+    pos_t s0 = E.leaf_start[i], len = E.leaf_start[i + 1] - s0;
+    bool desc = (E.leaf_info[i] >> 31) != 0;
+    int mode = leaf_mode(desc, E.leaf_depth[i] & 1);
+    K* k0 = reinterpret_cast<K*>(E.key[0]);
+    K* k1 = reinterpret_cast<K*>(E.key[1]);
+    T* t0 = HAS_TAGS ? reinterpret_cast<T*>(E.tag[0]) : nullptr;
+    T* t1 = HAS_TAGS ? reinterpret_cast<T*>(E.tag[1]) : nullptr;
+    if (mode == kLeafSwap) {
+      int64_t half = C::TILE / 2;
+      int64_t x0 = (int64_t)k * half, x1 = x0 + half < len / 2 ? x0 + half : len / 2;
+      for (int64_t x = x0 + threadIdx.x; x < x1; x += blockDim.x) {
+        pos_t u = s0 + x, v = s0 + len - 1 - x;
+        K a = ldcg(k0 + u), b = ldcg(k0 + v);
+        k0[u] = b;
+        k0[v] = a;
+        if (HAS_TAGS) {
+          T ta = ldcg(t0 + u), tb = ldcg(t0 + v);
+          t0[u] = tb;
+          t0[v] = ta;
+        }
+      }
+    } else {
+      int64_t x0 = (int64_t)k * C::TILE, x1 = x0 + C::TILE < len ? x0 + C::TILE : len;
+      for (int64_t x = x0 + threadIdx.x; x < x1; x += blockDim.x) {
+        pos_t from = s0 + x;
+        pos_t to = mode == kLeafRevCopy ? s0 + len - 1 - x : s0 + x;
+        k1[to] = ldcg(k0 + from);
+        if (HAS_TAGS) t1[to] = ldcg(t0 + from);
+      }
+    }
+  }
+
+  // --- fused subtree: form its leaves and run all of its merges in SMEM ---
+  __device__ static void fuse_task(const ExecArgs& E, uint32_t u, unsigned char* smem,
+                                   unsigned long long& comps) {
+    __shared__ uint32_t s_scan[40];
+    __shared__ int s_dmax;
+    K* X[2];
+    T* Y[2];
+    X[0] = reinterpret_cast<K*>(smem);
+    X[1] = X[0] + C::FCAP;
+    unsigned char* p = smem + 2 * (size_t)C::FCAP * C::kb;
+    Y[0] = reinterpret_cast<T*>(p);
+    Y[1] = Y[0] + (HAS_TAGS ? C::FCAP : 0);
+    p += HAS_TAGS ? 2 * (size_t)C::FCAP * TB : 0;
+    uint16_t* ns = reinterpret_cast<uint16_t*>(p);
+    uint16_t* nm = ns + C::MAXB;
+    uint16_t* ne = nm + C::MAXB;
+    uint16_t* lst = ne + C::MAXB;   // level node list
+    uint16_t* loff = lst + C::MAXB; // level chunk offsets
+    uint8_t* dep = reinterpret_cast<uint8_t*>(loff + C::MAXB);
+
+    int64_t la, lb;
+    pos_t s, e;
+    int droot;
+    if (u >= E.leaf_base) {
+      la = lb = u - E.leaf_base;
+      s = E.leaf_start[la];
+      e = E.leaf_start[la + 1];
+      droot = E.leaf_depth[la];
+    } else {
+      la = E.node_a[u];
+      lb = E.node_b[u];
+      s = E.node_s[u];
+      e = E.node_e[u];
+      droot = E.depth[u];
+    }
+    int len = int(e - s);
+    const K* g0 = reinterpret_cast<const K*>(E.key[0]);
+    const T* h0 = HAS_TAGS ? reinterpret_cast<const T*>(E.tag[0]) : nullptr;
+    for (int x = threadIdx.x; x < len; x += blockDim.x) {
+      X[0][x] = ldcg(g0 + s + x);
+      if (HAS_TAGS) Y[0][x] = ldcg(h0 + s + x);
+    }
+    __syncthreads();
+    // leaves: warp per leaf
+    int wid = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
+    for (int64_t li = la + wid; li <= lb; li += nwarp) {
+      int ls = int(E.leaf_start[li] - s), le = int(E.leaf_start[li + 1] - s), ll = le - ls;
+      uint32_t info = E.leaf_info[li];
+      uint32_t nl = info & 0x7fffffffu;
+      bool desc = (info >> 31) != 0;
+      int L = (nl >= (uint32_t)E.w) ? ll : (int)nl;
+      int dp = E.leaf_depth[li] & 1;
+      if (L >= ll) {
+        if (desc) {
+          if (dp == 0) {
+            for (int x = lane; x < ll / 2; x += 32) {
+              K a = X[0][ls + x], b = X[0][le - 1 - x];
+              X[0][ls + x] = b;
+              X[0][le - 1 - x] = a;
+              if (HAS_TAGS) { T ta = Y[0][ls + x]; Y[0][ls + x] = Y[0][le - 1 - x]; Y[0][le - 1 - x] = ta; }
+            }
+          } else {
+            for (int x = lane; x < ll; x += 32) {
+              X[1][ls + x] = X[0][le - 1 - x];
+              if (HAS_TAGS) Y[1][ls + x] = Y[0][le - 1 - x];
+            }
+          }
+        } else if (dp == 1) {
+          for (int x = lane; x < ll; x += 32) {
+            X[1][ls + x] = X[0][ls + x];
+            if (HAS_TAGS) Y[1][ls + x] = Y[0][ls + x];
+          }
+        }
+      } else {
+        // insertionsort_presorted on the post-reversal chunk (runcore.py:215-248)
+        int npre = L > 1 ? L : 1;
+        auto vidx = [&](int t) { return (desc && t < L) ? ls + L - 1 - t : ls + t; };
+        if (ll <= 32) {
+          K xv = K(0);
+          T tv = T(0);
+          if (lane < ll) {
+            xv = X[0][vidx(lane)];
+            if (HAS_TAGS) tv = Y[0][vidx(lane)];
+          }
+          int g = 0, rank = 0;
+          for (int q = 0; q < ll; ++q) {
+            K y = __shfl_sync(0xffffffffu, xv, q);
+            if (q < lane) { g += (y > xv); rank += (y <= xv); }
+            else if (q > lane) rank += (y < xv);
+          }
+          unsigned long long c = 0;
+          if (lane < ll && lane >= npre) c = (unsigned long long)(g + (g < lane ? 1 : 0));
+          comps += c;
+          __syncwarp();
+          if (lane < ll) {
+            X[dp][ls + rank] = xv;
+            if (HAS_TAGS) Y[dp][ls + rank] = tv;
+          }
+        } else {
+          K* dstk = X[1];
+          T* dstt = Y[1];
+          for (int t = lane; t < ll; t += 32) {
+            K xv = X[0][vidx(t)];
+            int g = 0, rank = 0;
+            for (int q = 0; q < ll; ++q) {
+              K y = X[0][vidx(q)];
+              if (q < t) { g += (y > xv); rank += (y <= xv); }
+              else if (q > t) rank += (y < xv);
+            }
+            if (t >= npre) comps += (unsigned long long)(g + (g < t ? 1 : 0));
+            dstk[ls + rank] = xv;
+            if (HAS_TAGS) dstt[ls + rank] = Y[0][vidx(t)];
+          }
+          __syncwarp();
+          if (dp == 0) {
+            for (int x = lane; x < ll; x += 32) {
+              X[0][ls + x] = X[1][ls + x];
+              if (HAS_TAGS) Y[0][ls + x] = Y[1][ls + x];
+            }
+          }
+        }
+      }
+      __syncwarp();
+    }
+    __syncthreads();
+    int nbd = int(lb - la);
+    if (nbd > 0) {
+      if (threadIdx.x == 0) s_dmax = droot;
+      __syncthreads();
+      int dmax_local = droot;
+      for (int x = threadIdx.x; x < nbd; x += blockDim.x) {
+        int64_t jj = la + 1 + x;
+        ns[x] = (uint16_t)(E.node_s[jj] - s);
+        nm[x] = (uint16_t)(E.leaf_start[jj] - s);
+        ne[x] = (uint16_t)(E.node_e[jj] - s);
+        int dd = E.depth[jj];
+        dep[x] = (uint8_t)dd;
+        dmax_local = dd > dmax_local ? dd : dmax_local;
+      }
+      atomicMax(&s_dmax, dmax_local);
+      __syncthreads();
+      int dmax = s_dmax;
+      const int per = (nbd + blockDim.x - 1) / blockDim.x;
+      for (int dd = dmax; dd >= droot; --dd) {
+        // compact this level's nodes and their chunk offsets (packed nodes<<16 | chunks)
+        uint32_t mine = 0;
+        int x0 = threadIdx.x * per;
+        for (int q = 0; q < per; ++q) {
+          int x = x0 + q;
+          if (x < nbd && dep[x] == dd) mine += (1u << 16) + (uint32_t)((ne[x] - ns[x] + C::IPTF - 1) / C::IPTF);
+        }
+        uint32_t total;
+        uint32_t pre = block_excl_scan_u32(mine, s_scan, &total);
+        uint32_t nidx = pre >> 16, coff = pre & 0xffffu;
+        for (int q = 0; q < per; ++q) {
+          int x = x0 + q;
+          if (x < nbd && dep[x] == dd) {
+            lst[nidx] = (uint16_t)x;
+            loff[nidx] = (uint16_t)coff;
+            ++nidx;
+            coff += (ne[x] - ns[x] + C::IPTF - 1) / C::IPTF;
+          }
+        }
+        __syncthreads();
+        int nlev = int(total >> 16), nchunk = int(total & 0xffffu);
+        const K* Xs = X[(dd + 1) & 1];
+        K* Xd = X[dd & 1];
+        const T* Ys = Y[(dd + 1) & 1];
+        T* Yd = Y[dd & 1];
+        for (int c = threadIdx.x; c < nchunk; c += blockDim.x) {
+          // node: last level entry with loff <= c
+          int lo = 0, hi = nlev - 1;
+          while (lo < hi) {
+            int md = (lo + hi + 1) >> 1;
+            if (loff[md] <= c) lo = md; else hi = md - 1;
+          }
+          int x = lst[lo];
+          int a0 = ns[x], mm = nm[x], e0 = ne[x];
+          int na = mm - a0, nb = e0 - mm, size = e0 - a0;
+          int o = (c - loff[lo]) * C::IPTF;
+          int cnt = size - o < C::IPTF ? size - o : C::IPTF;
+          int ai = smem_merge_path(Xs + a0, na, Xs + mm, nb, o);
+          int bi = o - ai;
+          for (int q = 0; q < cnt; ++q) {
+            bool takeA = (bi >= nb) || (ai < na && Xs[a0 + ai] <= Xs[mm + bi]);
+            int si = takeA ? a0 + ai : mm + bi;
+            Xd[a0 + o + q] = Xs[si];
+            if (HAS_TAGS) Yd[a0 + o + q] = Ys[si];
+            ai += takeA;
+            bi += !takeA;
+          }
+          if (E.classic && o == 0) {
+            K maxL = Xs[mm - 1], maxR = Xs[e0 - 1];
+            int rl = smem_count(Xs + mm, nb, maxL, false);
+            int lr = smem_count(Xs + a0, na, maxR, true);
+            int pl = na - 1 + rl, pr = nb - 1 + lr;
+            comps += (unsigned long long)((pl < pr ? pl : pr) + 1);
+          }
+        }
+        __syncthreads();
+      }
+    }
+    K* gd = reinterpret_cast<K*>(E.key[droot & 1]);
+    T* hd = HAS_TAGS ? reinterpret_cast<T*>(E.tag[droot & 1]) : nullptr;
+    const K* Xr = X[droot & 1];
+    const T* Yr = Y[droot & 1];
+    for (int x = threadIdx.x; x < len; x += blockDim.x) {
+      gd[s + x] = Xr[x];
+      if (HAS_TAGS) hd[s + x] = Yr[x];
+    }
+  }
+};
+
+template <typename K, int TB>
+__global__ void __launch_bounds__(kExecThreads) k_execute(ExecArgs E) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ unsigned long long s_task;
+  __shared__ unsigned long long sred[32];
+  unsigned long long comps = 0;
+  unsigned long long ntasks = E.met->n_tasks;
+  for (;;) {
+    if (threadIdx.x == 0) s_task = atomicAdd(&E.met->task_ctr, 1ull);
+    __syncthreads();
+    unsigned long long t = s_task;
+    if (t >= ntasks) break;
+    uint64_t rec = E.tasks[t];
+    uint32_t kind = task_kind(rec), id = task_id(rec), tile = task_tile(rec);
+    if (kind == kTaskMerge) Exec<K, TB>::merge_task(E, id, tile, smem, comps);
+    else if (kind == kTaskLeaf) Exec<K, TB>::leaf_task(E, id - E.leaf_base, tile);
+    else Exec<K, TB>::fuse_task(E, id, smem, comps);
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) atomicAdd(E.done + id, 1u);
+  }
+  unsigned long long s = block_sum(comps, sred);
+  if (threadIdx.x == 0 && s) atomicAdd(&E.met->comparisons, s);
+}
+
+}  // namespace rs

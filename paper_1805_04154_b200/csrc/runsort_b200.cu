@@ -1,0 +1,501 @@
+// runsort_b200.cu -- C ABI (include/runsort_b200.h) and launch orchestration.
+//
+// Pipeline for powersort (reference sorters.py:430-519), all on one stream,
+// no host synchronisation until the caller asks for the Metrics:
+//   1. k_scan_tables   pair-type bits + per-tile min-run candidate tables
+//   2. k_group_compose / k_group_entries / k_tile_entries / k_emit_leaves
+//                      -> leaf starts and natural-run info (sorters.py:462-470)
+//   3. k_keys_powers   midpoint keys, node powers (sorters.py:414-423)
+//   4. k_scan_*        left/right ancestor counts -> depths, max stack height
+//   5. k_tree          trie ranges, parents, children, spans
+//   6. k_classify / k_task_offsets / k_task_fill   executor task list
+//   7. k_execute       persistent dataflow executor (leaves + merges)
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/runsort_b200.h"
+#include "rs_chain.cuh"
+#include "rs_common.cuh"
+#include "rs_exec.cuh"
+#include "rs_tree.cuh"
+
+using namespace rs;
+
+namespace {
+
+thread_local std::string g_err;
+
+constexpr int kPhases = 4;
+struct Prof {
+  bool on = false;
+  bool created = false;
+  bool recorded = false;
+  cudaEvent_t ev[kPhases + 1];
+};
+thread_local Prof g_prof;
+
+void prof_mark(int i, cudaStream_t st) {
+  if (!g_prof.on) return;
+  if (!g_prof.created) {
+    for (auto& e : g_prof.ev) cudaEventCreate(&e);
+    g_prof.created = true;
+  }
+  cudaEventRecord(g_prof.ev[i], st);
+  if (i == kPhases) g_prof.recorded = true;
+}
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define RS_CUDA(call)                                                                    \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      return fail(RS_ECUDA, std::string(#call " failed: ") + cudaGetErrorString(e_));   \
+  } while (0)
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+struct Layout {
+  // inputs
+  int64_t n;
+  int w, kb, tb;
+  int tile, fcap;
+  // derived sizes
+  int64_t words, ntiles, ngroups, r_max, nchunks, max_tasks;
+  uint32_t leaf_base;
+  // offsets
+  size_t o_key1, o_tag1, o_ascw, o_tables, o_gtab, o_gentry, o_goff, o_tentry, o_toff;
+  size_t o_leaf_start, o_leaf_info, o_leaf_depth, o_K, o_P, o_la, o_ra, o_depth;
+  size_t o_node_a, o_node_b, o_node_s, o_node_e, o_parent, o_child, o_need, o_done;
+  size_t o_agg, o_tasks, o_met, total;
+};
+
+int exec_tile(int kb, int tb) {
+  if (kb == 4) return tb == 0 ? ExecCfg<int32_t, 0>::TILE : (tb == 4 ? ExecCfg<int32_t, 4>::TILE : ExecCfg<int32_t, 8>::TILE);
+  return tb == 0 ? ExecCfg<int64_t, 0>::TILE : (tb == 4 ? ExecCfg<int64_t, 4>::TILE : ExecCfg<int64_t, 8>::TILE);
+}
+int exec_fcap(int kb, int tb) {
+  if (kb == 4) return tb == 0 ? ExecCfg<int32_t, 0>::FCAP : (tb == 4 ? ExecCfg<int32_t, 4>::FCAP : ExecCfg<int32_t, 8>::FCAP);
+  return tb == 0 ? ExecCfg<int64_t, 0>::FCAP : (tb == 4 ? ExecCfg<int64_t, 4>::FCAP : ExecCfg<int64_t, 8>::FCAP);
+}
+
+Layout make_layout(int64_t n, int w, int kb, int tb) {
+  Layout L{};
+  L.n = n;
+  L.w = w;
+  L.kb = kb;
+  L.tb = tb;
+  L.tile = exec_tile(kb, tb);
+  L.fcap = exec_fcap(kb, tb);
+  L.words = (n + 31) / 32 + 2;
+  L.ntiles = (n + kChainT - 1) / kChainT;
+  L.ngroups = (L.ntiles + kChainGroup - 1) / kChainGroup;
+  int64_t minleaf = w > 2 ? w : 2;
+  L.r_max = n / minleaf + 2;
+  if (L.r_max > n + 1) L.r_max = n + 1;
+  L.leaf_base = (uint32_t)(L.r_max + 1);
+  L.nchunks = (L.r_max + kScanChunk - 1) / kScanChunk + 1;
+  int levels = 2;
+  for (int64_t x = n; x; x >>= 1) ++levels;
+  L.max_tasks = (int64_t)levels * (n / L.tile + n / L.fcap + 2) + 3 * L.r_max + 2 * (n / L.tile) + 16;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = align_up(off + bytes, 256);
+    return o;
+  };
+  L.o_key1 = take((size_t)n * kb + 64);
+  L.o_tag1 = take((size_t)n * tb + 64);
+  L.o_ascw = take((size_t)L.words * 4);
+  L.o_tables = take((size_t)L.ntiles * (w + 1) * 8);
+  L.o_gtab = take((size_t)L.ngroups * (w + 1) * 8);
+  L.o_gentry = take((size_t)L.ngroups * 4);
+  L.o_goff = take((size_t)L.ngroups * 8);
+  L.o_tentry = take((size_t)L.ntiles * 4);
+  L.o_toff = take((size_t)L.ntiles * 8);
+  L.o_leaf_start = take((size_t)(L.r_max + 1) * 8);
+  L.o_leaf_info = take((size_t)L.r_max * 4);
+  L.o_leaf_depth = take((size_t)L.r_max);
+  L.o_K = take((size_t)L.r_max * 8);
+  L.o_P = take((size_t)L.r_max);
+  L.o_la = take((size_t)L.r_max);
+  L.o_ra = take((size_t)L.r_max);
+  L.o_depth = take((size_t)L.r_max);
+  L.o_node_a = take((size_t)L.r_max * 4);
+  L.o_node_b = take((size_t)L.r_max * 4);
+  L.o_node_s = take((size_t)L.r_max * 8);
+  L.o_node_e = take((size_t)L.r_max * 8);
+  L.o_parent = take((size_t)(2 * L.r_max + 2) * 4);
+  L.o_child = take((size_t)(2 * L.r_max + 2) * 4);
+  L.o_need = take((size_t)(2 * L.r_max + 2) * 4);
+  L.o_done = take((size_t)(2 * L.r_max + 2) * 4);
+  L.o_agg = take((size_t)2 * L.nchunks * sizeof(MC));
+  L.o_tasks = take((size_t)L.max_tasks * 8);
+  L.o_met = take(sizeof(DevMetrics));
+  L.total = off + 256;
+  return L;
+}
+
+struct DevInfo {
+  int sms = 0;
+  bool init = false;
+};
+std::mutex g_mu;
+DevInfo g_dev[64];
+
+int device_sms(int* sms) {
+  int dev;
+  RS_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!g_dev[dev].init) {
+    RS_CUDA(cudaDeviceGetAttribute(&g_dev[dev].sms, cudaDevAttrMultiProcessorCount, dev));
+    g_dev[dev].init = true;
+  }
+  *sms = g_dev[dev].sms;
+  return RS_OK;
+}
+
+template <typename K, int TB>
+int exec_grid(int sms, int* grid, size_t* smem) {
+  static int occ[64] = {0};
+  int dev;
+  RS_CUDA(cudaGetDevice(&dev));
+  *smem = Exec<K, TB>::smem_bytes();
+  if (occ[dev] == 0) {
+    RS_CUDA(cudaFuncSetAttribute(k_execute<K, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem));
+    int o = 0;
+    RS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_execute<K, TB>, kExecThreads, *smem));
+    if (o < 1) return fail(RS_ECUDA, "executor does not fit on an SM");
+    occ[dev] = o;
+  }
+  *grid = sms * occ[dev];
+  return RS_OK;
+}
+
+template <typename K, int TB>
+int run_powersort(K* keys, void* tags, int64_t n, int w, int classic, unsigned char* ws, const Layout& L,
+                  cudaStream_t st) {
+  int sms;
+  if (int e = device_sms(&sms)) return e;
+  auto at = [&](size_t o) { return ws + o; };
+  DevMetrics* met = reinterpret_cast<DevMetrics*>(at(L.o_met));
+  uint32_t* ascw = reinterpret_cast<uint32_t*>(at(L.o_ascw));
+  uint2* tables = reinterpret_cast<uint2*>(at(L.o_tables));
+  uint2* gtab = reinterpret_cast<uint2*>(at(L.o_gtab));
+  uint32_t* gentry = reinterpret_cast<uint32_t*>(at(L.o_gentry));
+  uint64_t* goff = reinterpret_cast<uint64_t*>(at(L.o_goff));
+  uint32_t* tentry = reinterpret_cast<uint32_t*>(at(L.o_tentry));
+  uint64_t* toff = reinterpret_cast<uint64_t*>(at(L.o_toff));
+  pos_t* leaf_start = reinterpret_cast<pos_t*>(at(L.o_leaf_start));
+  uint32_t* leaf_info = reinterpret_cast<uint32_t*>(at(L.o_leaf_info));
+  uint8_t* leaf_depth = at(L.o_leaf_depth);
+  uint64_t* Kk = reinterpret_cast<uint64_t*>(at(L.o_K));
+  uint8_t* P = at(L.o_P);
+  uint8_t* la = at(L.o_la);
+  uint8_t* ra = at(L.o_ra);
+  uint8_t* depth = at(L.o_depth);
+  int32_t* node_a = reinterpret_cast<int32_t*>(at(L.o_node_a));
+  int32_t* node_b = reinterpret_cast<int32_t*>(at(L.o_node_b));
+  pos_t* node_s = reinterpret_cast<pos_t*>(at(L.o_node_s));
+  pos_t* node_e = reinterpret_cast<pos_t*>(at(L.o_node_e));
+  int32_t* parent = reinterpret_cast<int32_t*>(at(L.o_parent));
+  uint32_t* child = reinterpret_cast<uint32_t*>(at(L.o_child));
+  uint32_t* need = reinterpret_cast<uint32_t*>(at(L.o_need));
+  uint32_t* done = reinterpret_cast<uint32_t*>(at(L.o_done));
+  MC* agg = reinterpret_cast<MC*>(at(L.o_agg));
+  uint64_t* tasks = reinterpret_cast<uint64_t*>(at(L.o_tasks));
+
+  prof_mark(0, st);
+  RS_CUDA(cudaMemsetAsync(met, 0, sizeof(DevMetrics), st));
+  RS_CUDA(cudaMemsetAsync(done, 0, (size_t)(2 * L.r_max + 2) * 4, st));
+
+  // 1-2: leaves
+  int W1 = w + 1;
+  int maxw = kMaxWinWords(w);
+  size_t sm_scan = (size_t)maxw * 8 + (size_t)maxw * 2 + 64;
+  k_scan_tables<K><<<(unsigned)L.ntiles, 128, sm_scan, st>>>(keys, n, w, ascw, tables);
+  RS_CUDA(cudaGetLastError());
+  int batch = (int)((40 * 1024 - (size_t)W1 * 8) / ((size_t)W1 * 8));
+  if (batch < 1) batch = 1;
+  if (batch > kTableBatch) batch = kTableBatch;
+  int cthreads = W1 < 1024 ? ((W1 + 31) / 32) * 32 : 1024;
+  size_t sm_comp = (size_t)batch * W1 * 8 + (size_t)W1 * 8 + 64;
+  if (sm_comp > 48 * 1024) RS_CUDA(cudaFuncSetAttribute(k_group_compose, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_comp));
+  k_group_compose<<<(unsigned)L.ngroups, cthreads, sm_comp, st>>>(tables, L.ntiles, w, batch, gtab);
+  RS_CUDA(cudaGetLastError());
+  int gbatch = (int)(96 * 1024 / ((size_t)W1 * 8));
+  if (gbatch < 1) gbatch = 1;
+  if (gbatch > 4096) gbatch = 4096;
+  size_t sm_ge = (size_t)gbatch * W1 * 8;
+  if (sm_ge > 48 * 1024) RS_CUDA(cudaFuncSetAttribute(k_group_entries, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_ge));
+  k_group_entries<<<1, 1024, sm_ge, st>>>(gtab, L.ngroups, w, gbatch, gentry, goff, leaf_start, n, L.r_max, met);
+  RS_CUDA(cudaGetLastError());
+  int tbatch = (int)(48 * 1024 / ((size_t)W1 * 8));
+  if (tbatch < 1) tbatch = 1;
+  if (tbatch > kChainGroup) tbatch = kChainGroup;
+  k_tile_entries<<<(unsigned)L.ngroups, 256, (size_t)tbatch * W1 * 8, st>>>(tables, L.ntiles, w, tbatch, gentry,
+                                                                              goff, tentry, toff);
+  RS_CUDA(cudaGetLastError());
+  size_t sm_emit = (size_t)8 * (maxw * 2 + (maxw + 1) / 2 + 1) * 4;
+  k_emit_leaves<<<(unsigned)((L.ntiles + 7) / 8), 256, sm_emit, st>>>(ascw, n, w, L.ntiles, tentry, toff, L.r_max,
+                                                                      leaf_start, leaf_info);
+  RS_CUDA(cudaGetLastError());
+  prof_mark(1, st);
+
+  // 3-5: tree
+  int F = n <= ((int64_t)1 << 31) ? 32 : 63;
+  int64_t gs = (L.r_max + 255) / 256;
+  unsigned grid_r = (unsigned)(gs < (int64_t)sms * 8 ? gs : (int64_t)sms * 8);
+  if (grid_r == 0) grid_r = 1;
+  k_keys_powers<<<grid_r, 256, 0, st>>>(leaf_start, n, F, met, Kk, P);
+  RS_CUDA(cudaGetLastError());
+  int64_t gc = 2 * L.nchunks;
+  unsigned grid_c = (unsigned)(gc < (int64_t)sms * 4 ? gc : (int64_t)sms * 4);
+  k_scan_reduce<<<grid_c, kScanThreads, 0, st>>>(P, met, agg, L.nchunks);
+  RS_CUDA(cudaGetLastError());
+  k_scan_top<<<2, 1024, 0, st>>>(met, agg, L.nchunks);
+  RS_CUDA(cudaGetLastError());
+  k_scan_down<<<grid_c, kScanThreads, 0, st>>>(P, met, agg, L.nchunks, la, ra);
+  RS_CUDA(cudaGetLastError());
+  TreeArrays T{leaf_start, leaf_info, Kk, P, la, ra, depth, leaf_depth, node_a, node_b,
+               parent, child, node_s, node_e, L.leaf_base};
+  k_tree<<<grid_r, 256, 0, st>>>(T, F, met);
+  RS_CUDA(cudaGetLastError());
+  prof_mark(2, st);
+
+  // 6: tasks
+  ClassifyArgs CA{n, w, classic, L.fcap, L.tile, L.leaf_base, leaf_start, leaf_info, leaf_depth, depth,
+                  node_s, node_e, parent, need, tasks, met};
+  k_classify<<<grid_r, 256, 0, st>>>(CA);
+  RS_CUDA(cudaGetLastError());
+  k_task_offsets<<<1, 32, 0, st>>>(met);
+  RS_CUDA(cudaGetLastError());
+  k_task_fill<<<grid_r, 256, 0, st>>>(CA);
+  RS_CUDA(cudaGetLastError());
+  prof_mark(3, st);
+
+  // 7: execute
+  int grid;
+  size_t smem;
+  if (int e = exec_grid<K, TB>(sms, &grid, &smem)) return e;
+  ExecArgs E;
+  E.key[0] = keys;
+  E.key[1] = at(L.o_key1);
+  E.tag[0] = tags;
+  E.tag[1] = at(L.o_tag1);
+  E.n = n;
+  E.w = w;
+  E.classic = classic;
+  E.leaf_base = L.leaf_base;
+  E.leaf_start = leaf_start;
+  E.leaf_info = leaf_info;
+  E.leaf_depth = leaf_depth;
+  E.depth = depth;
+  E.node_a = node_a;
+  E.node_b = node_b;
+  E.node_s = node_s;
+  E.node_e = node_e;
+  E.child = child;
+  E.need = need;
+  E.done = done;
+  E.tasks = tasks;
+  E.met = met;
+  k_execute<K, TB><<<grid, kExecThreads, smem, st>>>(E);
+  RS_CUDA(cudaGetLastError());
+  prof_mark(4, st);
+  return RS_OK;
+}
+
+int validate(int algo, int key_dtype, int tag_bytes, int64_t n, int32_t w, int32_t merge_kind, int* kb) {
+  if (algo != RS_ALGO_POWERSORT && algo != RS_ALGO_PEEKSORT) return fail(RS_EINVAL, "unknown algorithm");
+  if (key_dtype == RS_KEY_I32) *kb = 4;
+  else if (key_dtype == RS_KEY_I64) *kb = 8;
+  else return fail(RS_EUNSUPPORTED, "keys must be int32 or int64");
+  if (tag_bytes != 0 && tag_bytes != 4 && tag_bytes != 8) return fail(RS_EUNSUPPORTED, "tags must be 4 or 8 bytes wide");
+  if (n < 0) return fail(RS_EINVAL, "n must be >= 0");
+  if (w < 1) return fail(RS_EINVAL, "min_run_len must be >= 1");
+  if (merge_kind != RS_MERGE_BITONIC && merge_kind != RS_MERGE_CLASSIC)
+    return fail(RS_EINVAL, "merge_kind must be one of ('bitonic', 'classic')");
+  if (w > exec_fcap(*kb, tag_bytes))
+    return fail(RS_EUNSUPPORTED, "min_run_len exceeds the device path's fused-subtree capacity");
+  if (n >= ((int64_t)1 << 40)) return fail(RS_EUNSUPPORTED, "n >= 2^40 is not supported");
+  if (algo == RS_ALGO_PEEKSORT) return fail(RS_EUNSUPPORTED, "peeksort device path not built yet");
+  return RS_OK;
+}
+
+int read_metrics(const Layout& L, unsigned char* ws, cudaStream_t st, rs_metrics* out) {
+  DevMetrics hm;
+  RS_CUDA(cudaMemcpyAsync(&hm, ws + L.o_met, sizeof(DevMetrics), cudaMemcpyDeviceToHost, st));
+  RS_CUDA(cudaStreamSynchronize(st));
+  if (hm.error) return fail(RS_EINVARIANT, "device invariant failure (leaf count exceeded bound)");
+  if (out) {
+    out->merge_cost = hm.merge_cost;
+    out->comparisons = hm.comparisons;
+    out->runs_detected = hm.runs_detected;
+    out->max_stack_height = hm.max_stack_height;
+  }
+  return RS_OK;
+}
+
+int export_tree(const Layout& L, unsigned char* ws, cudaStream_t st, rs_tree* tree) {
+  DevMetrics hm;
+  RS_CUDA(cudaMemcpyAsync(&hm, ws + L.o_met, sizeof(DevMetrics), cudaMemcpyDeviceToHost, st));
+  RS_CUDA(cudaStreamSynchronize(st));
+  int64_t r = (int64_t)hm.n_leaves;
+  tree->n_leaves = r;
+  if (r > tree->capacity) return fail(RS_EINVAL, "tree capacity too small");
+  std::vector<int64_t> starts(r + 1);
+  RS_CUDA(cudaMemcpyAsync(starts.data(), ws + L.o_leaf_start, (r + 1) * 8, cudaMemcpyDeviceToHost, st));
+  std::vector<uint8_t> P(r), la(r), ra(r);
+  if (r > 1) {
+    RS_CUDA(cudaMemcpyAsync(P.data(), ws + L.o_P, r, cudaMemcpyDeviceToHost, st));
+    RS_CUDA(cudaMemcpyAsync(la.data(), ws + L.o_la, r, cudaMemcpyDeviceToHost, st));
+    RS_CUDA(cudaMemcpyAsync(ra.data(), ws + L.o_ra, r, cudaMemcpyDeviceToHost, st));
+  }
+  RS_CUDA(cudaStreamSynchronize(st));
+  for (int64_t i = 0; i < r; ++i)
+    if (tree->leaf_len) tree->leaf_len[i] = starts[i + 1] - starts[i];
+  for (int64_t j = 1; j < r; ++j) {
+    if (tree->node_power) tree->node_power[j - 1] = P[j];
+    if (tree->node_depth) tree->node_depth[j - 1] = (uint8_t)(la[j] + ra[j]);
+  }
+  return RS_OK;
+}
+
+template <typename K>
+int dispatch_tags(K* keys, int tb, void* tags, int64_t n, int w, int classic, unsigned char* ws, const Layout& L,
+                  cudaStream_t st) {
+  if (tb == 0) return run_powersort<K, 0>(keys, nullptr, n, w, classic, ws, L, st);
+  if (tb == 4) return run_powersort<K, 4>(keys, tags, n, w, classic, ws, L, st);
+  return run_powersort<K, 8>(keys, tags, n, w, classic, ws, L, st);
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t rs_workspace_bytes(int algo, int key_dtype, int tag_bytes, int64_t n, int32_t min_run_len) {
+  (void)algo;
+  int kb = key_dtype == RS_KEY_I64 ? 8 : 4;
+  if (n <= 1) return 256;
+  if (min_run_len < 1) min_run_len = 1;
+  return make_layout(n, min_run_len, kb, tag_bytes).total;
+}
+
+int rs_sort(int algo, int key_dtype, void* keys, int tag_bytes, void* tags, int64_t n, int32_t min_run_len,
+            int32_t merge_kind, void* workspace, size_t ws_bytes, void* stream, rs_metrics* out, rs_tree* tree) {
+  int kb;
+  if (int e = validate(algo, key_dtype, tag_bytes, n, min_run_len, merge_kind, &kb)) return e;
+  if (tags == nullptr) tag_bytes = 0;
+  if (n <= 1) {  // sorters.py:445-450
+    if (out) { memset(out, 0, sizeof(*out)); out->runs_detected = (uint64_t)n; }
+    if (tree) {
+      tree->n_leaves = n;
+      if (n == 1 && tree->capacity >= 1 && tree->leaf_len) tree->leaf_len[0] = 1;
+    }
+    return RS_OK;
+  }
+  if (!keys || !workspace) return fail(RS_EINVAL, "null keys or workspace");
+  Layout L = make_layout(n, min_run_len, kb, tag_bytes);
+  if (ws_bytes < L.total) return fail(RS_ENOMEM, "workspace too small");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  unsigned char* ws = reinterpret_cast<unsigned char*>(workspace);
+  int e;
+  if (kb == 4) e = dispatch_tags<int32_t>(reinterpret_cast<int32_t*>(keys), tag_bytes, tags, n, min_run_len,
+                                        merge_kind, ws, L, st);
+  else e = dispatch_tags<int64_t>(reinterpret_cast<int64_t*>(keys), tag_bytes, tags, n, min_run_len, merge_kind,
+                                  ws, L, st);
+  if (e) return e;
+  if (out || tree) {
+    if ((e = read_metrics(L, ws, st, out))) return e;
+    if (tree && (e = export_tree(L, ws, st, tree))) return e;
+  }
+  return RS_OK;
+}
+
+int rs_fetch_metrics(int algo, int key_dtype, int tag_bytes, int64_t n, int32_t min_run_len, void* workspace,
+                     void* stream, rs_metrics* out) {
+  (void)algo;
+  if (n <= 1) {
+    if (out) { memset(out, 0, sizeof(*out)); out->runs_detected = (uint64_t)n; }
+    return RS_OK;
+  }
+  int kb = key_dtype == RS_KEY_I64 ? 8 : 4;
+  Layout L = make_layout(n, min_run_len, kb, tag_bytes);
+  return read_metrics(L, reinterpret_cast<unsigned char*>(workspace), reinterpret_cast<cudaStream_t>(stream), out);
+}
+
+int rs_sort_host(int algo, int key_dtype, void* keys, int tag_bytes, void* tags, int64_t n, int32_t min_run_len,
+                 int32_t merge_kind, rs_metrics* out, rs_tree* tree) {
+  int kb;
+  if (int e = validate(algo, key_dtype, tag_bytes, n, min_run_len, merge_kind, &kb)) return e;
+  if (tags == nullptr) tag_bytes = 0;
+  if (n <= 1) return rs_sort(algo, key_dtype, keys, tag_bytes, tags, n, min_run_len, merge_kind, nullptr, 0,
+                             nullptr, out, tree);
+  size_t ws = rs_workspace_bytes(algo, key_dtype, tag_bytes, n, min_run_len);
+  void *dk = nullptr, *dt = nullptr, *dws = nullptr;
+  cudaStream_t st;
+  RS_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  int rc = RS_OK;
+  do {
+    if (cudaMallocAsync(&dk, (size_t)n * kb + 64, st) != cudaSuccess ||
+        (tag_bytes && cudaMallocAsync(&dt, (size_t)n * tag_bytes + 64, st) != cudaSuccess) ||
+        cudaMallocAsync(&dws, ws, st) != cudaSuccess) {
+      rc = fail(RS_ENOMEM, "device allocation failed");
+      break;
+    }
+    if (cudaMemcpyAsync(dk, keys, (size_t)n * kb, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+        (tag_bytes && cudaMemcpyAsync(dt, tags, (size_t)n * tag_bytes, cudaMemcpyHostToDevice, st) != cudaSuccess)) {
+      rc = fail(RS_ECUDA, "host-to-device copy failed");
+      break;
+    }
+    rc = rs_sort(algo, key_dtype, dk, tag_bytes, dt, n, min_run_len, merge_kind, dws, ws, st, out, tree);
+    if (rc) break;
+    if (cudaMemcpyAsync(keys, dk, (size_t)n * kb, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        (tag_bytes && cudaMemcpyAsync(tags, dt, (size_t)n * tag_bytes, cudaMemcpyDeviceToHost, st) != cudaSuccess) ||
+        cudaStreamSynchronize(st) != cudaSuccess) {
+      rc = fail(RS_ECUDA, "device-to-host copy failed");
+      break;
+    }
+  } while (0);
+  if (dk) cudaFreeAsync(dk, st);
+  if (dt) cudaFreeAsync(dt, st);
+  if (dws) cudaFreeAsync(dws, st);
+  cudaStreamSynchronize(st);
+  cudaStreamDestroy(st);
+  return rc;
+}
+
+int32_t rs_max_min_run_len(int key_dtype, int tag_bytes) {
+  return exec_fcap(key_dtype == RS_KEY_I64 ? 8 : 4, tag_bytes);
+}
+
+int rs_profile(int enable) {
+  g_prof.on = enable != 0;
+  g_prof.recorded = false;
+  return RS_OK;
+}
+
+int rs_profile_read(double* ms, int cap) {
+  if (!g_prof.recorded) return 0;
+  if (cudaEventSynchronize(g_prof.ev[kPhases]) != cudaSuccess) return 0;
+  int k = 0;
+  for (int i = 0; i < kPhases && i < cap; ++i) {
+    float t = 0.f;
+    cudaEventElapsedTime(&t, g_prof.ev[i], g_prof.ev[i + 1]);
+    ms[k++] = t;
+  }
+  return k;
+}
+
+const char* rs_last_error(void) { return g_err.c_str(); }
+
+int rs_version(void) { return 100; }
+
+}  // extern "C"

@@ -1,0 +1,298 @@
+"""Drop-in powersort / peeksort entry points backed by the B200 CUDA path.
+
+Mirrors reference sorters.py (calling convention :3-8, SortConfig :63-87,
+peeksort :146-361, node powers :368-423, powersort :430-519, SORTERS
+:671-678).  The keys are sorted in place, the optional ``tags`` payload moves
+identically, and a ``Metrics`` is returned (created if not passed, otherwise
+accumulated into), with the reference's exact counter values.
+
+Inputs: numpy arrays (staged through the GPU and written back in place) or
+torch tensors (CUDA tensors are sorted in place on their device).  Keys of
+int32/int64 are sorted natively; narrower integers are widened and unsigned
+ones sign-flipped to an order-preserving signed type.  There is no CPU
+fallback: without a CUDA device or the built library, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from .opttree import MergeLeaf, tree_from_depths
+from .runcore import Metrics
+
+__all__ = [
+    "SortConfig",
+    "peeksort",
+    "powersort",
+    "node_power_def",
+    "node_power_bitwise",
+    "SORTERS",
+]
+
+MERGE_KINDS = ("bitonic", "classic")
+
+
+@dataclass(frozen=True)
+class SortConfig:
+    """Shared sorter knobs (reference sorters.py:63-87).
+
+    min_run_len   runs shorter than this are extended by insertion sort
+                  (powersort) or recursion bottoms out in insertion sort
+                  (peeksort); 1 disables the cutoff entirely.
+    merge_kind    "bitonic" (exactly m+n comparisons) or "classic"
+                  (two-pointer, at most m+n-1).
+    record_tree   record the merge tree into Metrics.merge_tree.
+    alpha         growth ratio for the alpha-stack/alpha-merge rules.
+    """
+
+    min_run_len: int = 24
+    merge_kind: str = "bitonic"
+    record_tree: bool = False
+    alpha: float = 2.0
+
+    def __post_init__(self) -> None:
+        if self.min_run_len < 1:
+            raise ValueError("min_run_len must be >= 1")
+        if self.merge_kind not in MERGE_KINDS:
+            raise ValueError(f"merge_kind must be one of {MERGE_KINDS}")
+        if not self.alpha > 1.0:
+            raise ValueError("alpha must be > 1")
+
+
+# ---------------------------------------------------------------------------
+# Node powers (host integer functions; reference sorters.py:368-411)
+
+
+def _validate_power_args(s1: int, e1: int, s2: int, e2: int, n: int) -> None:
+    if not (1 <= s1 <= e1 < s2 <= e2 <= n):
+        raise ValueError(
+            f"invalid run positions: need 1 <= s1 <= e1 < s2 <= e2 <= n, "
+            f"got ({s1}, {e1}, {s2}, {e2}, {n})"
+        )
+
+
+def node_power_def(s1: int, e1: int, s2: int, e2: int, n: int) -> int:
+    """Smallest l >= 1 with the normalized run midpoints in different cells of
+    the 2**-l grid (1-based runs, exact integers, any n)."""
+    _validate_power_args(s1, e1, s2, e2, n)
+    a2 = s1 + e1 - 1  # 2n * midpoint of run 1 (1-based)
+    b2 = s2 + e2 - 1
+    two_n = 2 * n
+    level = 1
+    while (a2 << level) // two_n == (b2 << level) // two_n:
+        level += 1
+    return level
+
+
+def node_power_bitwise(s1: int, e1: int, s2: int, e2: int, n: int) -> int:
+    """Loop-free node power via 31-bit fixed point (n < 2**31 only)."""
+    _validate_power_args(s1, e1, s2, e2, n)
+    if n >= 1 << 31:
+        raise ValueError("bitwise node power supports n < 2**31 only")
+    afix = ((s1 + e1 - 1) << 31) // (2 * n)
+    bfix = ((s2 + e2 - 1) << 31) // (2 * n)
+    return 32 - (afix ^ bfix).bit_length()
+
+
+# ---------------------------------------------------------------------------
+# Staging
+
+
+def _torch():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise RuntimeError("no CUDA device visible: the B200 sort path has no CPU fallback")
+    return torch
+
+
+_SIGNED = {np.dtype(np.int32): _lib.RS_KEY_I32, np.dtype(np.int64): _lib.RS_KEY_I64}
+
+
+class _Staged:
+    """A contiguous CUDA int32/int64 view of the caller's keys or tags, plus
+    the write-back needed to land the result in the caller's object."""
+
+    def __init__(self, obj, is_keys: bool):
+        torch = _torch()
+        self.obj = obj
+        self.dev_t = None
+        self.writeback = None
+        self.flip = None
+        if isinstance(obj, torch.Tensor):
+            self.is_torch = True
+            t = obj
+            npdt = np.dtype(str(t.dtype).replace("torch.", "")) if t.dtype not in (torch.bool,) else np.dtype(bool)
+        else:
+            self.is_torch = False
+            arr = np.asarray(obj)
+            if arr.ndim != 1:
+                raise ValueError("expected a one-dimensional array")
+            npdt = arr.dtype
+        self.n = int(obj.shape[0]) if hasattr(obj, "shape") else len(obj)
+        if is_keys:
+            self.kind, self.code = self._key_plan(npdt)
+        else:
+            if npdt.itemsize not in (4, 8):
+                raise NotImplementedError("tags must have a 4- or 8-byte dtype")
+            self.kind, self.code = "raw", npdt.itemsize
+        dev = torch.device("cuda", torch.cuda.current_device())
+        stream = torch.cuda.current_stream(dev)
+        if self.is_torch:
+            t = obj
+            if t.dim() != 1:
+                raise ValueError("expected a one-dimensional tensor")
+            base = t
+            if t.device.type != "cuda":
+                d = t.to(dev, non_blocking=t.is_pinned())
+            elif not t.is_contiguous():
+                d = t.contiguous()
+            else:
+                d = t
+        else:
+            arr = np.ascontiguousarray(np.asarray(obj))
+            d = torch.from_numpy(arr).to(dev)
+            base = None
+        d = self._to_work(d)
+        self.dev_t = d
+        self.base = base
+        self.stream = stream
+
+    def _key_plan(self, npdt):
+        if npdt in _SIGNED:
+            return "native", _SIGNED[npdt]
+        if npdt in (np.dtype(np.int8), np.dtype(np.int16), np.dtype(np.uint8), np.dtype(np.uint16),
+                    np.dtype(bool)):
+            return "widen", _lib.RS_KEY_I32
+        if npdt == np.dtype(np.uint32):
+            return "flip32", _lib.RS_KEY_I32
+        if npdt == np.dtype(np.uint64):
+            return "flip64", _lib.RS_KEY_I64
+        raise NotImplementedError(f"keys of dtype {npdt} are not supported on the device path "
+                                  "(integers only)")
+
+    def _to_work(self, d):
+        torch = _torch()
+        if self.kind == "raw":
+            if d.element_size() == 4 and d.dtype != torch.int32:
+                d = d.view(torch.int32)
+            elif d.element_size() == 8 and d.dtype != torch.int64:
+                d = d.view(torch.int64)
+            return d
+        if self.kind == "native":
+            return d
+        if self.kind == "widen":
+            self.orig_dtype = d.dtype
+            return d.to(torch.int32)
+        if self.kind == "flip32":
+            return d.view(torch.int32) ^ torch.tensor(-(1 << 31), dtype=torch.int32, device=d.device)
+        if self.kind == "flip64":
+            return d.view(torch.int64) ^ torch.tensor(-(1 << 63), dtype=torch.int64, device=d.device)
+        raise AssertionError(self.kind)
+
+    def finish(self):
+        torch = _torch()
+        d = self.dev_t
+        if self.kind == "widen":
+            d = d.to(self.orig_dtype)
+        elif self.kind == "flip32":
+            d = (d ^ torch.tensor(-(1 << 31), dtype=torch.int32, device=d.device)).view(torch.uint32)
+        elif self.kind == "flip64":
+            d = (d ^ torch.tensor(-(1 << 63), dtype=torch.int64, device=d.device)).view(torch.uint64)
+        if self.is_torch:
+            t = self.obj
+            if d.data_ptr() != t.data_ptr() or d.dtype != t.dtype:
+                if d.dtype != t.dtype:
+                    d = d.view(t.dtype) if d.element_size() == t.element_size() else d.to(t.dtype)
+                t.copy_(d, non_blocking=t.device.type == "cpu" and t.is_pinned())
+        else:
+            host = d.cpu().numpy()
+            arr = self.obj
+            if host.dtype != arr.dtype:
+                host = host.view(arr.dtype) if host.itemsize == arr.dtype.itemsize else host.astype(arr.dtype)
+            arr[...] = host
+
+
+def _device_sort(algo: int, a, cfg: SortConfig, metrics: Metrics, tags) -> Metrics:
+    L = _lib.lib()
+    torch = _torch()
+    keys = _Staged(a, True)
+    n = keys.n
+    tg = None
+    if tags is not None:
+        tg = _Staged(tags, False)
+        if tg.n != n:
+            raise ValueError("tags must have the same length as the keys")
+    w = int(cfg.min_run_len)
+    kind = _lib.RS_MERGE_CLASSIC if cfg.merge_kind == "classic" else _lib.RS_MERGE_BITONIC
+    tb = tg.code if tg is not None else 0
+    ws_bytes = L.rs_workspace_bytes(algo, keys.code, tb, n, w)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=keys.dev_t.device)
+    out = _lib.RsMetrics()
+    tree = None
+    bufs = None
+    if cfg.record_tree and n > 1:
+        cap = n
+        bufs = (np.zeros(cap, dtype=np.int64), np.zeros(cap, dtype=np.uint8), np.zeros(cap, dtype=np.uint8))
+        tree = _lib.RsTree(cap, 0, bufs[0].ctypes.data, bufs[1].ctypes.data, bufs[2].ctypes.data)
+    rc = L.rs_sort(algo, keys.code, keys.dev_t.data_ptr(), tb,
+                   tg.dev_t.data_ptr() if tg is not None else None, n, w, kind,
+                   ws.data_ptr(), ws_bytes, keys.stream.cuda_stream, ctypes.byref(out),
+                   ctypes.byref(tree) if tree is not None else None)
+    _lib.check(rc)
+    keys.finish()
+    if tg is not None:
+        tg.finish()
+    if keys.is_torch and keys.obj.device.type == "cpu":
+        keys.stream.synchronize()
+    metrics.merge_cost += int(out.merge_cost)
+    metrics.comparisons += int(out.comparisons)
+    if algo == _lib.RS_ALGO_PEEKSORT:
+        metrics.runs_detected = int(out.runs_detected)  # sorters.py:358 assigns
+    else:
+        metrics.runs_detected += int(out.runs_detected)  # sorters.py:464 accumulates
+        if int(out.max_stack_height) > metrics.max_stack_height:
+            metrics.max_stack_height = int(out.max_stack_height)
+    if tree is not None:
+        r = int(tree.n_leaves)
+        lens = bufs[0][:r]
+        depths = bufs[2][: r - 1]
+        powers = bufs[1][: r - 1] if algo == _lib.RS_ALGO_POWERSORT else None
+        metrics.merge_tree = tree_from_depths(lens, depths, powers)
+    return metrics
+
+
+def _entry(algo, a, cfg, metrics, tags):
+    cfg = cfg or SortConfig()
+    metrics = metrics or Metrics()
+    n = len(a)
+    if n <= 1:  # sorters.py:445-450 / :168-173
+        metrics.runs_detected = n
+        if cfg.record_tree and n == 1:
+            metrics.merge_tree = MergeLeaf(0, 1)
+        return metrics
+    return _device_sort(algo, a, cfg, metrics, tags)
+
+
+def powersort(a, cfg: Optional[SortConfig] = None, metrics: Optional[Metrics] = None,
+              tags=None) -> Metrics:
+    """One-pass stack-based natural mergesort driven by node powers
+    (reference sorters.py:430-519), executed on the GPU."""
+    return _entry(_lib.RS_ALGO_POWERSORT, a, cfg, metrics, tags)
+
+
+def peeksort(a, cfg: Optional[SortConfig] = None, metrics: Optional[Metrics] = None,
+             tags=None) -> Metrics:
+    """Top-down natural mergesort splitting at the run boundary closest to the
+    midpoint (reference sorters.py:146-361), executed on the GPU."""
+    return _entry(_lib.RS_ALGO_PEEKSORT, a, cfg, metrics, tags)
+
+
+SORTERS = {
+    "peeksort": peeksort,
+    "powersort": powersort,
+}
