@@ -40,7 +40,7 @@ sys.path.insert(0, REPO)
 
 PEAKS = os.path.join(REPO, "MEASURED_PEAKS.json")
 FALLBACK_HBM_GBS = 6650.0
-KERNELS_PER_SORT = 14  # our launches per powersort (see csrc/runsort_b200.cu run_powersort)
+KERNELS_PER_SORT = 16  # our launches per powersort (see csrc/runsort_b200.cu run_powersort)
 METRIC = "powersort keys/s at n=1e7 int32 random-runs; % of HBM roofline; 1/2/4/8 GPU"
 
 

@@ -101,6 +101,11 @@ int rs_sort_host(int algo, int key_dtype, void* keys, int tag_bytes, void* tags,
 int rs_profile(int enable);
 int rs_profile_read(double* ms, int cap);
 
+/* Diagnostics: copy up to `cap` executor cycle counters of the last rs_sort
+ * that used `workspace` (nonzero only in an RS_INSTR build).  Synchronizes. */
+int rs_debug_counters(int key_dtype, int tag_bytes, int64_t n, int32_t min_run_len, void* workspace,
+                      uint64_t* out, int cap);
+
 /* Largest min_run_len the device path accepts for this element type. */
 int32_t rs_max_min_run_len(int key_dtype, int tag_bytes);
 

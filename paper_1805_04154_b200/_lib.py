@@ -9,7 +9,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "librunsort_b200.so")
+LIB_PATH = os.environ.get("RS_LIB") or os.path.join(HERE, "librunsort_b200.so")
 
 RS_OK, RS_EINVAL, RS_EINVARIANT, RS_ENOMEM, RS_ECUDA, RS_EUNSUPPORTED = range(6)
 RS_ALGO_POWERSORT, RS_ALGO_PEEKSORT = 0, 1
@@ -18,7 +18,7 @@ RS_MERGE_BITONIC, RS_MERGE_CLASSIC = 0, 1
 
 # every symbol include/runsort_b200.h declares
 EXPORTS = ("rs_workspace_bytes", "rs_sort", "rs_fetch_metrics", "rs_sort_host", "rs_profile",
-           "rs_profile_read", "rs_max_min_run_len", "rs_last_error", "rs_version")
+           "rs_profile_read", "rs_debug_counters", "rs_max_min_run_len", "rs_last_error", "rs_version")
 
 
 class RsMetrics(ctypes.Structure):
@@ -60,6 +60,9 @@ def lib():
         L.rs_profile.argtypes = [ctypes.c_int]
         L.rs_profile_read.restype = ctypes.c_int
         L.rs_profile_read.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.c_int]
+        L.rs_debug_counters.restype = ctypes.c_int
+        L.rs_debug_counters.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p,
+                                        ctypes.POINTER(ctypes.c_uint64), ctypes.c_int]
         L.rs_max_min_run_len.restype = ctypes.c_int32
         L.rs_max_min_run_len.argtypes = [ctypes.c_int, ctypes.c_int]
         L.rs_last_error.restype = ctypes.c_char_p

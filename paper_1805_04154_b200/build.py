@@ -28,18 +28,19 @@ def needs_build() -> bool:
     return any(os.path.getmtime(s) > t for s in sources() + [hdr])
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, instr: bool = False) -> str:
+    out = LIB.replace(".so", "_instr.so") if instr else LIB
+    if not instr and not force and not needs_build():
         return LIB
-    cmd = [NVCC, *FLAGS, "-o", LIB + ".tmp", os.path.join(CSRC, "runsort_b200.cu")]
+    cmd = [NVCC, *FLAGS, *(["-DRS_INSTR"] if instr else []), "-o", out + ".tmp",
+           os.path.join(CSRC, "runsort_b200.cu")]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB)
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, instr="--instr" in sys.argv))

@@ -100,17 +100,29 @@ __global__ void __launch_bounds__(128) k_scan_tables(const K* __restrict__ a, po
   uint16_t* nz = reinterpret_cast<uint16_t*>(bw + nwords);
   int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   int64_t own0 = t0 >> 5, own1 = (t1 + 31) >> 5;
-  for (int qi = wid; qi < nwords; qi += nw) {
-    int64_t q = q0 + qi;
-    pos_t k = 32 * q + lane;
-    K v = k < n ? a[k] : K(0);
-    K nx = __shfl_down_sync(0xffffffffu, v, 1);
-    if (lane == 31) nx = (k + 1 < n) ? a[k + 1] : K(0);
-    bool bit = (k < n - 1) && (v <= nx);
-    uint32_t word = __ballot_sync(0xffffffffu, bit);
-    if (lane == 0) {
-      asc[qi] = word;
-      if (q >= own0 && q < own1) ascw[q] = word;
+  // each warp handles runs of 8 consecutive words: 8 independent loads per lane
+  constexpr int U = 8;
+  for (int qb = wid * U; qb < nwords; qb += nw * U) {
+    K v[U + 1];
+#pragma unroll
+    for (int u = 0; u <= U; ++u) {
+      pos_t k = 32 * (q0 + qb + u) + lane;
+      v[u] = (qb + u <= nwords && k < n && (u < U || lane == 0)) ? __ldcg(a + k) : K(0);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      int qi = qb + u;
+      K nx = __shfl_down_sync(0xffffffffu, v[u], 1);
+      K first_next = __shfl_sync(0xffffffffu, v[u + 1], 0);
+      if (lane == 31) nx = first_next;
+      pos_t k = 32 * (q0 + qi) + lane;
+      bool bit = qi < nwords && (k < n - 1) && (v[u] <= nx);
+      uint32_t word = __ballot_sync(0xffffffffu, bit);
+      if (lane == 0 && qi < nwords) {
+        int64_t q = q0 + qi;
+        asc[qi] = word;
+        if (q >= own0 && q < own1) ascw[q] = word;
+      }
     }
   }
   __syncthreads();
@@ -154,7 +166,7 @@ __global__ void k_group_compose(const uint2* __restrict__ tables, int64_t ntiles
   for (int64_t kb = k0; kb < k1; kb += batch) {
     int nb = int((k1 - kb) < batch ? (k1 - kb) : batch);
     __syncthreads();
-    for (int x = threadIdx.x; x < nb * W1; x += blockDim.x) stab[x] = tables[kb * W1 + x];
+    copy_g2s(stab, tables + kb * W1, nb * W1, threadIdx.x, blockDim.x);
     __syncthreads();
     for (int c = threadIdx.x; c < W1; c += blockDim.x) {
       uint32_t e = cur[c], s = cnt[c];
@@ -185,7 +197,7 @@ __global__ void k_group_entries(const uint2* __restrict__ gtab, int64_t ngroups,
   for (int64_t gb = 0; gb < ngroups; gb += batch) {
     int nb = int((ngroups - gb) < batch ? (ngroups - gb) : batch);
     __syncthreads();
-    for (int x = threadIdx.x; x < nb * W1; x += blockDim.x) stab[x] = gtab[gb * W1 + x];
+    copy_g2s(stab, gtab + gb * W1, nb * W1, threadIdx.x, blockDim.x);
     __syncthreads();
     if (threadIdx.x == 0) {
       uint32_t e = s_e;
@@ -226,7 +238,7 @@ __global__ void k_tile_entries(const uint2* __restrict__ tables, int64_t ntiles,
   for (int64_t kb = k0; kb < k1; kb += batch) {
     int nb = int((k1 - kb) < batch ? (k1 - kb) : batch);
     __syncthreads();
-    for (int x = threadIdx.x; x < nb * W1; x += blockDim.x) stab[x] = tables[kb * W1 + x];
+    copy_g2s(stab, tables + kb * W1, nb * W1, threadIdx.x, blockDim.x);
     __syncthreads();
     if (threadIdx.x == 0) {
       uint32_t e = s_e;

@@ -42,7 +42,8 @@ struct DevMetrics {
   unsigned long long error;       // nonzero: invariant failure (maps to AssertionError)
   unsigned long long n_leaves;    // r
   unsigned long long n_tasks;     // total executor tasks
-  unsigned long long task_ctr;    // executor claim counter
+  unsigned long long task_ctr;    // merge-executor claim counter (starts at phaseA)
+  unsigned long long task_ctr_A;  // phase-A claim counter
   unsigned long long phaseA;      // number of phase-A tasks (fuse + leaf tiles)
   unsigned long long cursorA;     // phase-A slot allocator
   unsigned long long max_depth;   // deepest internal node
@@ -50,12 +51,47 @@ struct DevMetrics {
   unsigned long long depth_tiles[kMaxDepth];
   unsigned long long depth_base[kMaxDepth];
   unsigned long long depth_cursor[kMaxDepth];
+  unsigned long long instr[8];  // RS_INSTR builds: cycle counters (see rs_merge.cuh)
+  unsigned long long depth_wait[kMaxDepth];  // RS_INSTR: producer dependency-wait cycles per depth
 };
+
+#ifdef RS_INSTR
+#define RS_T0(v) long long v = clock64()
+#define RS_ACC(met, i, v) atomicAdd(&(met)->instr[i], (unsigned long long)(clock64() - (v)))
+#else
+#define RS_T0(v)
+#define RS_ACC(met, i, v)
+#endif
 
 __device__ __forceinline__ int bitlen64(uint64_t x) { return x ? 64 - __clzll((long long)x) : 0; }
 
 template <typename T>
 __device__ __forceinline__ T ldcg(const T* p) { return __ldcg(p); }
+
+// Copy `len` elements global -> shared with U independent loads in flight per thread.
+template <typename T, int U = 8>
+__device__ __forceinline__ void copy_g2s(T* __restrict__ dst, const T* __restrict__ src, int len, int tid,
+                                         int nthreads) {
+  for (int base = tid; base < len; base += nthreads * U) {
+    T v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      int x = base + u * nthreads;
+      if (x < len) v[u] = __ldcg(src + x);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      int x = base + u * nthreads;
+      if (x < len) dst[x] = v[u];
+    }
+  }
+}
+
+// Publish completion of a CTA's global writes: call after a barrier that all
+// writers passed; one thread does release-fence + relaxed add (CUTLASS-style).
+__device__ __forceinline__ void release_add_u32(uint32_t* p, uint32_t v) {
+  asm volatile("fence.acq_rel.gpu;\n\tred.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
 __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
   uint32_t v;

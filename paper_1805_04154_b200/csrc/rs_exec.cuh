@@ -76,7 +76,9 @@ struct ClassifyArgs {
   int w;
   int classic;
   int fcap;
-  int tile;
+  int tile;   // leaf-tile granularity (phase A)
+  int mtile;  // merge-tile granularity (merge executor)
+  int msuper; // merge tiles per merge task
   uint32_t leaf_base;
   const pos_t* leaf_start;
   const uint32_t* leaf_info;
@@ -105,18 +107,29 @@ __device__ __forceinline__ int classify_leaf(const ClassifyArgs& A, int64_t i, i
   *tiles = leaf_tiles(len, mode, A.tile);
   return *tiles > 0 ? 2 : 0;
 }
-__device__ __forceinline__ int classify_node(const ClassifyArgs& A, int64_t j, int64_t* tiles) {
+// Big nodes: *tiles = merge tiles (the node's completion count), *tasks = super tasks.
+__device__ __forceinline__ int classify_node(const ClassifyArgs& A, int64_t j, int64_t* tiles, int64_t* tasks) {
   pos_t span = A.node_e[j] - A.node_s[j];
   *tiles = 0;
+  *tasks = 0;
   if (span <= A.fcap) return parent_small(A, A.parent[j]) ? 0 : 1;
-  *tiles = (span + A.tile - 1) / A.tile;
+  *tiles = (span + A.mtile - 1) / A.mtile;
+  *tasks = (*tiles + A.msuper - 1) / A.msuper;
   return 2;
 }
 
-__global__ void k_classify(ClassifyArgs A) {
+// Chunks of kOrdChunk elements (leaf i and boundary j = i).  Merge tasks are
+// ordered by depth (deepest first) and, within a depth, by position, so a
+// node's tasks are claimed after the wave of its children's tasks has passed.
+constexpr int kOrdChunk = 1024;
+
+// Element-parallel: leaf i and boundary j = i per thread.  Big nodes add their
+// task count to their (chunk, depth) cell for the ordered fill.
+__global__ void __launch_bounds__(256) k_classify(ClassifyArgs A, uint32_t* __restrict__ chunk_depth) {
   __shared__ unsigned long long sred[32];
   int64_t r = (int64_t)A.met->n_leaves;
   unsigned long long comps = 0, mcost = 0, cntA = 0;
+  unsigned maxd = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < r; i += (int64_t)gridDim.x * blockDim.x) {
     // leaf: detection comparisons (runcore.py:154/157 closed form)
     pos_t s0 = A.leaf_start[i], len = A.leaf_start[i + 1] - s0;
@@ -135,15 +148,15 @@ __global__ void k_classify(ClassifyArgs A) {
       pos_t span = A.node_e[i] - A.node_s[i];
       mcost += span;
       if (!A.classic) comps += span;  // runcore.py:299-301
-      int64_t tn;
-      int cn = classify_node(A, i, &tn);
+      int64_t tn, tk;
+      int cn = classify_node(A, i, &tn, &tk);
       if (cn == 1) { A.need[i] = 1; cntA += 1; }
       else if (cn == 2) {
         A.need[i] = (uint32_t)tn;
         int d = A.depth[i];
-        atomicAdd(&A.met->depth_tiles[d], (unsigned long long)tn);
-        atomicMax(&A.met->max_depth, (unsigned long long)d);
-        atomicAdd(&A.met->n_merge_tasks, (unsigned long long)tn);
+        atomicAdd(&chunk_depth[(i / kOrdChunk) * kMaxDepth + d], (uint32_t)tk);
+        atomicAdd(&A.met->depth_tiles[d], (unsigned long long)tk);
+        maxd = d > (int)maxd ? d : maxd;
       } else A.need[i] = 0;
     }
   }
@@ -153,6 +166,8 @@ __global__ void k_classify(ClassifyArgs A) {
   if (threadIdx.x == 0 && s) atomicAdd(&A.met->merge_cost, s);
   s = block_sum(cntA, sred);
   if (threadIdx.x == 0 && s) atomicAdd(&A.met->phaseA, s);
+  maxd = warp_max(maxd);
+  if ((threadIdx.x & 31) == 0 && maxd) atomicMax(&A.met->max_depth, (unsigned long long)maxd);
 }
 
 __global__ void k_task_offsets(DevMetrics* met) {
@@ -165,33 +180,100 @@ __global__ void k_task_offsets(DevMetrics* met) {
   }
   met->n_tasks = base;
   met->cursorA = 0;
-  met->task_ctr = 0;
+  met->task_ctr = met->phaseA;
+  met->task_ctr_A = 0;
 }
 
-__global__ void k_task_fill(ClassifyArgs A) {
+// Per depth: exclusive scan of the chunk task counts, offset by depth_base.
+__global__ void k_order_scan(const DevMetrics* __restrict__ met, uint32_t* __restrict__ chunk_depth) {
+  int d = threadIdx.x;
+  if (d >= kMaxDepth) return;
+  int64_t r = (int64_t)met->n_leaves;
+  int64_t nch = (r + kOrdChunk - 1) / kOrdChunk;
+  uint32_t run = (uint32_t)met->depth_base[d];
+  for (int64_t c = 0; c < nch; ++c) {
+    uint32_t v = chunk_depth[c * kMaxDepth + d];
+    chunk_depth[c * kMaxDepth + d] = run;
+    run += v;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_task_fill(ClassifyArgs A, const uint32_t* __restrict__ chunk_depth) {
+  __shared__ uint32_t run[kMaxDepth];
+  __shared__ uint8_t s_dep[kOrdChunk];
+  __shared__ uint32_t s_slot[kOrdChunk];
   int64_t r = (int64_t)A.met->n_leaves;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < r; i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t tl;
-    int c = classify_leaf(A, i, &tl);
-    uint32_t lid = A.leaf_base + (uint32_t)i;
-    if (c == 1) {
-      unsigned long long slot = atomicAdd(&A.met->cursorA, 1ull);
-      A.tasks[slot] = make_task(kTaskFuse, 0, lid);
-    } else if (c == 2) {
-      unsigned long long slot = atomicAdd(&A.met->cursorA, (unsigned long long)tl);
-      for (int64_t k = 0; k < tl; ++k) A.tasks[slot + k] = make_task(kTaskLeaf, (uint32_t)k, lid);
-    }
-    if (i >= 1) {
-      int64_t tn;
-      int cn = classify_node(A, i, &tn);
-      if (cn == 1) {
+  int64_t nch = (r + kOrdChunk - 1) / kOrdChunk;
+  int lane = threadIdx.x & 31;
+  for (int64_t ch = blockIdx.x; ch < nch; ch += gridDim.x) {
+    for (int d = threadIdx.x; d < kMaxDepth; d += blockDim.x) run[d] = chunk_depth[ch * kMaxDepth + d];
+    __syncthreads();
+    int64_t i0 = ch * kOrdChunk, i1 = (ch + 1) * kOrdChunk < r ? (ch + 1) * kOrdChunk : r;
+    // phase-A tasks (any order)
+    for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+      int64_t tl;
+      int c = classify_leaf(A, i, &tl);
+      uint32_t lid = A.leaf_base + (uint32_t)i;
+      if (c == 1) {
         unsigned long long slot = atomicAdd(&A.met->cursorA, 1ull);
-        A.tasks[slot] = make_task(kTaskFuse, 0, (uint32_t)i);
-      } else if (cn == 2) {
-        unsigned long long slot = atomicAdd(&A.met->depth_cursor[A.depth[i]], (unsigned long long)tn);
-        for (int64_t k = 0; k < tn; ++k) A.tasks[slot + k] = make_task(kTaskMerge, (uint32_t)k, (uint32_t)i);
+        A.tasks[slot] = make_task(kTaskFuse, 0, lid);
+      } else if (c == 2) {
+        unsigned long long slot = atomicAdd(&A.met->cursorA, (unsigned long long)tl);
+        for (int64_t k = 0; k < tl; ++k) A.tasks[slot + k] = make_task(kTaskLeaf, (uint32_t)k, lid);
+      }
+      if (i >= 1) {
+        int64_t tn, tk;
+        if (classify_node(A, i, &tn, &tk) == 1) {
+          unsigned long long slot = atomicAdd(&A.met->cursorA, 1ull);
+          A.tasks[slot] = make_task(kTaskFuse, 0, (uint32_t)i);
+        }
       }
     }
+    // merge tasks: slots by (depth, position).  Stage (depth, #tasks) of the
+    // chunk's boundaries in smem, warp 0 assigns ordered slots, all threads write.
+    __syncthreads();
+    int64_t cnt_i = i1 - i0;
+    for (int64_t x = threadIdx.x; x < cnt_i; x += blockDim.x) {
+      int64_t i = i0 + x;
+      int64_t tn, tk;
+      uint32_t dv = 0xffu, tv = 0;
+      if (i >= 1 && classify_node(A, i, &tn, &tk) == 2) { dv = A.depth[i]; tv = (uint32_t)tk; }
+      s_dep[x] = (uint8_t)dv;
+      s_slot[x] = tv;
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      for (int64_t g = 0; g < cnt_i; g += 32) {
+        int64_t x = g + lane;
+        int d = x < cnt_i ? s_dep[x] : 255;
+        uint32_t tk = x < cnt_i ? s_slot[x] : 0;
+        uint32_t pre = 0;
+#pragma unroll
+        for (int k = 1; k < 32; ++k) {
+          int dk = __shfl_up_sync(0xffffffffu, d, k);
+          uint32_t tkk = __shfl_up_sync(0xffffffffu, tk, k);
+          if (lane >= k && dk == d) pre += tkk;
+        }
+        uint32_t mask = __match_any_sync(0xffffffffu, d);
+        uint32_t slot = d != 255 ? run[d] + pre : 0;
+        __syncwarp();
+        if (d != 255) {
+          s_slot[x] = slot;
+          if (lane == 31 - __clz(mask)) run[d] = slot + tk;
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    for (int64_t x = threadIdx.x; x < cnt_i; x += blockDim.x) {
+      if (s_dep[x] == 255) continue;
+      int64_t i = i0 + x;
+      int64_t tn, tk;
+      classify_node(A, i, &tn, &tk);
+      uint32_t slot = s_slot[x];
+      for (int64_t k = 0; k < tk; ++k) A.tasks[slot + k] = make_task(kTaskMerge, (uint32_t)k, (uint32_t)i);
+    }
+    __syncthreads();
   }
 }
 
@@ -278,7 +360,7 @@ struct Exec {
   static constexpr size_t smem_fuse() {
     return 2 * (size_t)C::FCAP * (C::kb + TB) + (size_t)C::MAXB * (3 * 2 + 1 + 2 + 2) + 256;
   }
-  static constexpr size_t smem_bytes() { return smem_merge() > smem_fuse() ? smem_merge() : smem_fuse(); }
+  static constexpr size_t smem_bytes() { return smem_fuse(); }
 
   __device__ static void wait_ready(const ExecArgs& E, uint32_t id) {
     uint32_t need = E.need[id];
@@ -380,27 +462,55 @@ struct Exec {
     K* k1 = reinterpret_cast<K*>(E.key[1]);
     T* t0 = HAS_TAGS ? reinterpret_cast<T*>(E.tag[0]) : nullptr;
     T* t1 = HAS_TAGS ? reinterpret_cast<T*>(E.tag[1]) : nullptr;
+    constexpr int U = 8;
     if (mode == kLeafSwap) {
       int64_t half = C::TILE / 2;
       int64_t x0 = (int64_t)k * half, x1 = x0 + half < len / 2 ? x0 + half : len / 2;
-      for (int64_t x = x0 + threadIdx.x; x < x1; x += blockDim.x) {
-        pos_t u = s0 + x, v = s0 + len - 1 - x;
-        K a = ldcg(k0 + u), b = ldcg(k0 + v);
-        k0[u] = b;
-        k0[v] = a;
-        if (HAS_TAGS) {
-          T ta = ldcg(t0 + u), tb = ldcg(t0 + v);
-          t0[u] = tb;
-          t0[v] = ta;
+      for (int64_t xb = x0 + threadIdx.x; xb < x1; xb += (int64_t)blockDim.x * U) {
+        K a[U], b[U];
+        T ta[U], tb[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          int64_t x = xb + (int64_t)u * blockDim.x;
+          if (x < x1) {
+            a[u] = ldcg(k0 + s0 + x);
+            b[u] = ldcg(k0 + s0 + len - 1 - x);
+            if (HAS_TAGS) { ta[u] = ldcg(t0 + s0 + x); tb[u] = ldcg(t0 + s0 + len - 1 - x); }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          int64_t x = xb + (int64_t)u * blockDim.x;
+          if (x < x1) {
+            k0[s0 + x] = b[u];
+            k0[s0 + len - 1 - x] = a[u];
+            if (HAS_TAGS) { t0[s0 + x] = tb[u]; t0[s0 + len - 1 - x] = ta[u]; }
+          }
         }
       }
     } else {
       int64_t x0 = (int64_t)k * C::TILE, x1 = x0 + C::TILE < len ? x0 + C::TILE : len;
-      for (int64_t x = x0 + threadIdx.x; x < x1; x += blockDim.x) {
-        pos_t from = s0 + x;
-        pos_t to = mode == kLeafRevCopy ? s0 + len - 1 - x : s0 + x;
-        k1[to] = ldcg(k0 + from);
-        if (HAS_TAGS) t1[to] = ldcg(t0 + from);
+      bool rev = mode == kLeafRevCopy;
+      for (int64_t xb = x0 + threadIdx.x; xb < x1; xb += (int64_t)blockDim.x * U) {
+        K a[U];
+        T ta[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          int64_t x = xb + (int64_t)u * blockDim.x;
+          if (x < x1) {
+            a[u] = ldcg(k0 + s0 + x);
+            if (HAS_TAGS) ta[u] = ldcg(t0 + s0 + x);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          int64_t x = xb + (int64_t)u * blockDim.x;
+          if (x < x1) {
+            pos_t to = rev ? s0 + len - 1 - x : s0 + x;
+            k1[to] = a[u];
+            if (HAS_TAGS) t1[to] = ta[u];
+          }
+        }
       }
     }
   }
@@ -443,10 +553,8 @@ struct Exec {
     int len = int(e - s);
     const K* g0 = reinterpret_cast<const K*>(E.key[0]);
     const T* h0 = HAS_TAGS ? reinterpret_cast<const T*>(E.tag[0]) : nullptr;
-    for (int x = threadIdx.x; x < len; x += blockDim.x) {
-      X[0][x] = ldcg(g0 + s + x);
-      if (HAS_TAGS) Y[0][x] = ldcg(h0 + s + x);
-    }
+    copy_g2s(X[0], g0 + s, len, threadIdx.x, blockDim.x);
+    if (HAS_TAGS) copy_g2s(Y[0], h0 + s, len, threadIdx.x, blockDim.x);
     __syncthreads();
     // leaves: warp per leaf
     int wid = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
@@ -618,26 +726,25 @@ struct Exec {
   }
 };
 
+// Phase A: fused subtrees and big-leaf tiles (no dependencies among them).
 template <typename K, int TB>
-__global__ void __launch_bounds__(kExecThreads) k_execute(ExecArgs E) {
+__global__ void __launch_bounds__(kExecThreads) k_phaseA(ExecArgs E) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ unsigned long long s_task;
   __shared__ unsigned long long sred[32];
   unsigned long long comps = 0;
-  unsigned long long ntasks = E.met->n_tasks;
+  unsigned long long ntasks = E.met->phaseA;
   for (;;) {
-    if (threadIdx.x == 0) s_task = atomicAdd(&E.met->task_ctr, 1ull);
+    if (threadIdx.x == 0) s_task = atomicAdd(&E.met->task_ctr_A, 1ull);
     __syncthreads();
     unsigned long long t = s_task;
     if (t >= ntasks) break;
     uint64_t rec = E.tasks[t];
     uint32_t kind = task_kind(rec), id = task_id(rec), tile = task_tile(rec);
-    if (kind == kTaskMerge) Exec<K, TB>::merge_task(E, id, tile, smem, comps);
-    else if (kind == kTaskLeaf) Exec<K, TB>::leaf_task(E, id - E.leaf_base, tile);
+    if (kind == kTaskLeaf) Exec<K, TB>::leaf_task(E, id - E.leaf_base, tile);
     else Exec<K, TB>::fuse_task(E, id, smem, comps);
-    __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) atomicAdd(E.done + id, 1u);
+    if (threadIdx.x == 0) release_add_u32(E.done + id, 1u);
   }
   unsigned long long s = block_sum(comps, sred);
   if (threadIdx.x == 0 && s) atomicAdd(&E.met->comparisons, s);

@@ -1,0 +1,538 @@
+// rs_merge.cuh -- warp-specialized TMA merge executor for the large tree nodes.
+//
+// Reference: runcore.py:251-279 (_stable_merge: stable two-run merge, ties go
+// to the left run), runcore.py:282-326 (merge_cost / comparison accounting),
+// sorters.py:478-516 (every internal node of the power tree is one merge).
+//
+// Each CTA = 1 producer warp + 8 consumer warps, with an S-stage shared-memory
+// ring guarded by mbarriers:
+//   producer  claims a "super task" (up to kSuper consecutive output tiles of
+//             one node), waits until both children are complete (per-node
+//             counters, acquire loads), finds the merge-path split of every
+//             tile boundary with lane-group parallel searches in HBM, then for
+//             each tile issues 1D TMA bulk copies (cp.async.bulk) of its A and
+//             B input windows into a free stage, completing on the stage's
+//             full barrier.
+//   consumers merge the stage (per-thread merge path in SMEM, IPT outputs per
+//             thread held in registers), write the result back into the stage
+//             and stream it to HBM with coalesced stores, publish the tile on
+//             the node's counter, and release the stage.
+// Task order is deepest-first, so every wait is on an earlier task and the
+// persistent grid (all CTAs resident) cannot deadlock.
+#pragma once
+#include "rs_common.cuh"
+#include "rs_exec.cuh"
+
+namespace rs {
+
+constexpr int kSuper = 1;              // tiles per merge task
+constexpr int kStages = 2;             // smem ring depth
+constexpr int kHold = 1;               // producer's out-of-order task window
+constexpr int kConsumerThreads = 256;  // 8 consumer warps
+constexpr int kMergeThreads = kConsumerThreads + 64;  // + producer warp + signaller warp
+
+template <typename K, int TB>
+struct MergeCfg {
+  static constexpr int kb = sizeof(K);
+  static constexpr int eb = kb + TB;
+  static constexpr int IPT = eb == 4 ? 31 : (eb <= 8 ? 15 : (eb <= 12 ? 11 : 7));  // odd: conflict-free write-back
+  static constexpr int TILE = kConsumerThreads * IPT;
+  static constexpr int KBYTES = TILE * kb + 128;
+  static constexpr int TBYTES = TB ? TILE * TB + 128 : 0;
+  static constexpr int STAGE = KBYTES + TBYTES;
+  static constexpr size_t SMEM = (size_t)kStages * STAGE + 1024;
+};
+
+struct StageHdr {
+  pos_t dst;     // first output element index
+  int32_t len;   // outputs in this tile
+  int32_t la;    // A elements
+  int32_t offA;  // element offsets inside the stage's key region
+  int32_t offB;
+  int32_t toffA; // element offsets inside the stage's tag region
+  int32_t toffB;
+  uint32_t node;
+  int32_t parity;  // destination buffer
+  int32_t end;
+  int32_t pad;
+};
+
+// ---- PTX helpers (mbarrier + 1D TMA bulk copies) ----
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_addr(bar)), "r"(parity), "r"(0x989680u)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"r"(kConsumerThreads) : "memory"); }
+
+// Issue the aligned bulk copy covering elements [e0, e1) of `base` (element
+// size es) into smem at `dst`; returns bytes and the element offset of e0.
+__device__ __forceinline__ uint32_t tma_window(unsigned char* dst, const void* base, pos_t e0, pos_t e1, int es,
+                                               uint64_t* bar, int32_t* off) {
+  if (e1 <= e0) {
+    *off = 0;
+    return 0;
+  }
+  uintptr_t a0 = reinterpret_cast<uintptr_t>(base) + (uintptr_t)e0 * es;
+  uintptr_t a1 = reinterpret_cast<uintptr_t>(base) + (uintptr_t)e1 * es;
+  uintptr_t g0 = a0 & ~(uintptr_t)15;
+  uintptr_t g1 = (a1 + 15) & ~(uintptr_t)15;
+  *off = (int32_t)((a0 - g0) / es);
+  uint32_t bytes = (uint32_t)(g1 - g0);
+  tma_load_1d(dst, reinterpret_cast<const void*>(g0), bytes, bar);
+  return bytes;
+}
+
+struct MergeArgs {
+  void* key[2];
+  void* tag[2];
+  int classic;
+  const pos_t* leaf_start;
+  const uint8_t* depth;
+  const pos_t* node_s;
+  const pos_t* node_e;
+  const uint32_t* child;
+  const uint32_t* need;
+  uint32_t* done;
+  const uint64_t* tasks;
+  DevMetrics* met;
+};
+
+__device__ __forceinline__ bool counter_ready(const uint32_t* done, const uint32_t* need, uint32_t id) {
+  uint32_t nd = need[id];
+  return nd == 0 || ld_acquire_u32(done + id) >= nd;
+}
+
+__device__ __forceinline__ void wait_counter(const uint32_t* done, const uint32_t* need, uint32_t id) {
+  uint32_t nd = need[id];
+  if (nd == 0) return;
+  unsigned ns = 32;
+  while (ld_acquire_u32(done + id) < nd) {
+    __nanosleep(ns);
+    if (ns < 512) ns <<= 1;
+  }
+}
+
+// Lane-group merge-path search: lanes [g*G, g*G+G) cooperate on diagonal `diag`
+// of group g.  Returns the split (number of A elements) in every lane.
+template <typename K>
+__device__ __forceinline__ int64_t group_merge_path(const K* A, int64_t na, const K* B, int64_t nb, int64_t diag,
+                                                    bool active, int G) {
+  int lane = threadIdx.x & 31;
+  int g = lane / G, gl = lane % G;
+  int64_t lo = 0, hi = 0;
+  if (active) {
+    lo = diag - nb > 0 ? diag - nb : 0;
+    hi = diag < na ? diag : na;
+  }
+  for (;;) {
+    bool need = active && (hi - lo > G);
+    if (!__any_sync(0xffffffffu, need)) break;
+    int64_t idx = 0;
+    bool pred = false;
+    if (need) {
+      int64_t span = hi - lo;
+      idx = lo + (span * (gl + 1)) / (G + 1);
+      pred = ldcg(A + idx) <= ldcg(B + (diag - 1 - idx));
+    }
+    uint32_t bal = __ballot_sync(0xffffffffu, pred);
+    int base = g * G;
+    uint32_t mine = (bal >> base) & ((1u << G) - 1u);
+    int c = __popc(mine);
+    int64_t idx_lo = __shfl_sync(0xffffffffu, idx, base + (c > 0 ? c - 1 : 0));
+    int64_t idx_hi = __shfl_sync(0xffffffffu, idx, base + (c < G ? c : G - 1));
+    if (need) {
+      int64_t nlo = c > 0 ? idx_lo + 1 : lo;
+      int64_t nhi = c < G ? idx_hi : hi;
+      lo = nlo;
+      hi = nhi;
+    }
+  }
+  int64_t idx = lo + gl;
+  bool pred = active && idx < hi && ldcg(A + idx) <= ldcg(B + (diag - 1 - idx));
+  uint32_t bal = __ballot_sync(0xffffffffu, pred);
+  uint32_t mine = (bal >> (g * G)) & ((1u << G) - 1u);
+  return lo + __popc(mine);
+}
+
+template <typename K>
+__device__ int64_t warp_count(const K* A, int64_t len, K v, bool or_equal) {
+  int lane = threadIdx.x & 31;
+  int64_t lo = 0, hi = len;
+  while (hi - lo > 32) {
+    int64_t span = hi - lo;
+    int64_t idx = lo + (span * (lane + 1)) / 33;
+    K x = ldcg(A + idx);
+    bool pred = or_equal ? (x <= v) : (x < v);
+    uint32_t bal = __ballot_sync(0xffffffffu, pred);
+    int c = __popc(bal);
+    int64_t nlo = c > 0 ? __shfl_sync(0xffffffffu, idx, c - 1) + 1 : lo;
+    int64_t nhi = c < 32 ? __shfl_sync(0xffffffffu, idx, c < 32 ? c : 31) : hi;
+    lo = nlo;
+    hi = nhi;
+  }
+  int64_t idx = lo + lane;
+  bool pred = false;
+  if (idx < hi) {
+    K x = ldcg(A + idx);
+    pred = or_equal ? (x <= v) : (x < v);
+  }
+  return lo + __popc(__ballot_sync(0xffffffffu, pred));
+}
+
+template <typename K, int TB>
+__global__ void __launch_bounds__(kMergeThreads) k_merge_exec(MergeArgs E) {
+  using C = MergeCfg<K, TB>;
+  using T = typename TagT<TB>::type;
+  constexpr bool HT = TB != 0;
+  extern __shared__ __align__(128) unsigned char smem_m[];
+  unsigned char* smem = smem_m;
+  __shared__ __align__(8) uint64_t full_bar[kStages];
+  __shared__ __align__(8) uint64_t empty_bar[kStages];
+  __shared__ __align__(8) uint64_t stored_bar[kStages];
+  __shared__ StageHdr hdr[kStages];
+
+  int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+      mbar_init(&stored_bar[s], kConsumerThreads / 32);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  unsigned long long ntasks = E.met->n_tasks;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------- producer
+    unsigned long long comps = 0;
+    int stage = 0;
+    uint32_t phase = 0;  // flips when stage wraps
+    const int G = 32 / (kSuper + 1);
+    // Small out-of-order window: up to kHold claimed tasks are held and the
+    // oldest one whose children are complete is prepared first.  Every held
+    // task depends only on earlier tasks, so the oldest held-but-unready task
+    // in the whole grid always becomes ready: no deadlock.
+    uint32_t hj[kHold], hsk[kHold];
+    bool hv[kHold];
+#pragma unroll
+    for (int w = 0; w < kHold; ++w) hv[w] = false;
+    bool exhausted = false;
+    for (;;) {
+#pragma unroll
+      for (int w = 0; w < kHold; ++w) {
+        if (!hv[w] && !exhausted) {
+          unsigned long long t = 0;
+          if (lane == 0) t = atomicAdd(&E.met->task_ctr, 1ull);
+          t = __shfl_sync(0xffffffffu, t, 0);
+          if (t >= ntasks) {
+            exhausted = true;
+          } else {
+            uint64_t rec = E.tasks[t];
+            hj[w] = task_id(rec);
+            hsk[w] = task_tile(rec);
+            hv[w] = true;
+          }
+        }
+      }
+      bool any = false;
+#pragma unroll
+      for (int w = 0; w < kHold; ++w) any |= hv[w];
+      if (!any) break;
+      RS_T0(tw);
+      int pick = -1;
+      unsigned ns = 32;
+      for (;;) {
+        if (lane == 0) {
+#pragma unroll
+          for (int w = 0; w < kHold; ++w) {
+            if (pick < 0 && hv[w] && counter_ready(E.done, E.need, E.child[2 * hj[w]]) &&
+                counter_ready(E.done, E.need, E.child[2 * hj[w] + 1]))
+              pick = w;
+          }
+        }
+        pick = __shfl_sync(0xffffffffu, pick, 0);
+        if (pick >= 0) break;
+        __nanosleep(ns);
+        if (ns < 256) ns <<= 1;
+      }
+      uint32_t j = 0, sk = 0;
+#pragma unroll
+      for (int w = 0; w < kHold; ++w)
+        if (w == pick) { j = hj[w]; sk = hsk[w]; hv[w] = false; }
+      if (lane == 0) {
+        fence_proxy_async();
+#ifdef RS_INSTR
+        atomicAdd(&E.met->depth_wait[E.depth[j]], (unsigned long long)(clock64() - tw));
+#endif
+        RS_ACC(E.met, 0, tw);
+      }
+      __syncwarp();
+      RS_T0(tsrch);
+      pos_t s = E.node_s[j], e = E.node_e[j], m = E.leaf_start[j];
+      int d = E.depth[j];
+      const K* src = reinterpret_cast<const K*>(((d + 1) & 1) ? E.key[1] : E.key[0]);
+      const T* tsrc = HT ? reinterpret_cast<const T*>(((d + 1) & 1) ? E.tag[1] : E.tag[0]) : nullptr;
+      int64_t tot = e - s, na = m - s, nb = e - m;
+      int64_t ntile = (tot + C::TILE - 1) / C::TILE;
+      int64_t kbeg = (int64_t)sk * kSuper;
+      int64_t kend = kbeg + kSuper < ntile ? kbeg + kSuper : ntile;
+      int g = lane / G;
+      int64_t diag = (kbeg + g) * (int64_t)C::TILE;
+      if (diag > tot) diag = tot;
+      bool in_range = g <= (kend - kbeg) && g < kSuper + 1 && lane < G * (kSuper + 1);
+      bool trivial = diag == 0 || diag == tot;
+      int64_t split = group_merge_path(src + s, na, src + m, nb, diag, in_range && !trivial, G);
+      if (diag == 0) split = 0;
+      else if (diag == tot) split = na;
+      if (lane == 0) RS_ACC(E.met, 1, tsrch);
+      if (E.classic && kbeg == 0) {
+        // runcore.py:321-324
+        K maxL = ldcg(src + m - 1), maxR = ldcg(src + e - 1);
+        int64_t rl = warp_count(src + m, nb, maxL, false);
+        int64_t lr = warp_count(src + s, na, maxR, true);
+        int64_t pl = na - 1 + rl, pr = nb - 1 + lr;
+        if (lane == 0) comps += (unsigned long long)((pl < pr ? pl : pr) + 1);
+      }
+      for (int64_t k = kbeg; k < kend; ++k) {
+        int gi = int(k - kbeg);
+        int64_t i0 = __shfl_sync(0xffffffffu, split, gi * G);
+        int64_t i1 = __shfl_sync(0xffffffffu, split, (gi + 1) * G);
+        if (lane == 0) {
+          RS_T0(te);
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          RS_ACC(E.met, 2, te);
+          int64_t o0 = k * (int64_t)C::TILE;
+          int64_t o1 = o0 + C::TILE < tot ? o0 + C::TILE : tot;
+          int64_t j0 = o0 - i0, j1 = o1 - i1;
+          unsigned char* sk_base = smem + (size_t)stage * C::STAGE;
+          StageHdr& h = hdr[stage];
+          h.dst = s + o0;
+          h.len = int32_t(o1 - o0);
+          h.la = int32_t(i1 - i0);
+          h.node = j;
+          h.parity = d & 1;
+          h.end = 0;
+          // expected bytes first (tx count may complete before arrive otherwise)
+          uintptr_t ka0 = reinterpret_cast<uintptr_t>(src + s + i0), ka1 = reinterpret_cast<uintptr_t>(src + s + i1);
+          uintptr_t kb0 = reinterpret_cast<uintptr_t>(src + m + j0), kb1 = reinterpret_cast<uintptr_t>(src + m + j1);
+          uint32_t bA = i1 > i0 ? (uint32_t)(((ka1 + 15) & ~(uintptr_t)15) - (ka0 & ~(uintptr_t)15)) : 0u;
+          uint32_t bB = j1 > j0 ? (uint32_t)(((kb1 + 15) & ~(uintptr_t)15) - (kb0 & ~(uintptr_t)15)) : 0u;
+          uint32_t tx = bA + bB;
+          uint32_t tA = 0, tBb = 0;
+          if (HT) {
+            uintptr_t ta0 = reinterpret_cast<uintptr_t>(tsrc + s + i0), ta1 = reinterpret_cast<uintptr_t>(tsrc + s + i1);
+            uintptr_t tb0 = reinterpret_cast<uintptr_t>(tsrc + m + j0), tb1 = reinterpret_cast<uintptr_t>(tsrc + m + j1);
+            tA = i1 > i0 ? (uint32_t)(((ta1 + 15) & ~(uintptr_t)15) - (ta0 & ~(uintptr_t)15)) : 0u;
+            tBb = j1 > j0 ? (uint32_t)(((tb1 + 15) & ~(uintptr_t)15) - (tb0 & ~(uintptr_t)15)) : 0u;
+            tx += tA + tBb;
+          }
+          mbar_arrive_tx(&full_bar[stage], tx);
+          int32_t offA, offB;
+          uint32_t gotA = tma_window(sk_base, src, s + i0, s + i1, sizeof(K), &full_bar[stage], &offA);
+          uint32_t bstart = (gotA + 15) & ~15u;
+          tma_window(sk_base + bstart, src, m + j0, m + j1, sizeof(K), &full_bar[stage], &offB);
+          h.offA = offA;
+          h.offB = offB + int32_t(bstart / sizeof(K));
+          if (HT) {
+            unsigned char* tg = sk_base + C::KBYTES;
+            int32_t toA, toB;
+            uint32_t gtA = tma_window(tg, tsrc, s + i0, s + i1, TB, &full_bar[stage], &toA);
+            uint32_t tbs = (gtA + 15) & ~15u;
+            tma_window(tg + tbs, tsrc, m + j0, m + j1, TB, &full_bar[stage], &toB);
+            h.toffA = toA;
+            h.toffB = toB + int32_t(tbs / (TB ? TB : 1));
+          }
+        }
+        __syncwarp();
+        if (++stage == kStages) { stage = 0; phase ^= 1; }
+      }
+    }
+    if (lane == 0) {
+      mbar_wait(&empty_bar[stage], phase ^ 1);
+      hdr[stage].end = 1;
+      mbar_arrive(&full_bar[stage]);
+      if (comps) atomicAdd(&E.met->comparisons, comps);
+    }
+    return;
+  }
+
+  if (warp == 1) {
+    // ------------------------------------------------------------ signaller
+    // Publishes finished tiles (release fence + counter add) off the consumers'
+    // critical path, then hands the stage back to the producer.
+    int stage = 0;
+    uint32_t phase = 0;
+    for (;;) {
+      mbar_wait(&stored_bar[stage], phase);
+      int end = hdr[stage].end;
+      uint32_t node = hdr[stage].node;
+      if (end) break;
+      if (lane == 0) {
+        release_add_u32(E.done + node, 1u);
+        mbar_arrive(&empty_bar[stage]);
+      }
+      __syncwarp();
+      if (++stage == kStages) { stage = 0; phase ^= 1; }
+    }
+    return;
+  }
+
+  // --------------------------------------------------------------- consumers
+  int ct = threadIdx.x - 64;
+  int cl = ct & 31;
+  constexpr int VK = 16 / sizeof(K);
+  constexpr int VT = HT ? 16 / (HT ? TB : 1) : 1;
+  int stage = 0;
+  uint32_t phase = 0;
+  for (;;) {
+    RS_T0(tf);
+    mbar_wait(&full_bar[stage], phase);
+    if (ct == 0) RS_ACC(E.met, 3, tf);
+    RS_T0(tk);
+    const StageHdr h = hdr[stage];
+    if (h.end) {
+      if (cl == 0) mbar_arrive(&stored_bar[stage]);
+      break;
+    }
+    unsigned char* base = smem + (size_t)stage * C::STAGE;
+    K* sk = reinterpret_cast<K*>(base);
+    T* st = reinterpret_cast<T*>(base + C::KBYTES);
+    const K* A = sk + h.offA;
+    const K* B = sk + h.offB;
+    const T* TA = HT ? st + h.toffA : nullptr;
+    const T* TBp = HT ? st + h.toffB : nullptr;
+    int len = h.len, la = h.la, lb = len - la;
+    int d0 = ct * C::IPT;
+    int cnt = len - d0;
+    cnt = cnt < 0 ? 0 : (cnt > C::IPT ? C::IPT : cnt);
+    K rk[C::IPT];
+    T rt[HT ? C::IPT : 1];
+    if (cnt > 0) {
+      // lean merge-path search: lo = #A outputs before diagonal d0
+      int lo = d0 - lb > 0 ? d0 - lb : 0;
+      int len_s = (d0 < la ? d0 : la) - lo;
+      while (len_s > 0) {
+        int half = len_s >> 1;
+        int mid = lo + half;
+        bool c = A[mid] <= B[d0 - 1 - mid];
+        lo = c ? mid + 1 : lo;
+        len_s = c ? len_s - half - 1 : half;
+      }
+      const K* pa = A + lo;
+      const K* pb = B + (d0 - lo);
+      const K* ea = A + la;
+      const K* eb = B + lb;
+      K va = *pa, vb = *pb;
+      if (cnt == C::IPT) {
+#pragma unroll
+        for (int q = 0; q < C::IPT; ++q) {
+          bool p = (pa < ea) && (pb >= eb || va <= vb);
+          rk[q] = p ? va : vb;
+          if (HT) rt[q] = p ? TA[pa - A] : TBp[pb - B];
+          pa += p;
+          pb += !p;
+          K nv = *(p ? pa : pb);
+          va = p ? nv : va;
+          vb = p ? vb : nv;
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < C::IPT; ++q) {
+          if (q < cnt) {
+            bool p = (pa < ea) && (pb >= eb || va <= vb);
+            rk[q] = p ? va : vb;
+            if (HT) rt[q] = p ? TA[pa - A] : TBp[pb - B];
+            pa += p;
+            pb += !p;
+            K nv = *(p ? pa : pb);
+            va = p ? nv : va;
+            vb = p ? vb : nv;
+          }
+        }
+      }
+    }
+    // write back with the global 16B phase so the store loop can use 16B vectors
+    K* gdst = reinterpret_cast<K*>(h.parity ? E.key[1] : E.key[0]) + h.dst;
+    int pad = int((reinterpret_cast<uintptr_t>(gdst) & 15) / sizeof(K));
+    T* tdst = HT ? reinterpret_cast<T*>(h.parity ? E.tag[1] : E.tag[0]) + h.dst : nullptr;
+    int tpad = HT ? int((reinterpret_cast<uintptr_t>(tdst) & 15) / (HT ? TB : 1)) : 0;
+    consumer_sync();
+#pragma unroll
+    for (int q = 0; q < C::IPT; ++q) {
+      if (q < cnt) {
+        sk[pad + d0 + q] = rk[q];
+        if (HT) st[tpad + d0 + q] = rt[q];
+      }
+    }
+    consumer_sync();
+    {
+      int h0 = (VK - pad) % VK;
+      if (h0 > len) h0 = len;
+      int nvec = (len - h0) / VK;
+      int tail0 = h0 + nvec * VK;
+      if (ct < h0) gdst[ct] = sk[pad + ct];
+      const uint4* sv = reinterpret_cast<const uint4*>(sk + pad + h0);
+      uint4* gv = reinterpret_cast<uint4*>(gdst + h0);
+      for (int v = ct; v < nvec; v += kConsumerThreads) gv[v] = sv[v];
+      if (ct < len - tail0) gdst[tail0 + ct] = sk[pad + tail0 + ct];
+    }
+    if (HT) {
+      int h0 = (VT - tpad) % VT;
+      if (h0 > len) h0 = len;
+      int nvec = (len - h0) / VT;
+      int tail0 = h0 + nvec * VT;
+      if (ct < h0) tdst[ct] = st[tpad + ct];
+      const uint4* sv = reinterpret_cast<const uint4*>(st + tpad + h0);
+      uint4* gv = reinterpret_cast<uint4*>(tdst + h0);
+      for (int v = ct; v < nvec; v += kConsumerThreads) gv[v] = sv[v];
+      if (ct < len - tail0) tdst[tail0 + ct] = st[tpad + tail0 + ct];
+    }
+    // each warp: order its lanes' stores (syncwarp), then one arrival per warp
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (cl == 0) mbar_arrive(&stored_bar[stage]);
+    if (ct == 0) RS_ACC(E.met, 4, tk);
+    if (++stage == kStages) { stage = 0; phase ^= 1; }
+  }
+}
+
+}  // namespace rs

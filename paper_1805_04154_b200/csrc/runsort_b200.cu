@@ -20,6 +20,7 @@
 #include "rs_chain.cuh"
 #include "rs_common.cuh"
 #include "rs_exec.cuh"
+#include "rs_merge.cuh"
 #include "rs_tree.cuh"
 
 using namespace rs;
@@ -73,7 +74,7 @@ struct Layout {
   size_t o_key1, o_tag1, o_ascw, o_tables, o_gtab, o_gentry, o_goff, o_tentry, o_toff;
   size_t o_leaf_start, o_leaf_info, o_leaf_depth, o_K, o_P, o_la, o_ra, o_depth;
   size_t o_node_a, o_node_b, o_node_s, o_node_e, o_parent, o_child, o_need, o_done;
-  size_t o_agg, o_tasks, o_met, total;
+  size_t o_agg, o_tasks, o_chunkdep, o_met, total;
 };
 
 int exec_tile(int kb, int tb) {
@@ -137,6 +138,7 @@ Layout make_layout(int64_t n, int w, int kb, int tb) {
   L.o_done = take((size_t)(2 * L.r_max + 2) * 4);
   L.o_agg = take((size_t)2 * L.nchunks * sizeof(MC));
   L.o_tasks = take((size_t)L.max_tasks * 8);
+  L.o_chunkdep = take((size_t)((L.r_max + kOrdChunk - 1) / kOrdChunk + 1) * kMaxDepth * 4);
   L.o_met = take(sizeof(DevMetrics));
   L.total = off + 256;
   return L;
@@ -162,19 +164,25 @@ int device_sms(int* sms) {
 }
 
 template <typename K, int TB>
-int exec_grid(int sms, int* grid, size_t* smem) {
-  static int occ[64] = {0};
+int exec_grid(int sms, int* grid_a, size_t* smem_a, int* grid_m, size_t* smem_m) {
+  static int occ_a[64] = {0}, occ_m[64] = {0};
   int dev;
   RS_CUDA(cudaGetDevice(&dev));
-  *smem = Exec<K, TB>::smem_bytes();
-  if (occ[dev] == 0) {
-    RS_CUDA(cudaFuncSetAttribute(k_execute<K, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem));
+  *smem_a = Exec<K, TB>::smem_bytes();
+  *smem_m = MergeCfg<K, TB>::SMEM;
+  if (occ_a[dev] == 0) {
+    RS_CUDA(cudaFuncSetAttribute(k_phaseA<K, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem_a));
+    RS_CUDA(cudaFuncSetAttribute(k_merge_exec<K, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem_m));
     int o = 0;
-    RS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_execute<K, TB>, kExecThreads, *smem));
-    if (o < 1) return fail(RS_ECUDA, "executor does not fit on an SM");
-    occ[dev] = o;
+    RS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_phaseA<K, TB>, kExecThreads, *smem_a));
+    if (o < 1) return fail(RS_ECUDA, "phase-A kernel does not fit on an SM");
+    occ_a[dev] = o;
+    RS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_merge_exec<K, TB>, kMergeThreads, *smem_m));
+    if (o < 1) return fail(RS_ECUDA, "merge executor does not fit on an SM");
+    occ_m[dev] = o;
   }
-  *grid = sms * occ[dev];
+  *grid_a = sms * occ_a[dev];
+  *grid_m = sms * occ_m[dev];
   return RS_OK;
 }
 
@@ -224,7 +232,7 @@ int run_powersort(K* keys, void* tags, int64_t n, int w, int classic, unsigned c
   int batch = (int)((40 * 1024 - (size_t)W1 * 8) / ((size_t)W1 * 8));
   if (batch < 1) batch = 1;
   if (batch > kTableBatch) batch = kTableBatch;
-  int cthreads = W1 < 1024 ? ((W1 + 31) / 32) * 32 : 1024;
+  int cthreads = W1 <= 256 ? 256 : (W1 < 1024 ? ((W1 + 31) / 32) * 32 : 1024);
   size_t sm_comp = (size_t)batch * W1 * 8 + (size_t)W1 * 8 + 64;
   if (sm_comp > 48 * 1024) RS_CUDA(cudaFuncSetAttribute(k_group_compose, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_comp));
   k_group_compose<<<(unsigned)L.ngroups, cthreads, sm_comp, st>>>(tables, L.ntiles, w, batch, gtab);
@@ -270,20 +278,27 @@ int run_powersort(K* keys, void* tags, int64_t n, int w, int classic, unsigned c
   prof_mark(2, st);
 
   // 6: tasks
-  ClassifyArgs CA{n, w, classic, L.fcap, L.tile, L.leaf_base, leaf_start, leaf_info, leaf_depth, depth,
+  ClassifyArgs CA{n, w, classic, L.fcap, L.tile, MergeCfg<K, TB>::TILE, kSuper, L.leaf_base, leaf_start, leaf_info, leaf_depth, depth,
                   node_s, node_e, parent, need, tasks, met};
-  k_classify<<<grid_r, 256, 0, st>>>(CA);
+  uint32_t* chunkdep = reinterpret_cast<uint32_t*>(at(L.o_chunkdep));
+  int64_t nch_max = (L.r_max + kOrdChunk - 1) / kOrdChunk;
+  RS_CUDA(cudaMemsetAsync(chunkdep, 0, (size_t)(nch_max + 1) * kMaxDepth * 4, st));
+  unsigned grid_o = (unsigned)(nch_max < (int64_t)sms * 4 ? nch_max : (int64_t)sms * 4);
+  if (grid_o == 0) grid_o = 1;
+  k_classify<<<grid_r, 256, 0, st>>>(CA, chunkdep);
   RS_CUDA(cudaGetLastError());
   k_task_offsets<<<1, 32, 0, st>>>(met);
   RS_CUDA(cudaGetLastError());
-  k_task_fill<<<grid_r, 256, 0, st>>>(CA);
+  k_order_scan<<<1, kMaxDepth, 0, st>>>(met, chunkdep);
+  RS_CUDA(cudaGetLastError());
+  k_task_fill<<<grid_o, 256, 0, st>>>(CA, chunkdep);
   RS_CUDA(cudaGetLastError());
   prof_mark(3, st);
 
   // 7: execute
-  int grid;
-  size_t smem;
-  if (int e = exec_grid<K, TB>(sms, &grid, &smem)) return e;
+  int grid_a, grid_m;
+  size_t smem_a, smem_m;
+  if (int e = exec_grid<K, TB>(sms, &grid_a, &smem_a, &grid_m, &smem_m)) return e;
   ExecArgs E;
   E.key[0] = keys;
   E.key[1] = at(L.o_key1);
@@ -306,7 +321,24 @@ int run_powersort(K* keys, void* tags, int64_t n, int w, int classic, unsigned c
   E.done = done;
   E.tasks = tasks;
   E.met = met;
-  k_execute<K, TB><<<grid, kExecThreads, smem, st>>>(E);
+  k_phaseA<K, TB><<<grid_a, kExecThreads, smem_a, st>>>(E);
+  RS_CUDA(cudaGetLastError());
+  MergeArgs M;
+  M.key[0] = E.key[0];
+  M.key[1] = E.key[1];
+  M.tag[0] = E.tag[0];
+  M.tag[1] = E.tag[1];
+  M.classic = classic;
+  M.leaf_start = leaf_start;
+  M.depth = depth;
+  M.node_s = node_s;
+  M.node_e = node_e;
+  M.child = child;
+  M.need = need;
+  M.done = done;
+  M.tasks = tasks;
+  M.met = met;
+  k_merge_exec<K, TB><<<grid_m, kMergeThreads, smem_m, st>>>(M);
   RS_CUDA(cudaGetLastError());
   prof_mark(4, st);
   return RS_OK;
@@ -470,6 +502,24 @@ int rs_sort_host(int algo, int key_dtype, void* keys, int tag_bytes, void* tags,
   cudaStreamSynchronize(st);
   cudaStreamDestroy(st);
   return rc;
+}
+
+int rs_debug_counters(int key_dtype, int tag_bytes, int64_t n, int32_t min_run_len, void* workspace, uint64_t* out,
+                      int cap) {
+  if (n <= 1 || !workspace || !out) return 0;
+  int kb = key_dtype == RS_KEY_I64 ? 8 : 4;
+  Layout L = make_layout(n, min_run_len, kb, tag_bytes);
+  DevMetrics hm;
+  RS_CUDA(cudaDeviceSynchronize());
+  RS_CUDA(cudaMemcpy(&hm, reinterpret_cast<unsigned char*>(workspace) + L.o_met, sizeof(DevMetrics),
+                     cudaMemcpyDeviceToHost));
+  int k = 0;
+  for (; k < cap && k < 8; ++k) out[k] = hm.instr[k];
+  if (k < cap) out[k++] = hm.n_tasks;
+  if (k < cap) out[k++] = hm.phaseA;
+  for (int d = 0; d < kMaxDepth && k < cap; ++d) out[k++] = hm.depth_wait[d];
+  for (int d = 0; d < kMaxDepth && k < cap; ++d) out[k++] = hm.depth_tiles[d];
+  return k;
 }
 
 int32_t rs_max_min_run_len(int key_dtype, int tag_bytes) {

@@ -1,0 +1,39 @@
+"""Run a few powersorts of one BASELINE config (device-resident) -- for ncu / nsight runs."""
+import argparse, ctypes, sys
+sys.path.insert(0, '.')
+import torch
+from paper_1805_04154_b200 import _lib, workloads
+
+ap = argparse.ArgumentParser()
+ap.add_argument('--config', type=int, default=2)
+ap.add_argument('--n', type=int, default=None)
+ap.add_argument('--reps', type=int, default=3)
+ap.add_argument('--w', type=int, default=24)
+a = ap.parse_args()
+keys, tags = workloads.generate(a.config, a.n)
+L = _lib.lib()
+dev = torch.device('cuda')
+src = torch.from_numpy(keys).to(dev); work = torch.empty_like(src)
+tsrc = torch.from_numpy(tags).to(dev) if tags is not None else None
+twork = torch.empty_like(tsrc) if tsrc is not None else None
+kc = _lib.RS_KEY_I32 if keys.itemsize == 4 else _lib.RS_KEY_I64
+tb = tags.itemsize if tags is not None else 0
+n = len(keys)
+wsb = L.rs_workspace_bytes(0, kc, tb, n, a.w)
+ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
+st = torch.cuda.current_stream()
+for i in range(a.reps):
+    work.copy_(src)
+    if twork is not None: twork.copy_(tsrc)
+    m = _lib.RsMetrics()
+    _lib.check(L.rs_sort(0, kc, work.data_ptr(), tb, twork.data_ptr() if twork is not None else None, n, a.w, 0,
+                         ws.data_ptr(), wsb, st.cuda_stream, ctypes.byref(m), None))
+torch.cuda.synchronize()
+print('ok', m.merge_cost, m.runs_detected)
+if __import__('os').environ.get('RS_LIB'):
+    buf = (ctypes.c_uint64 * 138)()
+    k = L.rs_debug_counters(kc, tb, n, a.w, ws.data_ptr(), buf, 138)
+    dw = list(buf[10:74]); dt = list(buf[74:138])
+    print('depth: wait_cycles(M) tasks', [(d, round(dw[d] / 1e6, 1), dt[d]) for d in range(64) if dt[d]])
+    names = ['prod_dep_wait', 'prod_search', 'prod_stage_wait', 'cons_full_wait', 'cons_tile_work', '-', '-', '-', 'n_tasks', 'phaseA']
+    print({nm: buf[i] for i, nm in enumerate(names[:k])})
