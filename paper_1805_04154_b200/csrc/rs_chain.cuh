@@ -86,11 +86,9 @@ __host__ __device__ constexpr int kMaxWinWords(int w) { return (kChainT + w + 96
 // K1+K2a: pair-type bits for this tile (written to ascw) and the tile's
 // candidate table.  One CTA per chain tile.
 template <typename K>
-__global__ void __launch_bounds__(128) k_scan_tables(const K* __restrict__ a, pos_t n, int w,
-                                                     uint32_t* __restrict__ ascw,
-                                                     uint2* __restrict__ tables) {
+__device__ void d_scan_table_tile(const K* __restrict__ a, pos_t n, int w, uint32_t* __restrict__ ascw,
+                                  uint2* __restrict__ tables, int64_t tile) {
   extern __shared__ uint32_t smem_u32[];
-  int64_t tile = blockIdx.x;
   pos_t t0, t1;
   int64_t q0, q1;
   chain_window(tile, n, w, &q0, &q1, &t0, &t1);
@@ -152,15 +150,130 @@ __global__ void __launch_bounds__(128) k_scan_tables(const K* __restrict__ a, po
   }
 }
 
+// K1+K2a with TMA, one chain tile per warp: the warp stages its key window in
+// a warp-private shared-memory slice with one 1D bulk copy (mbarrier
+// completion), derives the pair-type bits and B-words there, and its lanes
+// walk the w+1 candidates.  16+ tiles are in flight per SM.
+__host__ __device__ inline int chain_win_bytes(int w, int kb) {
+  return ((kChainT + w + 192) * kb + 16 + 127) / 128 * 128;
+}
+__host__ __device__ inline int chain_warp_bytes(int w, int kb) {
+  int maxw = kMaxWinWords(w);
+  return chain_win_bytes(w, kb) + ((maxw * 8 + maxw * 2 + 127) / 128) * 128;
+}
+
+template <typename K>
+__device__ void d_scan_tables_tma(const K* __restrict__ a, pos_t n, int w, uint32_t* __restrict__ ascw,
+                                  uint2* __restrict__ tables, int64_t ntiles) {
+  extern __shared__ __align__(128) unsigned char smem_tab[];
+  __shared__ __align__(8) uint64_t kbar[32];
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int maxw = kMaxWinWords(w);
+  unsigned char* kbuf = smem_tab + (size_t)wid * chain_warp_bytes(w, sizeof(K));
+  uint32_t* asc = reinterpret_cast<uint32_t*>(kbuf + chain_win_bytes(w, sizeof(K)));
+  uint32_t* bw = asc + maxw;
+  uint16_t* nz = reinterpret_cast<uint16_t*>(bw + maxw);
+  if (lane == 0) {
+    mbar_init(&kbar[wid], 1);
+    mbar_fence_init();
+  }
+  __syncwarp();
+  uint32_t ph = 0;
+  for (int64_t tile = (int64_t)blockIdx.x * nw + wid; tile < ntiles; tile += (int64_t)gridDim.x * nw) {
+    pos_t t0, t1;
+    int64_t q0, q1;
+    chain_window(tile, n, w, &q0, &q1, &t0, &t1);
+    int nwords = int(q1 - q0);
+    pos_t e0 = 32 * q0, e1 = 32 * q1 + 1 < n ? 32 * q1 + 1 : n;
+    int32_t koff = 0;
+    if (lane == 0) {
+      uintptr_t a0 = reinterpret_cast<uintptr_t>(a + e0), a1 = reinterpret_cast<uintptr_t>(a + e1);
+      uint32_t bytes = (uint32_t)(((a1 + 15) & ~(uintptr_t)15) - (a0 & ~(uintptr_t)15));
+      fence_proxy_async_smem();
+      mbar_arrive_tx(&kbar[wid], bytes);
+      tma_window(kbuf, a, e0, e1, sizeof(K), &kbar[wid], &koff);
+    }
+    koff = __shfl_sync(0xffffffffu, koff, 0);
+    mbar_wait(&kbar[wid], ph);
+    ph ^= 1u;
+    const K* sk = reinterpret_cast<const K*>(kbuf) + koff;  // element 32*q0
+    int64_t own0 = t0 >> 5, own1 = (t1 + 31) >> 5;
+    constexpr int VEC = 16 / sizeof(K);  // elements per 16B lane load = words per warp load
+    constexpr int LPW = 32 / VEC;        // lanes per word
+    if (koff % VEC == 0) {
+      // vector path: one LDS.128 per lane covers VEC words per warp step
+      for (int vb = 0; vb < nwords; vb += VEC) {
+        const uint4 raw = reinterpret_cast<const uint4*>(sk + 32 * vb)[lane];
+        const K* x = reinterpret_cast<const K*>(&raw);
+        K first = x[0];
+        K nxt = __shfl_down_sync(0xffffffffu, first, 1);
+        if (lane == 31) nxt = sk[32 * vb + 32 * VEC];
+        pos_t k0 = 32 * (q0 + vb) + (pos_t)lane * VEC;
+        uint32_t nib = 0;
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) {
+          K cur = x[i];
+          K nx = i + 1 < VEC ? x[i + 1] : nxt;
+          if (k0 + i < n - 1 && cur <= nx) nib |= 1u << i;
+        }
+        uint32_t word = nib << ((lane % LPW) * VEC);
+#pragma unroll
+        for (int o = 1; o < LPW; o <<= 1) word |= __shfl_xor_sync(0xffffffffu, word, o);
+        int wi = vb + lane / LPW;
+        if ((lane % LPW) == 0 && wi < nwords) {
+          int64_t q = q0 + wi;
+          asc[wi] = word;
+          if (q >= own0 && q < own1) ascw[q] = word;
+        }
+      }
+    } else
+    for (int qi = 0; qi < nwords; ++qi) {
+      pos_t k = 32 * (q0 + qi) + lane;
+      int rel = 32 * qi + lane;
+      bool bit = false;
+      if (k < n - 1) bit = sk[rel] <= sk[rel + 1];
+      uint32_t word = __ballot_sync(0xffffffffu, bit);
+      if (lane == 0) {
+        int64_t q = q0 + qi;
+        asc[qi] = word;
+        if (q >= own0 && q < own1) ascw[q] = word;
+      }
+    }
+    __syncwarp();
+    pos_t base = 32 * q0;
+    build_bwords_warp(asc, 0u, bw, nz, nwords, base, n, t0 > 0);
+    for (int c = lane; c <= w; c += 32) {
+      pos_t p;
+      if (c < w) p = t0 + c;
+      else if (t0 == 0) p = 0;
+      else {
+        pos_t ne = nat_end_win(bw, nz, nwords, base, n, t0 - 1);
+        p = ne >= kInf ? kInf : ne + 1;
+      }
+      uint32_t cnt = 0;
+      while (p < t1) {
+        ++cnt;
+        pos_t ne = nat_end_win(bw, nz, nwords, base, n, p);
+        if (ne >= kInf) { p = kInf; break; }
+        p = chain_next(p, ne, w, n);
+      }
+      uint32_t ex;
+      if (p >= kInf) ex = (uint32_t)w;
+      else ex = (p - t1 < w) ? (uint32_t)(p - t1) : (uint32_t)w;
+      tables[tile * (w + 1) + c] = make_uint2(ex, cnt);
+    }
+    __syncwarp();
+  }
+}
+
 // K2b: compose the tables of each group of kChainGroup tiles.
 // out[g*(w+1)+c] = (exit candidate after the group, #leaves) starting at candidate c.
-__global__ void k_group_compose(const uint2* __restrict__ tables, int64_t ntiles, int w, int batch,
-                                uint2* __restrict__ gtab) {
+__device__ void d_group_compose(const uint2* __restrict__ tables, int64_t ntiles, int w, int batch,
+                                uint2* __restrict__ gtab, int64_t g) {
   extern __shared__ uint2 stab[];
   int W1 = w + 1;
   uint32_t* cur = reinterpret_cast<uint32_t*>(stab + (size_t)batch * W1);
   uint32_t* cnt = cur + W1;
-  int64_t g = blockIdx.x;
   int64_t k0 = g * kChainGroup, k1 = k0 + kChainGroup < ntiles ? k0 + kChainGroup : ntiles;
   for (int c = threadIdx.x; c < W1; c += blockDim.x) { cur[c] = c; cnt[c] = 0; }
   for (int64_t kb = k0; kb < k1; kb += batch) {
@@ -185,7 +298,7 @@ __global__ void k_group_compose(const uint2* __restrict__ tables, int64_t ntiles
 
 // K2c: one CTA walks the group tables from candidate 0 of tile 0, recording each
 // group's entry candidate and leaf offset; writes r and the start sentinel.
-__global__ void k_group_entries(const uint2* __restrict__ gtab, int64_t ngroups, int w, int batch,
+__device__ void d_group_entries(const uint2* __restrict__ gtab, int64_t ngroups, int w, int batch,
                                 uint32_t* __restrict__ gentry, uint64_t* __restrict__ goff,
                                 pos_t* __restrict__ leaf_start, pos_t n, int64_t r_max,
                                 DevMetrics* __restrict__ met) {
@@ -225,24 +338,23 @@ __global__ void k_group_entries(const uint2* __restrict__ gtab, int64_t ngroups,
 
 // K2d: per group, walk the tile tables to get each tile's entry and leaf offset
 // (tables staged through shared memory in batches).
-__global__ void k_tile_entries(const uint2* __restrict__ tables, int64_t ntiles, int w, int batch,
+__device__ void d_tile_entries(const uint2* __restrict__ tables, int64_t ntiles, int w, int batch,
                                const uint32_t* __restrict__ gentry, const uint64_t* __restrict__ goff,
-                               uint32_t* __restrict__ tentry, uint64_t* __restrict__ toff) {
+                               uint32_t* __restrict__ tentry, uint64_t* __restrict__ toff, int64_t g) {
   extern __shared__ uint2 stab[];
-  __shared__ uint32_t s_e;
-  __shared__ unsigned long long s_off;
+  __shared__ uint32_t s_e2;
+  __shared__ unsigned long long s_off2;
   int W1 = w + 1;
-  int64_t g = blockIdx.x;
   int64_t k0 = g * kChainGroup, k1 = k0 + kChainGroup < ntiles ? k0 + kChainGroup : ntiles;
-  if (threadIdx.x == 0) { s_e = gentry[g]; s_off = goff[g]; }
+  if (threadIdx.x == 0) { s_e2 = gentry[g]; s_off2 = goff[g]; }
   for (int64_t kb = k0; kb < k1; kb += batch) {
     int nb = int((k1 - kb) < batch ? (k1 - kb) : batch);
     __syncthreads();
     copy_g2s(stab, tables + kb * W1, nb * W1, threadIdx.x, blockDim.x);
     __syncthreads();
     if (threadIdx.x == 0) {
-      uint32_t e = s_e;
-      unsigned long long off = s_off;
+      uint32_t e = s_e2;
+      unsigned long long off = s_off2;
       for (int k = 0; k < nb; ++k) {
         tentry[kb + k] = e;
         toff[kb + k] = off;
@@ -250,23 +362,19 @@ __global__ void k_tile_entries(const uint2* __restrict__ tables, int64_t ntiles,
         off += t.y;
         e = t.x;
       }
-      s_e = e;
-      s_off = off;
+      s_e2 = e;
+      s_off2 = off;
     }
   }
 }
 
 // K2e: one warp per tile re-walks the chain from the tile's true entry and emits
 // leaves: start position and info = min(natural run length, w) | desc << 31.
-__global__ void __launch_bounds__(256) k_emit_leaves(const uint32_t* __restrict__ ascw, pos_t n, int w,
-                                                     int64_t ntiles, const uint32_t* __restrict__ tentry,
-                                                     const uint64_t* __restrict__ toff, int64_t r_max,
-                                                     pos_t* __restrict__ leaf_start,
-                                                     uint32_t* __restrict__ leaf_info) {
+__device__ void d_emit_tile(const uint32_t* __restrict__ ascw, pos_t n, int w, const uint32_t* __restrict__ tentry,
+                            const uint64_t* __restrict__ toff, int64_t r_max, pos_t* __restrict__ leaf_start,
+                            uint32_t* __restrict__ leaf_info, int64_t tile) {
   extern __shared__ uint32_t smem_u32[];
   int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  int64_t tile = (int64_t)blockIdx.x * (blockDim.x >> 5) + wid;
-  if (tile >= ntiles) return;
   int maxw = kMaxWinWords(w);
   uint32_t* asc = smem_u32 + (size_t)wid * (maxw * 2 + (maxw + 1) / 2 + 1);
   uint32_t* bw = asc + maxw;
@@ -275,42 +383,57 @@ __global__ void __launch_bounds__(256) k_emit_leaves(const uint32_t* __restrict_
   int64_t q0, q1;
   chain_window(tile, n, w, &q0, &q1, &t0, &t1);
   int nwords = int(q1 - q0);
-  for (int q = lane; q < nwords; q += 32) asc[q] = ascw[q0 + q];
-  uint32_t prev0 = q0 > 0 ? ascw[q0 - 1] : 0u;
+  {
+    uint32_t v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      int q = lane + 32 * u;
+      v[u] = q < nwords ? __ldcg(ascw + q0 + q) : 0u;
+    }
+    for (int q = lane + 128; q < nwords; q += 32) asc[q] = __ldcg(ascw + q0 + q);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      int q = lane + 32 * u;
+      if (q < nwords) asc[q] = v[u];
+    }
+  }
+  uint32_t prev0 = q0 > 0 ? __ldcg(ascw + q0 - 1) : 0u;
   __syncwarp();
   pos_t base = 32 * q0;
   build_bwords_warp(asc, prev0, bw, nz, nwords, base, n, false);
-  if (lane != 0) return;
-  uint32_t e = tentry[tile];
-  uint64_t off = toff[tile];
-  pos_t p;
-  if (e < (uint32_t)w) p = t0 + e;
-  else if (t0 == 0) p = 0;
-  else {
-    pos_t ne = nat_end_win(bw, nz, nwords, base, n, t0 - 1);
-    p = ne >= kInf ? kInf : ne + 1;
-  }
-  while (p < t1) {
-    pos_t ne = nat_end_win(bw, nz, nwords, base, n, p);
-    uint32_t nl;
-    if (ne >= kInf) nl = (uint32_t)w;
+  if (lane == 0) {
+    uint32_t e = tentry[tile];
+    uint64_t off = toff[tile];
+    pos_t p;
+    if (e < (uint32_t)w) p = t0 + e;
+    else if (t0 == 0) p = 0;
     else {
-      pos_t L = ne - p + 1;
-      nl = L < w ? (uint32_t)L : (uint32_t)w;
+      pos_t ne = nat_end_win(bw, nz, nwords, base, n, t0 - 1);
+      p = ne >= kInf ? kInf : ne + 1;
     }
-    uint32_t desc = 0;
-    if (p < n - 1) {
-      pos_t rel = p - base;
-      desc = ((asc[rel >> 5] >> (rel & 31)) & 1u) ? 0u : 1u;
+    while (p < t1) {
+      pos_t ne = nat_end_win(bw, nz, nwords, base, n, p);
+      uint32_t nl;
+      if (ne >= kInf) nl = (uint32_t)w;
+      else {
+        pos_t L = ne - p + 1;
+        nl = L < w ? (uint32_t)L : (uint32_t)w;
+      }
+      uint32_t desc = 0;
+      if (p < n - 1) {
+        pos_t rel = p - base;
+        desc = ((asc[rel >> 5] >> (rel & 31)) & 1u) ? 0u : 1u;
+      }
+      if ((int64_t)off < r_max) {
+        leaf_start[off] = p;
+        leaf_info[off] = nl | (desc << 31);
+      }
+      ++off;
+      if (ne >= kInf) break;
+      p = chain_next(p, ne, w, n);
     }
-    if ((int64_t)off < r_max) {
-      leaf_start[off] = p;
-      leaf_info[off] = nl | (desc << 31);
-    }
-    ++off;
-    if (ne >= kInf) break;
-    p = chain_next(p, ne, w, n);
   }
+  __syncwarp();  // the warp's smem window is reused for its next tile
 }
 
 }  // namespace rs

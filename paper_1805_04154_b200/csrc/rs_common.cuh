@@ -12,7 +12,7 @@ constexpr int kWarp = 32;
 constexpr pos_t kInf = INT64_MAX / 4;
 
 // ---- chain (min-run) phase ----
-constexpr int kChainT = 4096;      // positions per chain tile
+constexpr int kChainT = 2048;      // positions per chain tile
 constexpr int kChainThreads = 256;
 constexpr int kChainGroup = 64;    // tiles per composition group
 constexpr int kTableBatch = 32;    // tables staged into smem per batch
@@ -53,12 +53,22 @@ struct DevMetrics {
   unsigned long long depth_cursor[kMaxDepth];
   unsigned long long instr[8];  // RS_INSTR builds: cycle counters (see rs_merge.cuh)
   unsigned long long depth_wait[kMaxDepth];  // RS_INSTR: producer dependency-wait cycles per depth
+  unsigned long long prep_ts[16];            // RS_INSTR: globaltimer at each prep phase boundary
+  unsigned int last_ctr[8];                  // 'last block done' counters of the prep kernel
 };
 
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 #ifdef RS_INSTR
+#define RS_TS(met, i) do { if (blockIdx.x == 0 && threadIdx.x == 0) (met)->prep_ts[i] = globaltimer_ns(); } while (0)
 #define RS_T0(v) long long v = clock64()
 #define RS_ACC(met, i, v) atomicAdd(&(met)->instr[i], (unsigned long long)(clock64() - (v)))
 #else
+#define RS_TS(met, i)
 #define RS_T0(v)
 #define RS_ACC(met, i, v)
 #endif
@@ -85,6 +95,21 @@ __device__ __forceinline__ void copy_g2s(T* __restrict__ dst, const T* __restric
       if (x < len) dst[x] = v[u];
     }
   }
+}
+
+// True (in every thread of the block) for the block that finishes last among
+// the grid's blocks on `counter`; that block then sees all others' writes.
+__device__ __forceinline__ bool last_block_done(unsigned int* counter) {
+  __shared__ bool s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    unsigned prev = atomicAdd(counter, 1u);
+    s_last = (prev == gridDim.x - 1);
+    if (s_last) __threadfence();
+  }
+  __syncthreads();
+  return s_last;
 }
 
 // Publish completion of a CTA's global writes: call after a barrier that all
@@ -171,6 +196,68 @@ __device__ __forceinline__ pos_t next_set_bit(const uint32_t* words, const uint1
   int q2 = nz[q + 1];
   if (q2 >= nwords) return kInf;
   return base + 32 * pos_t(q2) + __ffs(words[q2]) - 1;
+}
+
+// ---- PTX helpers (mbarrier + 1D TMA bulk copies) ----
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_addr(bar)), "r"(parity), "r"(0x989680u)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// Issue the aligned bulk copy covering elements [e0, e1) of `base` (element
+// size es) into smem at `dst`; returns bytes and the element offset of e0.
+__device__ __forceinline__ uint32_t tma_window(unsigned char* dst, const void* base, pos_t e0, pos_t e1, int es,
+                                               uint64_t* bar, int32_t* off) {
+  if (e1 <= e0) {
+    *off = 0;
+    return 0;
+  }
+  uintptr_t a0 = reinterpret_cast<uintptr_t>(base) + (uintptr_t)e0 * es;
+  uintptr_t a1 = reinterpret_cast<uintptr_t>(base) + (uintptr_t)e1 * es;
+  uintptr_t g0 = a0 & ~(uintptr_t)15;
+  uintptr_t g1 = (a1 + 15) & ~(uintptr_t)15;
+  *off = (int32_t)((a0 - g0) / es);
+  uint32_t bytes = (uint32_t)(g1 - g0);
+  tma_load_1d(dst, reinterpret_cast<const void*>(g0), bytes, bar);
+  return bytes;
 }
 
 }  // namespace rs

@@ -88,6 +88,7 @@ struct ClassifyArgs {
   const pos_t* node_e;
   const int32_t* parent;
   uint32_t* need;
+  uint8_t* cls;  // unified id -> 0 none, 1 fused root, 2 big (tiles in need[])
   uint64_t* tasks;
   DevMetrics* met;
 };
@@ -121,13 +122,20 @@ __device__ __forceinline__ int classify_node(const ClassifyArgs& A, int64_t j, i
 // Chunks of kOrdChunk elements (leaf i and boundary j = i).  Merge tasks are
 // ordered by depth (deepest first) and, within a depth, by position, so a
 // node's tasks are claimed after the wave of its children's tasks has passed.
-constexpr int kOrdChunk = 1024;
+constexpr int kOrdChunkMin = 256, kOrdChunkMax = 4096;
+// Chunk of boundaries for the ordered fill: small trees -> many small chunks.
+__host__ __device__ inline int64_t ord_chunk(int64_t r) {
+  int64_t c = kOrdChunkMin;
+  while (c < kOrdChunkMax && c * 512 < r) c <<= 1;
+  return c;
+}
 
 // Element-parallel: leaf i and boundary j = i per thread.  Big nodes add their
 // task count to their (chunk, depth) cell for the ordered fill.
-__global__ void __launch_bounds__(256) k_classify(ClassifyArgs A, uint32_t* __restrict__ chunk_depth) {
+__device__ void d_classify(ClassifyArgs A, uint32_t* __restrict__ chunk_depth) {
   __shared__ unsigned long long sred[32];
   int64_t r = (int64_t)A.met->n_leaves;
+  const int64_t ochunk = ord_chunk(r);
   unsigned long long comps = 0, mcost = 0, cntA = 0;
   unsigned maxd = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < r; i += (int64_t)gridDim.x * blockDim.x) {
@@ -143,6 +151,7 @@ __global__ void __launch_bounds__(256) k_classify(ClassifyArgs A, uint32_t* __re
     int c = classify_leaf(A, i, &tl);
     uint32_t lid = A.leaf_base + (uint32_t)i;
     A.need[lid] = c == 1 ? 1u : (uint32_t)tl;
+    A.cls[lid] = (uint8_t)c;
     cntA += c == 1 ? 1 : (unsigned long long)tl;
     if (i >= 1) {
       pos_t span = A.node_e[i] - A.node_s[i];
@@ -150,11 +159,12 @@ __global__ void __launch_bounds__(256) k_classify(ClassifyArgs A, uint32_t* __re
       if (!A.classic) comps += span;  // runcore.py:299-301
       int64_t tn, tk;
       int cn = classify_node(A, i, &tn, &tk);
+      A.cls[i] = (uint8_t)cn;
       if (cn == 1) { A.need[i] = 1; cntA += 1; }
       else if (cn == 2) {
         A.need[i] = (uint32_t)tn;
         int d = A.depth[i];
-        atomicAdd(&chunk_depth[(i / kOrdChunk) * kMaxDepth + d], (uint32_t)tk);
+        atomicAdd(&chunk_depth[(i / ochunk) * kMaxDepth + d], (uint32_t)tk);
         atomicAdd(&A.met->depth_tiles[d], (unsigned long long)tk);
         maxd = d > (int)maxd ? d : maxd;
       } else A.need[i] = 0;
@@ -170,8 +180,8 @@ __global__ void __launch_bounds__(256) k_classify(ClassifyArgs A, uint32_t* __re
   if ((threadIdx.x & 31) == 0 && maxd) atomicMax(&A.met->max_depth, (unsigned long long)maxd);
 }
 
-__global__ void k_task_offsets(DevMetrics* met) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+__device__ void d_task_offsets(DevMetrics* met) {
+  if (threadIdx.x != 0) return;
   unsigned long long base = met->phaseA;
   for (int d = (int)met->max_depth; d >= 0; --d) {
     met->depth_base[d] = base;
@@ -185,11 +195,12 @@ __global__ void k_task_offsets(DevMetrics* met) {
 }
 
 // Per depth: exclusive scan of the chunk task counts, offset by depth_base.
-__global__ void k_order_scan(const DevMetrics* __restrict__ met, uint32_t* __restrict__ chunk_depth) {
+__device__ void d_order_scan(const DevMetrics* __restrict__ met, uint32_t* __restrict__ chunk_depth) {
   int d = threadIdx.x;
   if (d >= kMaxDepth) return;
   int64_t r = (int64_t)met->n_leaves;
-  int64_t nch = (r + kOrdChunk - 1) / kOrdChunk;
+  int64_t oc = ord_chunk(r);
+  int64_t nch = (r + oc - 1) / oc;
   uint32_t run = (uint32_t)met->depth_base[d];
   for (int64_t c = 0; c < nch; ++c) {
     uint32_t v = chunk_depth[c * kMaxDepth + d];
@@ -198,46 +209,47 @@ __global__ void k_order_scan(const DevMetrics* __restrict__ met, uint32_t* __res
   }
 }
 
-__global__ void __launch_bounds__(256) k_task_fill(ClassifyArgs A, const uint32_t* __restrict__ chunk_depth) {
+__device__ void d_task_fill(ClassifyArgs A, const uint32_t* __restrict__ chunk_depth) {
   __shared__ uint32_t run[kMaxDepth];
-  __shared__ uint8_t s_dep[kOrdChunk];
-  __shared__ uint32_t s_slot[kOrdChunk];
+  // staging lives in the kernel's dynamic shared memory (dead by this phase)
+  extern __shared__ __align__(16) unsigned char smem_fill[];
+  uint32_t* s_slot = reinterpret_cast<uint32_t*>(smem_fill);
+  uint8_t* s_dep = smem_fill + kOrdChunkMax * 4;
   int64_t r = (int64_t)A.met->n_leaves;
-  int64_t nch = (r + kOrdChunk - 1) / kOrdChunk;
+  // phase-A tasks (any order), element-parallel
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < r; i += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t lid = A.leaf_base + (uint32_t)i;
+    int c = A.cls[lid];
+    if (c == 1) {
+      unsigned long long slot = atomicAdd(&A.met->cursorA, 1ull);
+      A.tasks[slot] = make_task(kTaskFuse, 0, lid);
+    } else if (c == 2) {
+      uint32_t tl = A.need[lid];
+      unsigned long long slot = atomicAdd(&A.met->cursorA, (unsigned long long)tl);
+      for (uint32_t k = 0; k < tl; ++k) A.tasks[slot + k] = make_task(kTaskLeaf, k, lid);
+    }
+    if (i >= 1 && A.cls[i] == 1) {
+      unsigned long long slot = atomicAdd(&A.met->cursorA, 1ull);
+      A.tasks[slot] = make_task(kTaskFuse, 0, (uint32_t)i);
+    }
+  }
+  // merge tasks: slots by (depth, position); chunk boundaries staged in smem,
+  // warp 0 assigns ordered slots, all threads write.
+  const int64_t oc = ord_chunk(r);
+  int64_t nch = (r + oc - 1) / oc;
   int lane = threadIdx.x & 31;
   for (int64_t ch = blockIdx.x; ch < nch; ch += gridDim.x) {
+    __syncthreads();
     for (int d = threadIdx.x; d < kMaxDepth; d += blockDim.x) run[d] = chunk_depth[ch * kMaxDepth + d];
-    __syncthreads();
-    int64_t i0 = ch * kOrdChunk, i1 = (ch + 1) * kOrdChunk < r ? (ch + 1) * kOrdChunk : r;
-    // phase-A tasks (any order)
-    for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
-      int64_t tl;
-      int c = classify_leaf(A, i, &tl);
-      uint32_t lid = A.leaf_base + (uint32_t)i;
-      if (c == 1) {
-        unsigned long long slot = atomicAdd(&A.met->cursorA, 1ull);
-        A.tasks[slot] = make_task(kTaskFuse, 0, lid);
-      } else if (c == 2) {
-        unsigned long long slot = atomicAdd(&A.met->cursorA, (unsigned long long)tl);
-        for (int64_t k = 0; k < tl; ++k) A.tasks[slot + k] = make_task(kTaskLeaf, (uint32_t)k, lid);
-      }
-      if (i >= 1) {
-        int64_t tn, tk;
-        if (classify_node(A, i, &tn, &tk) == 1) {
-          unsigned long long slot = atomicAdd(&A.met->cursorA, 1ull);
-          A.tasks[slot] = make_task(kTaskFuse, 0, (uint32_t)i);
-        }
-      }
-    }
-    // merge tasks: slots by (depth, position).  Stage (depth, #tasks) of the
-    // chunk's boundaries in smem, warp 0 assigns ordered slots, all threads write.
-    __syncthreads();
+    int64_t i0 = ch * oc, i1 = (ch + 1) * oc < r ? (ch + 1) * oc : r;
     int64_t cnt_i = i1 - i0;
     for (int64_t x = threadIdx.x; x < cnt_i; x += blockDim.x) {
       int64_t i = i0 + x;
-      int64_t tn, tk;
       uint32_t dv = 0xffu, tv = 0;
-      if (i >= 1 && classify_node(A, i, &tn, &tk) == 2) { dv = A.depth[i]; tv = (uint32_t)tk; }
+      if (i >= 1 && A.cls[i] == 2) {
+        dv = A.depth[i];
+        tv = (A.need[i] + A.msuper - 1) / A.msuper;
+      }
       s_dep[x] = (uint8_t)dv;
       s_slot[x] = tv;
     }
@@ -265,15 +277,15 @@ __global__ void __launch_bounds__(256) k_task_fill(ClassifyArgs A, const uint32_
       }
     }
     __syncthreads();
-    for (int64_t x = threadIdx.x; x < cnt_i; x += blockDim.x) {
+    // one warp per big node writes its task records
+    int wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int64_t x = wid; x < cnt_i; x += nw) {
       if (s_dep[x] == 255) continue;
       int64_t i = i0 + x;
-      int64_t tn, tk;
-      classify_node(A, i, &tn, &tk);
+      uint32_t tk = (A.need[i] + A.msuper - 1) / A.msuper;
       uint32_t slot = s_slot[x];
-      for (int64_t k = 0; k < tk; ++k) A.tasks[slot + k] = make_task(kTaskMerge, (uint32_t)k, (uint32_t)i);
+      for (uint32_t k = lane; k < tk; k += 32) A.tasks[slot + k] = make_task(kTaskMerge, k, (uint32_t)i);
     }
-    __syncthreads();
   }
 }
 

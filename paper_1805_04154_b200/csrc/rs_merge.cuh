@@ -57,68 +57,7 @@ struct StageHdr {
   int32_t pad;
 };
 
-// ---- PTX helpers (mbarrier + 1D TMA bulk copies) ----
-__device__ __forceinline__ uint32_t smem_addr(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_fence_init() {
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
-}
-__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
-      "selp.u32 %0, 1, 0, p;\n\t}"
-      : "=r"(ok)
-      : "r"(smem_addr(bar)), "r"(parity), "r"(0x989680u)
-      : "memory");
-  return ok != 0;
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  while (!mbar_try_wait(bar, parity)) {
-  }
-}
-__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_addr(dst)),
-      "l"(src), "r"(bytes), "r"(smem_addr(bar))
-      : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async;" ::: "memory"); }
-__device__ __forceinline__ void fence_proxy_async_smem() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
 __device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"r"(kConsumerThreads) : "memory"); }
-
-// Issue the aligned bulk copy covering elements [e0, e1) of `base` (element
-// size es) into smem at `dst`; returns bytes and the element offset of e0.
-__device__ __forceinline__ uint32_t tma_window(unsigned char* dst, const void* base, pos_t e0, pos_t e1, int es,
-                                               uint64_t* bar, int32_t* off) {
-  if (e1 <= e0) {
-    *off = 0;
-    return 0;
-  }
-  uintptr_t a0 = reinterpret_cast<uintptr_t>(base) + (uintptr_t)e0 * es;
-  uintptr_t a1 = reinterpret_cast<uintptr_t>(base) + (uintptr_t)e1 * es;
-  uintptr_t g0 = a0 & ~(uintptr_t)15;
-  uintptr_t g1 = (a1 + 15) & ~(uintptr_t)15;
-  *off = (int32_t)((a0 - g0) / es);
-  uint32_t bytes = (uint32_t)(g1 - g0);
-  tma_load_1d(dst, reinterpret_cast<const void*>(g0), bytes, bar);
-  return bytes;
-}
 
 struct MergeArgs {
   void* key[2];

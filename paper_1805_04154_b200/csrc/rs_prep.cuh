@@ -1,0 +1,120 @@
+// rs_prep.cuh -- one cooperative kernel for everything before the executors:
+// run detection + min-run chain (rs_chain.cuh), node powers and the merge tree
+// (rs_tree.cuh), classification and the ordered task list (rs_exec.cuh).
+// Phases are separated by grid-wide barriers instead of ~16 kernel launches.
+#pragma once
+#include <cooperative_groups.h>
+
+#include "rs_chain.cuh"
+#include "rs_exec.cuh"
+#include "rs_tree.cuh"
+
+namespace rs {
+
+struct PrepArgs {
+  const void* keys;
+  pos_t n;
+  int w;
+  int F;
+  int batch, gbatch, tbatch;
+  int64_t ntiles, ngroups, r_max, nchunks;
+  uint32_t* ascw;
+  uint2* tables;
+  uint2* gtab;
+  uint32_t* gentry;
+  uint64_t* goff;
+  uint32_t* tentry;
+  uint64_t* toff;
+  MC* agg;
+  uint32_t* chunkdep;
+  int64_t chunkdep_words;
+  uint32_t* done;
+  int64_t done_words;
+  TreeArrays T;
+  ClassifyArgs CA;
+};
+
+template <typename K>
+__global__ void __launch_bounds__(256, 3) k_prep(PrepArgs P) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  DevMetrics* met = P.CA.met;
+#ifdef RS_INSTR
+  unsigned long long t_start = globaltimer_ns();
+#endif
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t gthreads = (int64_t)gridDim.x * blockDim.x;
+  // zero per-call state (visible to everyone after the first grid barrier)
+  {
+    unsigned long long* m = reinterpret_cast<unsigned long long*>(met);
+    for (int64_t i = gtid; i < (int64_t)(sizeof(DevMetrics) / 8); i += gthreads) m[i] = 0;
+    for (int64_t i = gtid; i < P.done_words; i += gthreads) P.done[i] = 0;
+    for (int64_t i = gtid; i < P.chunkdep_words; i += gthreads) P.chunkdep[i] = 0;
+  }
+  // 1. pair-type bits + candidate tables (sorters.py:462-470, runcore.py:137-159)
+  const K* a = reinterpret_cast<const K*>(P.keys);
+  d_scan_tables_tma<K>(a, P.n, P.w, P.ascw, P.tables, P.ntiles);
+  grid.sync();
+  RS_TS(met, 1);
+#ifdef RS_INSTR
+  if (blockIdx.x == 0 && threadIdx.x == 0) met->prep_ts[0] = t_start;
+#endif
+  // 2. compose tables per group; the last block to finish walks the groups
+  for (int64_t g = blockIdx.x; g < P.ngroups; g += gridDim.x) {
+    d_group_compose(P.tables, P.ntiles, P.w, P.batch, P.gtab, g);
+    __syncthreads();
+  }
+  if (last_block_done(&met->last_ctr[0]))
+    d_group_entries(P.gtab, P.ngroups, P.w, P.gbatch, P.gentry, P.goff, const_cast<pos_t*>(P.T.leaf_start), P.n,
+                    P.r_max, met);
+  grid.sync();
+  RS_TS(met, 2);
+  // 3. tile entries
+  for (int64_t g = blockIdx.x; g < P.ngroups; g += gridDim.x) {
+    d_tile_entries(P.tables, P.ntiles, P.w, P.tbatch, P.gentry, P.goff, P.tentry, P.toff, g);
+    __syncthreads();
+  }
+  grid.sync();
+  RS_TS(met, 3);
+  // 4. emit leaves, one warp per chain tile
+  {
+    int nw = blockDim.x >> 5, wid = threadIdx.x >> 5;
+    for (int64_t t = (int64_t)blockIdx.x * nw + wid; t < P.ntiles; t += (int64_t)gridDim.x * nw)
+      d_emit_tile(P.ascw, P.n, P.w, P.tentry, P.toff, P.r_max, const_cast<pos_t*>(P.T.leaf_start),
+                  const_cast<uint32_t*>(P.T.leaf_info), t);
+  }
+  grid.sync();
+  RS_TS(met, 4);
+  // 5. node powers + ancestor-count scan (chunk aggregates); last block scans them
+  d_scan_reduce(P.T.leaf_start, P.n, P.F, const_cast<uint64_t*>(P.T.K), const_cast<uint8_t*>(P.T.P), met, P.agg,
+                P.nchunks);
+  if (last_block_done(&met->last_ctr[1])) {
+    d_scan_top(met, P.agg, P.nchunks, 0);
+    d_scan_top(met, P.agg, P.nchunks, 1);
+  }
+  grid.sync();
+  RS_TS(met, 5);
+  // 6. depths, max stack height (sorters.py:500-502)
+  d_scan_down(P.T.P, met, P.agg, P.nchunks, const_cast<uint8_t*>(P.T.la), const_cast<uint8_t*>(P.T.ra));
+  grid.sync();
+  RS_TS(met, 6);
+  // 7. trie ranges, parents, children, spans
+  d_tree(P.T, P.F, met);
+  grid.sync();
+  RS_TS(met, 7);
+  // 8. classification + Metrics closed forms; the last block lays out depths
+  d_classify(P.CA, P.chunkdep);
+  if (last_block_done(&met->last_ctr[2])) {
+    d_task_offsets(met);
+    __syncthreads();
+    d_order_scan(met, P.chunkdep);
+  }
+  grid.sync();
+  RS_TS(met, 8);
+  // 9. task records
+  d_task_fill(P.CA, P.chunkdep);
+  grid.sync();
+  RS_TS(met, 9);
+}
+
+}  // namespace rs

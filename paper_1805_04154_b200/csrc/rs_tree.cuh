@@ -42,7 +42,7 @@ __device__ __forceinline__ uint64_t mid_key(pos_t s0, pos_t s1, pos_t n, int F) 
 }
 
 // T1: midpoint keys and boundary powers.
-__global__ void k_keys_powers(const pos_t* __restrict__ leaf_start, pos_t n, int F,
+__device__ void d_keys_powers(const pos_t* __restrict__ leaf_start, pos_t n, int F,
                               const DevMetrics* __restrict__ met, uint64_t* __restrict__ K,
                               uint8_t* __restrict__ P) {
   int64_t r = (int64_t)met->n_leaves;
@@ -58,9 +58,14 @@ __global__ void k_keys_powers(const pos_t* __restrict__ leaf_start, pos_t n, int
 }
 
 // ---- T2: (mask, const) scans for left / right ancestor counts ----
-constexpr int kScanItems = 16;
+constexpr int kScanItems = 16;  // max items per thread
 constexpr int kScanThreads = 256;
 constexpr int kScanChunk = kScanItems * kScanThreads;
+// Items per thread adapt to r so that small trees still spread over many blocks.
+__device__ __forceinline__ int scan_items(int64_t m) {
+  int64_t per = (m + (int64_t)gridDim.x * kScanThreads - 1) / ((int64_t)gridDim.x * kScanThreads);
+  return per < 1 ? 1 : (per > kScanItems ? kScanItems : (int)per);
+}
 
 // boundary for scan position x in direction dir (m = r-1 boundaries)
 __device__ __forceinline__ int64_t scan_j(int64_t x, int64_t m, int dir) { return dir == 0 ? 1 + x : m - x; }
@@ -113,22 +118,52 @@ __device__ inline MC block_excl_scan_mc(MC v, MC* sm, MC* total) {
   return r;
 }
 
-__global__ void __launch_bounds__(kScanThreads) k_scan_reduce(const uint8_t* __restrict__ P,
-                                                              const DevMetrics* __restrict__ met,
-                                                              MC* __restrict__ agg /* [2][nchunks_max] */,
-                                                              int64_t nchunks_max) {
+// Also computes the node powers (dir 0 writes K and P): P_j from leaf starts
+// s_{j-1}, s_j, s_{j+1} (sorters.py:414-423).
+__device__ void d_scan_reduce(const pos_t* __restrict__ leaf_start, pos_t n, int F, uint64_t* __restrict__ Kk,
+                              uint8_t* __restrict__ P, const DevMetrics* __restrict__ met,
+                              MC* __restrict__ agg /* [2][nchunks_max] */, int64_t nchunks_max) {
   __shared__ MC sm[33];
-  int64_t m = (int64_t)met->n_leaves - 1;
-  if (m <= 0) return;
-  int64_t nch = (m + kScanChunk - 1) / kScanChunk;
+  int64_t r = (int64_t)met->n_leaves;
+  int64_t m = r - 1;
+  if (m <= 0) {
+    if (m == 0 && blockIdx.x == 0 && threadIdx.x == 0) Kk[0] = mid_key(leaf_start[0], leaf_start[1], n, F);
+    return;
+  }
+  const int items = scan_items(m);
+  const int64_t chunk = (int64_t)items * kScanThreads;
+  int64_t nch = (m + chunk - 1) / chunk;
   for (int64_t w = blockIdx.x; w < 2 * nch; w += gridDim.x) {
     int dir = int(w / nch);
     int64_t ch = w % nch;
-    int64_t x0 = ch * kScanChunk + (int64_t)threadIdx.x * kScanItems;
+    int64_t x0 = ch * chunk + (int64_t)threadIdx.x * items;
     MC v = mc_identity();
-    for (int k = 0; k < kScanItems; ++k) {
-      int64_t x = x0 + k;
-      if (x < m) v = mc_compose(v, mc_of_power(P[scan_j(x, m, dir)]));
+    if (dir == 0) {
+      uint64_t kprev = 0;
+      if (x0 < m) kprev = mid_key(leaf_start[x0], leaf_start[x0 + 1], n, F);
+      if (x0 == 0) Kk[0] = kprev;
+      for (int k = 0; k < items; ++k) {
+        int64_t x = x0 + k;
+        if (x < m) {
+          int64_t j = x + 1;
+          uint64_t kj = mid_key(leaf_start[j], leaf_start[j + 1], n, F);
+          int p = F + 1 - bitlen64(kprev ^ kj);
+          Kk[j] = kj;
+          P[j] = (uint8_t)p;
+          kprev = kj;
+          v = mc_compose(v, mc_of_power(p));
+        }
+      }
+    } else {
+      for (int k = 0; k < items; ++k) {
+        int64_t x = x0 + k;
+        if (x < m) {
+          int64_t j = scan_j(x, m, 1);
+          uint64_t ka = mid_key(leaf_start[j - 1], leaf_start[j], n, F);
+          uint64_t kb = mid_key(leaf_start[j], leaf_start[j + 1], n, F);
+          v = mc_compose(v, mc_of_power(F + 1 - bitlen64(ka ^ kb)));
+        }
+      }
     }
     MC t = block_reduce_mc(v, sm);
     if (threadIdx.x == 0) agg[dir * nchunks_max + ch] = t;
@@ -137,13 +172,13 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_reduce(const uint8_t* __r
 }
 
 // Exclusive scan of chunk aggregates, per direction (one CTA per direction).
-__global__ void __launch_bounds__(1024) k_scan_top(const DevMetrics* __restrict__ met, MC* __restrict__ agg,
-                                                   int64_t nchunks_max) {
+__device__ void d_scan_top(const DevMetrics* __restrict__ met, MC* __restrict__ agg,
+                           int64_t nchunks_max, int dir) {
   __shared__ MC sm[33];
   int64_t m = (int64_t)met->n_leaves - 1;
   if (m <= 0) return;
-  int64_t nch = (m + kScanChunk - 1) / kScanChunk;
-  int dir = blockIdx.x;
+  const int64_t chunk = (int64_t)scan_items(m) * kScanThreads;
+  int64_t nch = (m + chunk - 1) / chunk;
   MC carry = mc_identity();
   for (int64_t b = 0; b < nch; b += blockDim.x) {
     int64_t i = b + threadIdx.x;
@@ -155,7 +190,7 @@ __global__ void __launch_bounds__(1024) k_scan_top(const DevMetrics* __restrict_
   }
 }
 
-__global__ void __launch_bounds__(kScanThreads) k_scan_down(const uint8_t* __restrict__ P,
+__device__ void d_scan_down(const uint8_t* __restrict__ P,
                                                             DevMetrics* __restrict__ met,
                                                             const MC* __restrict__ agg, int64_t nchunks_max,
                                                             uint8_t* __restrict__ la, uint8_t* __restrict__ ra) {
@@ -163,19 +198,21 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_down(const uint8_t* __res
   __shared__ unsigned long long smax[32];
   int64_t m = (int64_t)met->n_leaves - 1;
   if (m <= 0) return;
-  int64_t nch = (m + kScanChunk - 1) / kScanChunk;
+  const int items = scan_items(m);
+  const int64_t chunk = (int64_t)items * kScanThreads;
+  int64_t nch = (m + chunk - 1) / chunk;
   unsigned long long best = 0;
   for (int64_t w = blockIdx.x; w < 2 * nch; w += gridDim.x) {
     int dir = int(w / nch);
     int64_t ch = w % nch;
-    int64_t x0 = ch * kScanChunk + (int64_t)threadIdx.x * kScanItems;
+    int64_t x0 = ch * chunk + (int64_t)threadIdx.x * items;
     uint8_t pw[kScanItems];
     MC v = mc_identity();
 #pragma unroll
     for (int k = 0; k < kScanItems; ++k) {
       int64_t x = x0 + k;
-      pw[k] = x < m ? P[scan_j(x, m, dir)] : 1;
-      if (x < m) v = mc_compose(v, mc_of_power(pw[k]));
+      pw[k] = (k < items && x < m) ? P[scan_j(x, m, dir)] : 1;
+      if (k < items && x < m) v = mc_compose(v, mc_of_power(pw[k]));
     }
     MC tot;
     MC ex = block_excl_scan_mc(v, sm, &tot);
@@ -184,7 +221,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_down(const uint8_t* __res
 #pragma unroll
     for (int k = 0; k < kScanItems; ++k) {
       int64_t x = x0 + k;
-      if (x < m) {
+      if (k < items && x < m) {
         int p = pw[k];
         uint64_t low = (1ull << (p - 1)) - 1;
         int cntv = __popcll(M & low);
@@ -229,7 +266,7 @@ struct TreeArrays {
   uint32_t leaf_base;
 };
 
-__global__ void k_tree(TreeArrays T, int F, const DevMetrics* __restrict__ met) {
+__device__ void d_tree(TreeArrays T, int F, const DevMetrics* __restrict__ met) {
   int64_t r = (int64_t)met->n_leaves;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < r; i += (int64_t)gridDim.x * blockDim.x) {
     // leaf i

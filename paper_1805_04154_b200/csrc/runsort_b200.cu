@@ -10,6 +10,7 @@
 //   5. k_tree          trie ranges, parents, children, spans
 //   6. k_classify / k_task_offsets / k_task_fill   executor task list
 //   7. k_execute       persistent dataflow executor (leaves + merges)
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -21,6 +22,7 @@
 #include "rs_common.cuh"
 #include "rs_exec.cuh"
 #include "rs_merge.cuh"
+#include "rs_prep.cuh"
 #include "rs_tree.cuh"
 
 using namespace rs;
@@ -74,7 +76,7 @@ struct Layout {
   size_t o_key1, o_tag1, o_ascw, o_tables, o_gtab, o_gentry, o_goff, o_tentry, o_toff;
   size_t o_leaf_start, o_leaf_info, o_leaf_depth, o_K, o_P, o_la, o_ra, o_depth;
   size_t o_node_a, o_node_b, o_node_s, o_node_e, o_parent, o_child, o_need, o_done;
-  size_t o_agg, o_tasks, o_chunkdep, o_met, total;
+  size_t o_agg, o_tasks, o_chunkdep, o_cls, o_met, total;
 };
 
 int exec_tile(int kb, int tb) {
@@ -101,7 +103,7 @@ Layout make_layout(int64_t n, int w, int kb, int tb) {
   L.r_max = n / minleaf + 2;
   if (L.r_max > n + 1) L.r_max = n + 1;
   L.leaf_base = (uint32_t)(L.r_max + 1);
-  L.nchunks = (L.r_max + kScanChunk - 1) / kScanChunk + 1;
+  L.nchunks = (L.r_max + kScanThreads - 1) / kScanThreads + 1;
   int levels = 2;
   for (int64_t x = n; x; x >>= 1) ++levels;
   L.max_tasks = (int64_t)levels * (n / L.tile + n / L.fcap + 2) + 3 * L.r_max + 2 * (n / L.tile) + 16;
@@ -138,7 +140,8 @@ Layout make_layout(int64_t n, int w, int kb, int tb) {
   L.o_done = take((size_t)(2 * L.r_max + 2) * 4);
   L.o_agg = take((size_t)2 * L.nchunks * sizeof(MC));
   L.o_tasks = take((size_t)L.max_tasks * 8);
-  L.o_chunkdep = take((size_t)((L.r_max + kOrdChunk - 1) / kOrdChunk + 1) * kMaxDepth * 4);
+  L.o_chunkdep = take((size_t)((L.r_max + kOrdChunkMin - 1) / kOrdChunkMin + 1) * kMaxDepth * 4);
+  L.o_cls = take((size_t)(2 * L.r_max + 2));
   L.o_met = take(sizeof(DevMetrics));
   L.total = off + 256;
   return L;
@@ -186,6 +189,24 @@ int exec_grid(int sms, int* grid_a, size_t* smem_a, int* grid_m, size_t* smem_m)
   return RS_OK;
 }
 
+template <typename K>
+int prep_grid(int sms, size_t smem, int* grid) {
+  static size_t cached_smem[64] = {0};
+  static int cached_occ[64] = {0};
+  int dev;
+  RS_CUDA(cudaGetDevice(&dev));
+  if (cached_smem[dev] != smem) {
+    RS_CUDA(cudaFuncSetAttribute(k_prep<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int o = 0;
+    RS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_prep<K>, 256, smem));
+    if (o < 1) return fail(RS_ECUDA, "prep kernel does not fit on an SM");
+    cached_occ[dev] = o;
+    cached_smem[dev] = smem;
+  }
+  *grid = sms * cached_occ[dev];
+  return RS_OK;
+}
+
 template <typename K, int TB>
 int run_powersort(K* keys, void* tags, int64_t n, int w, int classic, unsigned char* ws, const Layout& L,
                   cudaStream_t st) {
@@ -220,79 +241,59 @@ int run_powersort(K* keys, void* tags, int64_t n, int w, int classic, unsigned c
   uint64_t* tasks = reinterpret_cast<uint64_t*>(at(L.o_tasks));
 
   prof_mark(0, st);
-  RS_CUDA(cudaMemsetAsync(met, 0, sizeof(DevMetrics), st));
-  RS_CUDA(cudaMemsetAsync(done, 0, (size_t)(2 * L.r_max + 2) * 4, st));
-
-  // 1-2: leaves
+  // 1-6: everything before the executors in one cooperative kernel
   int W1 = w + 1;
   int maxw = kMaxWinWords(w);
-  size_t sm_scan = (size_t)maxw * 8 + (size_t)maxw * 2 + 64;
-  k_scan_tables<K><<<(unsigned)L.ntiles, 128, sm_scan, st>>>(keys, n, w, ascw, tables);
-  RS_CUDA(cudaGetLastError());
   int batch = (int)((40 * 1024 - (size_t)W1 * 8) / ((size_t)W1 * 8));
   if (batch < 1) batch = 1;
   if (batch > kTableBatch) batch = kTableBatch;
-  int cthreads = W1 <= 256 ? 256 : (W1 < 1024 ? ((W1 + 31) / 32) * 32 : 1024);
-  size_t sm_comp = (size_t)batch * W1 * 8 + (size_t)W1 * 8 + 64;
-  if (sm_comp > 48 * 1024) RS_CUDA(cudaFuncSetAttribute(k_group_compose, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_comp));
-  k_group_compose<<<(unsigned)L.ngroups, cthreads, sm_comp, st>>>(tables, L.ntiles, w, batch, gtab);
-  RS_CUDA(cudaGetLastError());
-  int gbatch = (int)(96 * 1024 / ((size_t)W1 * 8));
+  int gbatch = (int)(40 * 1024 / ((size_t)W1 * 8));
   if (gbatch < 1) gbatch = 1;
-  if (gbatch > 4096) gbatch = 4096;
-  size_t sm_ge = (size_t)gbatch * W1 * 8;
-  if (sm_ge > 48 * 1024) RS_CUDA(cudaFuncSetAttribute(k_group_entries, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_ge));
-  k_group_entries<<<1, 1024, sm_ge, st>>>(gtab, L.ngroups, w, gbatch, gentry, goff, leaf_start, n, L.r_max, met);
-  RS_CUDA(cudaGetLastError());
-  int tbatch = (int)(48 * 1024 / ((size_t)W1 * 8));
-  if (tbatch < 1) tbatch = 1;
-  if (tbatch > kChainGroup) tbatch = kChainGroup;
-  k_tile_entries<<<(unsigned)L.ngroups, 256, (size_t)tbatch * W1 * 8, st>>>(tables, L.ntiles, w, tbatch, gentry,
-                                                                              goff, tentry, toff);
-  RS_CUDA(cudaGetLastError());
-  size_t sm_emit = (size_t)8 * (maxw * 2 + (maxw + 1) / 2 + 1) * 4;
-  k_emit_leaves<<<(unsigned)((L.ntiles + 7) / 8), 256, sm_emit, st>>>(ascw, n, w, L.ntiles, tentry, toff, L.r_max,
-                                                                      leaf_start, leaf_info);
-  RS_CUDA(cudaGetLastError());
-  prof_mark(1, st);
-
-  // 3-5: tree
+  int tbatch = gbatch < kChainGroup ? gbatch : kChainGroup;
+  size_t sm = 8 * (size_t)chain_warp_bytes(w, sizeof(K));
+  sm = std::max(sm, (size_t)kOrdChunkMax * 5 + 64);
+  sm = std::max(sm, (size_t)batch * W1 * 8 + (size_t)W1 * 8 + 64);
+  sm = std::max(sm, (size_t)gbatch * W1 * 8);
+  sm = std::max(sm, (size_t)tbatch * W1 * 8);
+  sm = std::max(sm, (size_t)8 * (maxw * 2 + (maxw + 1) / 2 + 1) * 4);
   int F = n <= ((int64_t)1 << 31) ? 32 : 63;
-  int64_t gs = (L.r_max + 255) / 256;
-  unsigned grid_r = (unsigned)(gs < (int64_t)sms * 8 ? gs : (int64_t)sms * 8);
-  if (grid_r == 0) grid_r = 1;
-  k_keys_powers<<<grid_r, 256, 0, st>>>(leaf_start, n, F, met, Kk, P);
-  RS_CUDA(cudaGetLastError());
-  int64_t gc = 2 * L.nchunks;
-  unsigned grid_c = (unsigned)(gc < (int64_t)sms * 4 ? gc : (int64_t)sms * 4);
-  k_scan_reduce<<<grid_c, kScanThreads, 0, st>>>(P, met, agg, L.nchunks);
-  RS_CUDA(cudaGetLastError());
-  k_scan_top<<<2, 1024, 0, st>>>(met, agg, L.nchunks);
-  RS_CUDA(cudaGetLastError());
-  k_scan_down<<<grid_c, kScanThreads, 0, st>>>(P, met, agg, L.nchunks, la, ra);
-  RS_CUDA(cudaGetLastError());
-  TreeArrays T{leaf_start, leaf_info, Kk, P, la, ra, depth, leaf_depth, node_a, node_b,
-               parent, child, node_s, node_e, L.leaf_base};
-  k_tree<<<grid_r, 256, 0, st>>>(T, F, met);
-  RS_CUDA(cudaGetLastError());
-  prof_mark(2, st);
-
-  // 6: tasks
-  ClassifyArgs CA{n, w, classic, L.fcap, L.tile, MergeCfg<K, TB>::TILE, kSuper, L.leaf_base, leaf_start, leaf_info, leaf_depth, depth,
-                  node_s, node_e, parent, need, tasks, met};
   uint32_t* chunkdep = reinterpret_cast<uint32_t*>(at(L.o_chunkdep));
-  int64_t nch_max = (L.r_max + kOrdChunk - 1) / kOrdChunk;
-  RS_CUDA(cudaMemsetAsync(chunkdep, 0, (size_t)(nch_max + 1) * kMaxDepth * 4, st));
-  unsigned grid_o = (unsigned)(nch_max < (int64_t)sms * 4 ? nch_max : (int64_t)sms * 4);
-  if (grid_o == 0) grid_o = 1;
-  k_classify<<<grid_r, 256, 0, st>>>(CA, chunkdep);
-  RS_CUDA(cudaGetLastError());
-  k_task_offsets<<<1, 32, 0, st>>>(met);
-  RS_CUDA(cudaGetLastError());
-  k_order_scan<<<1, kMaxDepth, 0, st>>>(met, chunkdep);
-  RS_CUDA(cudaGetLastError());
-  k_task_fill<<<grid_o, 256, 0, st>>>(CA, chunkdep);
-  RS_CUDA(cudaGetLastError());
+  int64_t nch_max = (L.r_max + kOrdChunkMin - 1) / kOrdChunkMin;
+  PrepArgs PA;
+  PA.keys = keys;
+  PA.n = n;
+  PA.w = w;
+  PA.F = F;
+  PA.batch = batch;
+  PA.gbatch = gbatch;
+  PA.tbatch = tbatch;
+  PA.ntiles = L.ntiles;
+  PA.ngroups = L.ngroups;
+  PA.r_max = L.r_max;
+  PA.nchunks = L.nchunks;
+  PA.ascw = ascw;
+  PA.tables = tables;
+  PA.gtab = gtab;
+  PA.gentry = gentry;
+  PA.goff = goff;
+  PA.tentry = tentry;
+  PA.toff = toff;
+  PA.agg = agg;
+  PA.chunkdep = chunkdep;
+  PA.chunkdep_words = (nch_max + 1) * kMaxDepth;
+  PA.done = done;
+  PA.done_words = 2 * L.r_max + 2;
+  PA.T = TreeArrays{leaf_start, leaf_info, Kk, P, la, ra, depth, leaf_depth, node_a, node_b,
+                    parent, child, node_s, node_e, L.leaf_base};
+  PA.CA = ClassifyArgs{n, w, classic, L.fcap, L.tile, MergeCfg<K, TB>::TILE, kSuper, L.leaf_base,
+                       leaf_start, leaf_info, leaf_depth, depth, node_s, node_e, parent, need,
+                       reinterpret_cast<uint8_t*>(at(L.o_cls)), tasks, met};
+  int grid_p;
+  if (int e = prep_grid<K>(sms, sm, &grid_p)) return e;
+  void* kargs[] = {&PA};
+  RS_CUDA(cudaLaunchCooperativeKernel((void*)k_prep<K>, dim3(grid_p), dim3(256), kargs, sm, st));
+  prof_mark(1, st);
+  prof_mark(2, st);
   prof_mark(3, st);
 
   // 7: execute
@@ -519,6 +520,7 @@ int rs_debug_counters(int key_dtype, int tag_bytes, int64_t n, int32_t min_run_l
   if (k < cap) out[k++] = hm.phaseA;
   for (int d = 0; d < kMaxDepth && k < cap; ++d) out[k++] = hm.depth_wait[d];
   for (int d = 0; d < kMaxDepth && k < cap; ++d) out[k++] = hm.depth_tiles[d];
+  for (int d = 0; d < 16 && k < cap; ++d) out[k++] = hm.prep_ts[d];
   return k;
 }
 
