@@ -25,7 +25,7 @@
 
 namespace rs {
 
-constexpr int kSuper = 1;              // tiles per merge task
+constexpr int kSuperMax = 15;          // tiles per merge task: runtime, <= 15 (lane groups of >= 2)
 constexpr int kStages = 2;             // smem ring depth
 constexpr int kHold = 1;               // producer's out-of-order task window
 constexpr int kConsumerThreads = 256;  // 8 consumer warps
@@ -63,6 +63,7 @@ struct MergeArgs {
   void* key[2];
   void* tag[2];
   int classic;
+  int msuper;  // merge tiles per task (ClassifyArgs::msuper)
   const pos_t* leaf_start;
   const uint8_t* depth;
   const pos_t* node_s;
@@ -157,7 +158,7 @@ __device__ int64_t warp_count(const K* A, int64_t len, K v, bool or_equal) {
 }
 
 template <typename K, int TB>
-__global__ void __launch_bounds__(kMergeThreads) k_merge_exec(MergeArgs E) {
+__global__ void __launch_bounds__(kMergeThreads, 3) k_merge_exec(MergeArgs E) {
   using C = MergeCfg<K, TB>;
   using T = typename TagT<TB>::type;
   constexpr bool HT = TB != 0;
@@ -185,6 +186,7 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge_exec(MergeArgs E) {
     unsigned long long comps = 0;
     int stage = 0;
     uint32_t phase = 0;  // flips when stage wraps
+    const int kSuper = E.msuper;
     const int G = 32 / (kSuper + 1);
     // Small out-of-order window: up to kHold claimed tasks are held and the
     // oldest one whose children are complete is prepared first.  Every held

@@ -207,6 +207,19 @@ int prep_grid(int sms, size_t smem, int* grid) {
   return RS_OK;
 }
 
+// Tiles per merge task: enough tasks per tree level to keep every executor
+// CTA busy (>= ~8 per CTA), as many tiles as that allows so the producer's
+// split searches (one HBM round trip per step) are shared by more tiles.
+template <typename K, int TB>
+int merge_super(int64_t n, int sms) {
+  int64_t ctas = (int64_t)sms * 3;
+  int64_t per_level_tiles = n / MergeCfg<K, TB>::TILE;
+  int64_t s = per_level_tiles / (8 * ctas);
+  if (s < 1) s = 1;
+  if (s > 7) s = 7;
+  return (int)s;
+}
+
 template <typename K, int TB>
 int run_powersort(K* keys, void* tags, int64_t n, int w, int classic, unsigned char* ws, const Layout& L,
                   cudaStream_t st) {
@@ -285,7 +298,8 @@ int run_powersort(K* keys, void* tags, int64_t n, int w, int classic, unsigned c
   PA.done_words = 2 * L.r_max + 2;
   PA.T = TreeArrays{leaf_start, leaf_info, Kk, P, la, ra, depth, leaf_depth, node_a, node_b,
                     parent, child, node_s, node_e, L.leaf_base};
-  PA.CA = ClassifyArgs{n, w, classic, L.fcap, L.tile, MergeCfg<K, TB>::TILE, kSuper, L.leaf_base,
+  int msuper = merge_super<K, TB>(n, sms);
+  PA.CA = ClassifyArgs{n, w, classic, L.fcap, L.tile, MergeCfg<K, TB>::TILE, msuper, L.leaf_base,
                        leaf_start, leaf_info, leaf_depth, depth, node_s, node_e, parent, need,
                        reinterpret_cast<uint8_t*>(at(L.o_cls)), tasks, met};
   int grid_p;
@@ -330,6 +344,7 @@ int run_powersort(K* keys, void* tags, int64_t n, int w, int classic, unsigned c
   M.tag[0] = E.tag[0];
   M.tag[1] = E.tag[1];
   M.classic = classic;
+  M.msuper = msuper;
   M.leaf_start = leaf_start;
   M.depth = depth;
   M.node_s = node_s;
