@@ -185,7 +185,8 @@ def run_ours(args, rank, world, local_rank):
                    runs_detected=int(m.runs_detected), max_stack_height=int(m.max_stack_height))
 
     L.rs_profile(1)
-    phase = np.zeros(4)
+    phase = np.zeros(3)
+    exec_elems = None
     for _ in range(args.warmup):
         work.copy_(src)
         if twork is not None:
@@ -216,9 +217,11 @@ def run_ours(args, rank, world, local_rank):
         e1.synchronize()
         total_ms += e0.elapsed_time(e1)
         k = L.rs_profile_read(buf, 4)
+        if k >= 3:
+            phase += np.array(buf[:3])
+            exec_ms.append(buf[2])
         if k == 4:
-            phase += np.array(buf[:4])
-            exec_ms.append(buf[3])
+            exec_elems = int(buf[3])
     torch.cuda.synchronize()
     L.rs_profile(0)
     clk = clocks.stop()
@@ -253,10 +256,20 @@ def run_ours(args, rank, world, local_rank):
     ok = bool(np.all(hk.numpy()[:-1] <= hk.numpy()[1:]))
 
     peak, peak_src = hbm_peak()
-    alg_bytes = 2.0 * B * (metrics["merge_cost"] + n)
+    # merge executor: every element of every merge it runs is read + written once
+    alg_bytes = 2.0 * B * (exec_elems if exec_elems is not None else metrics["merge_cost"])
+    whole_bytes = 2.0 * B * (metrics["merge_cost"] + n)  # + one leaf-formation pass
     exec_avg = float(np.mean(exec_ms)) if exec_ms else float("nan")
     achieved = alg_bytes / (exec_avg / 1e3) / 1e9
-    whole = alg_bytes / (ms_step / 1e3) / 1e9
+    whole = whole_bytes / (ms_step / 1e3) / 1e9
+    traffic = None
+    try:
+        tj = json.load(open(os.path.join(REPO, "profiles", "traffic.json")))
+        t = tj.get(f"cfg{args.config}")
+        if t:
+            traffic = t["dram_read_bytes"] + t["dram_write_bytes"]
+    except Exception:
+        pass
     out = {
         "metric": METRIC,
         "value": value,
@@ -279,14 +292,15 @@ def run_ours(args, rank, world, local_rank):
         },
         "sorted_ok": ok,
         "metrics": metrics,
-        "phase_ms": {k: float(v / max(1, len(exec_ms))) for k, v in zip(["prep", "unused1", "unused2", "execute"], phase)},
+        "phase_ms": {k: float(v / max(1, len(exec_ms))) for k, v in zip(["prep", "phaseA", "merge"], phase)},
         "gpu_launches": KERNELS_PER_SORT * args.steps,
         "e2e": {"value": n * world / (e2e_step / 1e3), "unit": "keys/s", "ms_per_step": e2e_step,
                 "h2d_bytes_per_step": n * B, "d2h_bytes_per_step": n * B + 32},
-        "roofline": {"bound": "hbm", "kernel": "k_execute (leaf formation + all merges)",
+        "roofline": {"bound": "hbm", "kernel": "k_merge_exec (all merges of the large tree nodes)",
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": None, "algorithmic_bytes_per_launch": alg_bytes,
-                     "whole_sort_frac": whole / peak, "peak_source": peak_src},
+                     "traffic": traffic, "traffic_source": "profiles/traffic.json (ncu --set full, one launch)",
+                     "algorithmic_bytes_per_launch": alg_bytes, "merged_elements_per_launch": exec_elems,
+                     "whole_sort_achieved": whole, "whole_sort_frac": whole / peak, "peak_source": peak_src},
         "clocks": clk,
     }
     return out
@@ -314,6 +328,7 @@ def main():
     ap.add_argument("--n", type=int, default=None)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sharded", action="store_true", help="use the multi-GPU sharded path even at N=1")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -337,11 +352,16 @@ def main():
         print(json.dumps(out))
         return 0
 
-    if world > 1:
+    if world > 1 or args.sharded:
         import torch
         import torch.distributed as dist
 
         torch.cuda.set_device(local_rank)
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl")
         from paper_1805_04154_b200 import dist as rsdist
 

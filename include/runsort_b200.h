@@ -95,9 +95,12 @@ int rs_sort_host(int algo, int key_dtype, void* keys, int tag_bytes, void* tags,
                  int32_t min_run_len, int32_t merge_kind, rs_metrics* out, rs_tree* tree);
 
 /* Per-phase CUDA-event timing of subsequent rs_sort calls on this thread
- * (phases: leaves, tree, tasks, execute; events recorded on the sort's own
- * stream).  rs_profile_read waits for the last profiled call and writes up to
- * `cap` phase durations in milliseconds; returns the number written. */
+ * (events recorded on the sort's own stream).  rs_profile_read waits for the
+ * last profiled call and writes up to `cap` values: the durations in ms of
+ * [0] prep (run detection, min-run chain, merge tree, task list),
+ * [1] phase A (fused small subtrees + large-leaf formation), [2] the merge
+ * executor, then [3] the number of elements the merge executor merged
+ * (its share of merge_cost).  Returns the number of values written. */
 int rs_profile(int enable);
 int rs_profile_read(double* ms, int cap);
 

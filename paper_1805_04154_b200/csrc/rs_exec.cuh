@@ -136,7 +136,7 @@ __device__ void d_classify(ClassifyArgs A, uint32_t* __restrict__ chunk_depth) {
   __shared__ unsigned long long sred[32];
   int64_t r = (int64_t)A.met->n_leaves;
   const int64_t ochunk = ord_chunk(r);
-  unsigned long long comps = 0, mcost = 0, cntA = 0;
+  unsigned long long comps = 0, mcost = 0, cntA = 0, mbig = 0;
   unsigned maxd = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < r; i += (int64_t)gridDim.x * blockDim.x) {
     // leaf: detection comparisons (runcore.py:154/157 closed form)
@@ -163,6 +163,7 @@ __device__ void d_classify(ClassifyArgs A, uint32_t* __restrict__ chunk_depth) {
       if (cn == 1) { A.need[i] = 1; cntA += 1; }
       else if (cn == 2) {
         A.need[i] = (uint32_t)tn;
+        mbig += span;
         int d = A.depth[i];
         atomicAdd(&chunk_depth[(i / ochunk) * kMaxDepth + d], (uint32_t)tk);
         atomicAdd(&A.met->depth_tiles[d], (unsigned long long)tk);
@@ -176,6 +177,8 @@ __device__ void d_classify(ClassifyArgs A, uint32_t* __restrict__ chunk_depth) {
   if (threadIdx.x == 0 && s) atomicAdd(&A.met->merge_cost, s);
   s = block_sum(cntA, sred);
   if (threadIdx.x == 0 && s) atomicAdd(&A.met->phaseA, s);
+  s = block_sum(mbig, sred);
+  if (threadIdx.x == 0 && s) atomicAdd(&A.met->merge_cost_exec, s);
   maxd = warp_max(maxd);
   if ((threadIdx.x & 31) == 0 && maxd) atomicMax(&A.met->max_depth, (unsigned long long)maxd);
 }

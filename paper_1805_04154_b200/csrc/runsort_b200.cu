@@ -31,12 +31,13 @@ namespace {
 
 thread_local std::string g_err;
 
-constexpr int kPhases = 4;
+constexpr int kPhases = 3;  // prep, phase A, merge
 struct Prof {
   bool on = false;
   bool created = false;
   bool recorded = false;
   cudaEvent_t ev[kPhases + 1];
+  const DevMetrics* met = nullptr;  // of the last profiled call
 };
 thread_local Prof g_prof;
 
@@ -48,6 +49,9 @@ void prof_mark(int i, cudaStream_t st) {
   }
   cudaEventRecord(g_prof.ev[i], st);
   if (i == kPhases) g_prof.recorded = true;
+}
+void prof_set_met(const DevMetrics* m) {
+  if (g_prof.on) g_prof.met = m;
 }
 
 int fail(int code, const std::string& msg) {
@@ -254,6 +258,7 @@ int run_powersort(K* keys, void* tags, int64_t n, int w, int classic, unsigned c
   uint64_t* tasks = reinterpret_cast<uint64_t*>(at(L.o_tasks));
 
   prof_mark(0, st);
+  prof_set_met(met);
   // 1-6: everything before the executors in one cooperative kernel
   int W1 = w + 1;
   int maxw = kMaxWinWords(w);
@@ -307,8 +312,6 @@ int run_powersort(K* keys, void* tags, int64_t n, int w, int classic, unsigned c
   void* kargs[] = {&PA};
   RS_CUDA(cudaLaunchCooperativeKernel((void*)k_prep<K>, dim3(grid_p), dim3(256), kargs, sm, st));
   prof_mark(1, st);
-  prof_mark(2, st);
-  prof_mark(3, st);
 
   // 7: execute
   int grid_a, grid_m;
@@ -338,6 +341,7 @@ int run_powersort(K* keys, void* tags, int64_t n, int w, int classic, unsigned c
   E.met = met;
   k_phaseA<K, TB><<<grid_a, kExecThreads, smem_a, st>>>(E);
   RS_CUDA(cudaGetLastError());
+  prof_mark(2, st);
   MergeArgs M;
   M.key[0] = E.key[0];
   M.key[1] = E.key[1];
@@ -356,7 +360,7 @@ int run_powersort(K* keys, void* tags, int64_t n, int w, int classic, unsigned c
   M.met = met;
   k_merge_exec<K, TB><<<grid_m, kMergeThreads, smem_m, st>>>(M);
   RS_CUDA(cudaGetLastError());
-  prof_mark(4, st);
+  prof_mark(3, st);
   return RS_OK;
 }
 
@@ -557,6 +561,10 @@ int rs_profile_read(double* ms, int cap) {
     float t = 0.f;
     cudaEventElapsedTime(&t, g_prof.ev[i], g_prof.ev[i + 1]);
     ms[k++] = t;
+  }
+  if (k < cap && g_prof.met) {
+    unsigned long long v = 0;
+    if (cudaMemcpy(&v, &g_prof.met->merge_cost_exec, 8, cudaMemcpyDeviceToHost) == cudaSuccess) ms[k++] = (double)v;
   }
   return k;
 }
