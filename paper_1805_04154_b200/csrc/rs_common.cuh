@@ -56,6 +56,7 @@ struct DevMetrics {
   unsigned long long depth_wait[kMaxDepth];  // RS_INSTR: producer dependency-wait cycles per depth
   unsigned long long prep_ts[16];            // RS_INSTR: globaltimer at each prep phase boundary
   unsigned int last_ctr[8];                  // 'last block done' counters of the prep kernel
+  unsigned long long peek[8];                // peeksort replay counters (frontier sizes, records)
 };
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {

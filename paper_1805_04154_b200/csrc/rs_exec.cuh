@@ -79,6 +79,7 @@ struct ClassifyArgs {
   int tile;   // leaf-tile granularity (phase A)
   int mtile;  // merge-tile granularity (merge executor)
   int msuper; // merge tiles per merge task
+  int peek;   // peeksort: run-detection comparisons were counted during the replay
   uint32_t leaf_base;
   const pos_t* leaf_start;
   const uint32_t* leaf_info;
@@ -141,7 +142,7 @@ __device__ void d_classify(ClassifyArgs A, uint32_t* __restrict__ chunk_depth) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < r; i += (int64_t)gridDim.x * blockDim.x) {
     // leaf: detection comparisons (runcore.py:154/157 closed form)
     pos_t s0 = A.leaf_start[i], len = A.leaf_start[i + 1] - s0;
-    if (s0 < A.n - 1) {
+    if (!A.peek && s0 < A.n - 1) {
       uint32_t nl = A.leaf_info[i] & 0x7fffffffu;
       pos_t L = (nl >= (uint32_t)A.w) ? len : (pos_t)nl;
       pos_t ne = s0 + L - 1;

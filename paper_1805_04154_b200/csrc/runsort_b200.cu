@@ -23,6 +23,7 @@
 #include "rs_exec.cuh"
 #include "rs_merge.cuh"
 #include "rs_prep.cuh"
+#include "rs_peek.cuh"
 #include "rs_tree.cuh"
 
 using namespace rs;
@@ -81,6 +82,10 @@ struct Layout {
   size_t o_leaf_start, o_leaf_info, o_leaf_depth, o_K, o_P, o_la, o_ra, o_depth;
   size_t o_node_a, o_node_b, o_node_s, o_node_e, o_parent, o_child, o_need, o_done;
   size_t o_agg, o_tasks, o_chunkdep, o_cls, o_met, total;
+  // peeksort replay
+  int algo;
+  int64_t front_cap, rec_cap, sum_words, wchunks;
+  size_t o_front0, o_front1, o_pnodes, o_pleaves, o_prevs, o_lbits, o_wpre, o_wchunk, o_nozero, o_noone;
 };
 
 int exec_tile(int kb, int tb) {
@@ -92,8 +97,9 @@ int exec_fcap(int kb, int tb) {
   return tb == 0 ? ExecCfg<int64_t, 0>::FCAP : (tb == 4 ? ExecCfg<int64_t, 4>::FCAP : ExecCfg<int64_t, 8>::FCAP);
 }
 
-Layout make_layout(int64_t n, int w, int kb, int tb) {
+Layout make_layout(int64_t n, int w, int kb, int tb, int algo) {
   Layout L{};
+  L.algo = algo;
   L.n = n;
   L.w = w;
   L.kb = kb;
@@ -105,7 +111,7 @@ Layout make_layout(int64_t n, int w, int kb, int tb) {
   L.ngroups = (L.ntiles + kChainGroup - 1) / kChainGroup;
   int64_t minleaf = w > 2 ? w : 2;
   L.r_max = n / minleaf + 2;
-  if (L.r_max > n + 1) L.r_max = n + 1;
+  if (L.r_max > n + 1 || algo == RS_ALGO_PEEKSORT) L.r_max = n + 1;  // peeksort leaves can be single elements
   L.leaf_base = (uint32_t)(L.r_max + 1);
   L.nchunks = (L.r_max + kScanThreads - 1) / kScanThreads + 1;
   int levels = 2;
@@ -120,8 +126,9 @@ Layout make_layout(int64_t n, int w, int kb, int tb) {
   L.o_key1 = take((size_t)n * kb + 64);
   L.o_tag1 = take((size_t)n * tb + 64);
   L.o_ascw = take((size_t)L.words * 4);
-  L.o_tables = take((size_t)L.ntiles * (w + 1) * 8);
-  L.o_gtab = take((size_t)L.ngroups * (w + 1) * 8);
+  bool pk = algo == RS_ALGO_PEEKSORT;
+  L.o_tables = take(pk ? 0 : (size_t)L.ntiles * (w + 1) * 8);
+  L.o_gtab = take(pk ? 0 : (size_t)L.ngroups * (w + 1) * 8);
   L.o_gentry = take((size_t)L.ngroups * 4);
   L.o_goff = take((size_t)L.ngroups * 8);
   L.o_tentry = take((size_t)L.ntiles * 4);
@@ -146,6 +153,22 @@ Layout make_layout(int64_t n, int w, int kb, int tb) {
   L.o_tasks = take((size_t)L.max_tasks * 8);
   L.o_chunkdep = take((size_t)((L.r_max + kOrdChunkMin - 1) / kOrdChunkMin + 1) * kMaxDepth * 4);
   L.o_cls = take((size_t)(2 * L.r_max + 2));
+  if (pk) {
+    L.front_cap = n + 1;
+    L.rec_cap = n + 1;
+    L.sum_words = (L.words + 31) / 32 + 2;
+    L.wchunks = (L.words + kWordChunk - 1) / kWordChunk + 1;
+    L.o_front0 = take((size_t)L.front_cap * sizeof(PeekItem));
+    L.o_front1 = take((size_t)L.front_cap * sizeof(PeekItem));
+    L.o_pnodes = take((size_t)L.rec_cap * 32);
+    L.o_pleaves = take((size_t)L.rec_cap * 32);
+    L.o_prevs = take((size_t)L.rec_cap * 16);
+    L.o_lbits = take((size_t)L.words * 4);
+    L.o_wpre = take((size_t)L.words * 4);
+    L.o_wchunk = take((size_t)L.wchunks * 4);
+    L.o_nozero = take((size_t)L.sum_words * 4);
+    L.o_noone = take((size_t)L.sum_words * 4);
+  }
   L.o_met = take(sizeof(DevMetrics));
   L.total = off + 256;
   return L;
@@ -224,42 +247,131 @@ int merge_super(int64_t n, int sms) {
   return (int)s;
 }
 
+struct WsView {
+  DevMetrics* met;
+  uint32_t *ascw, *gentry, *tentry, *need, *done, *child, *chunkdep;
+  uint2 *tables, *gtab;
+  uint64_t *goff, *toff, *Kk, *tasks;
+  pos_t *leaf_start, *node_s, *node_e;
+  uint32_t* leaf_info;
+  uint8_t *leaf_depth, *P, *la, *ra, *depth, *cls;
+  int32_t *node_a, *node_b, *parent;
+  MC* agg;
+  void* key1;
+  void* tag1;
+};
+
+WsView view(unsigned char* ws, const Layout& L) {
+  auto at = [&](size_t o) { return ws + o; };
+  WsView V;
+  V.met = reinterpret_cast<DevMetrics*>(at(L.o_met));
+  V.ascw = reinterpret_cast<uint32_t*>(at(L.o_ascw));
+  V.tables = reinterpret_cast<uint2*>(at(L.o_tables));
+  V.gtab = reinterpret_cast<uint2*>(at(L.o_gtab));
+  V.gentry = reinterpret_cast<uint32_t*>(at(L.o_gentry));
+  V.goff = reinterpret_cast<uint64_t*>(at(L.o_goff));
+  V.tentry = reinterpret_cast<uint32_t*>(at(L.o_tentry));
+  V.toff = reinterpret_cast<uint64_t*>(at(L.o_toff));
+  V.leaf_start = reinterpret_cast<pos_t*>(at(L.o_leaf_start));
+  V.leaf_info = reinterpret_cast<uint32_t*>(at(L.o_leaf_info));
+  V.leaf_depth = at(L.o_leaf_depth);
+  V.Kk = reinterpret_cast<uint64_t*>(at(L.o_K));
+  V.P = at(L.o_P);
+  V.la = at(L.o_la);
+  V.ra = at(L.o_ra);
+  V.depth = at(L.o_depth);
+  V.node_a = reinterpret_cast<int32_t*>(at(L.o_node_a));
+  V.node_b = reinterpret_cast<int32_t*>(at(L.o_node_b));
+  V.node_s = reinterpret_cast<pos_t*>(at(L.o_node_s));
+  V.node_e = reinterpret_cast<pos_t*>(at(L.o_node_e));
+  V.parent = reinterpret_cast<int32_t*>(at(L.o_parent));
+  V.child = reinterpret_cast<uint32_t*>(at(L.o_child));
+  V.need = reinterpret_cast<uint32_t*>(at(L.o_need));
+  V.done = reinterpret_cast<uint32_t*>(at(L.o_done));
+  V.agg = reinterpret_cast<MC*>(at(L.o_agg));
+  V.tasks = reinterpret_cast<uint64_t*>(at(L.o_tasks));
+  V.chunkdep = reinterpret_cast<uint32_t*>(at(L.o_chunkdep));
+  V.cls = reinterpret_cast<uint8_t*>(at(L.o_cls));
+  V.key1 = at(L.o_key1);
+  V.tag1 = at(L.o_tag1);
+  return V;
+}
+
+TreeArrays tree_arrays(const WsView& V, const Layout& L) {
+  return TreeArrays{V.leaf_start, V.leaf_info, V.Kk, V.P, V.la, V.ra, V.depth, V.leaf_depth, V.node_a,
+                    V.node_b, V.parent, V.child, V.node_s, V.node_e, L.leaf_base};
+}
+
+template <typename K, int TB>
+ClassifyArgs classify_args(const WsView& V, const Layout& L, int64_t n, int w, int classic, int msuper, int peek) {
+  return ClassifyArgs{n, w, classic, L.fcap, L.tile, MergeCfg<K, TB>::TILE, msuper, peek, L.leaf_base,
+                      V.leaf_start, V.leaf_info, V.leaf_depth, V.depth, V.node_s, V.node_e, V.parent, V.need,
+                      V.cls, V.tasks, V.met};
+}
+
+// Phase A (fused subtrees, large leaves) + the merge executor.
+template <typename K, int TB>
+int launch_exec(K* keys, void* tags, int64_t n, int w, int classic, int msuper, const WsView& V, const Layout& L,
+                int sms, cudaStream_t st) {
+  int grid_a, grid_m;
+  size_t smem_a, smem_m;
+  if (int e = exec_grid<K, TB>(sms, &grid_a, &smem_a, &grid_m, &smem_m)) return e;
+  ExecArgs E;
+  E.key[0] = keys;
+  E.key[1] = V.key1;
+  E.tag[0] = tags;
+  E.tag[1] = V.tag1;
+  E.n = n;
+  E.w = w;
+  E.classic = classic;
+  E.leaf_base = L.leaf_base;
+  E.leaf_start = V.leaf_start;
+  E.leaf_info = V.leaf_info;
+  E.leaf_depth = V.leaf_depth;
+  E.depth = V.depth;
+  E.node_a = V.node_a;
+  E.node_b = V.node_b;
+  E.node_s = V.node_s;
+  E.node_e = V.node_e;
+  E.child = V.child;
+  E.need = V.need;
+  E.done = V.done;
+  E.tasks = V.tasks;
+  E.met = V.met;
+  k_phaseA<K, TB><<<grid_a, kExecThreads, smem_a, st>>>(E);
+  RS_CUDA(cudaGetLastError());
+  prof_mark(2, st);
+  MergeArgs M;
+  M.key[0] = E.key[0];
+  M.key[1] = E.key[1];
+  M.tag[0] = E.tag[0];
+  M.tag[1] = E.tag[1];
+  M.classic = classic;
+  M.msuper = msuper;
+  M.leaf_start = V.leaf_start;
+  M.depth = V.depth;
+  M.node_s = V.node_s;
+  M.node_e = V.node_e;
+  M.child = V.child;
+  M.need = V.need;
+  M.done = V.done;
+  M.tasks = V.tasks;
+  M.met = V.met;
+  k_merge_exec<K, TB><<<grid_m, kMergeThreads, smem_m, st>>>(M);
+  RS_CUDA(cudaGetLastError());
+  prof_mark(3, st);
+  return RS_OK;
+}
+
 template <typename K, int TB>
 int run_powersort(K* keys, void* tags, int64_t n, int w, int classic, unsigned char* ws, const Layout& L,
                   cudaStream_t st) {
   int sms;
   if (int e = device_sms(&sms)) return e;
-  auto at = [&](size_t o) { return ws + o; };
-  DevMetrics* met = reinterpret_cast<DevMetrics*>(at(L.o_met));
-  uint32_t* ascw = reinterpret_cast<uint32_t*>(at(L.o_ascw));
-  uint2* tables = reinterpret_cast<uint2*>(at(L.o_tables));
-  uint2* gtab = reinterpret_cast<uint2*>(at(L.o_gtab));
-  uint32_t* gentry = reinterpret_cast<uint32_t*>(at(L.o_gentry));
-  uint64_t* goff = reinterpret_cast<uint64_t*>(at(L.o_goff));
-  uint32_t* tentry = reinterpret_cast<uint32_t*>(at(L.o_tentry));
-  uint64_t* toff = reinterpret_cast<uint64_t*>(at(L.o_toff));
-  pos_t* leaf_start = reinterpret_cast<pos_t*>(at(L.o_leaf_start));
-  uint32_t* leaf_info = reinterpret_cast<uint32_t*>(at(L.o_leaf_info));
-  uint8_t* leaf_depth = at(L.o_leaf_depth);
-  uint64_t* Kk = reinterpret_cast<uint64_t*>(at(L.o_K));
-  uint8_t* P = at(L.o_P);
-  uint8_t* la = at(L.o_la);
-  uint8_t* ra = at(L.o_ra);
-  uint8_t* depth = at(L.o_depth);
-  int32_t* node_a = reinterpret_cast<int32_t*>(at(L.o_node_a));
-  int32_t* node_b = reinterpret_cast<int32_t*>(at(L.o_node_b));
-  pos_t* node_s = reinterpret_cast<pos_t*>(at(L.o_node_s));
-  pos_t* node_e = reinterpret_cast<pos_t*>(at(L.o_node_e));
-  int32_t* parent = reinterpret_cast<int32_t*>(at(L.o_parent));
-  uint32_t* child = reinterpret_cast<uint32_t*>(at(L.o_child));
-  uint32_t* need = reinterpret_cast<uint32_t*>(at(L.o_need));
-  uint32_t* done = reinterpret_cast<uint32_t*>(at(L.o_done));
-  MC* agg = reinterpret_cast<MC*>(at(L.o_agg));
-  uint64_t* tasks = reinterpret_cast<uint64_t*>(at(L.o_tasks));
-
+  WsView V = view(ws, L);
   prof_mark(0, st);
-  prof_set_met(met);
-  // 1-6: everything before the executors in one cooperative kernel
+  prof_set_met(V.met);
+  // everything before the executors in one cooperative kernel
   int W1 = w + 1;
   int maxw = kMaxWinWords(w);
   int batch = (int)((40 * 1024 - (size_t)W1 * 8) / ((size_t)W1 * 8));
@@ -275,7 +387,6 @@ int run_powersort(K* keys, void* tags, int64_t n, int w, int classic, unsigned c
   sm = std::max(sm, (size_t)tbatch * W1 * 8);
   sm = std::max(sm, (size_t)8 * (maxw * 2 + (maxw + 1) / 2 + 1) * 4);
   int F = n <= ((int64_t)1 << 31) ? 32 : 63;
-  uint32_t* chunkdep = reinterpret_cast<uint32_t*>(at(L.o_chunkdep));
   int64_t nch_max = (L.r_max + kOrdChunkMin - 1) / kOrdChunkMin;
   PrepArgs PA;
   PA.keys = keys;
@@ -289,79 +400,80 @@ int run_powersort(K* keys, void* tags, int64_t n, int w, int classic, unsigned c
   PA.ngroups = L.ngroups;
   PA.r_max = L.r_max;
   PA.nchunks = L.nchunks;
-  PA.ascw = ascw;
-  PA.tables = tables;
-  PA.gtab = gtab;
-  PA.gentry = gentry;
-  PA.goff = goff;
-  PA.tentry = tentry;
-  PA.toff = toff;
-  PA.agg = agg;
-  PA.chunkdep = chunkdep;
+  PA.ascw = V.ascw;
+  PA.tables = V.tables;
+  PA.gtab = V.gtab;
+  PA.gentry = V.gentry;
+  PA.goff = V.goff;
+  PA.tentry = V.tentry;
+  PA.toff = V.toff;
+  PA.agg = V.agg;
+  PA.chunkdep = V.chunkdep;
   PA.chunkdep_words = (nch_max + 1) * kMaxDepth;
-  PA.done = done;
+  PA.done = V.done;
   PA.done_words = 2 * L.r_max + 2;
-  PA.T = TreeArrays{leaf_start, leaf_info, Kk, P, la, ra, depth, leaf_depth, node_a, node_b,
-                    parent, child, node_s, node_e, L.leaf_base};
+  PA.T = tree_arrays(V, L);
   int msuper = merge_super<K, TB>(n, sms);
-  PA.CA = ClassifyArgs{n, w, classic, L.fcap, L.tile, MergeCfg<K, TB>::TILE, msuper, L.leaf_base,
-                       leaf_start, leaf_info, leaf_depth, depth, node_s, node_e, parent, need,
-                       reinterpret_cast<uint8_t*>(at(L.o_cls)), tasks, met};
+  PA.CA = classify_args<K, TB>(V, L, n, w, classic, msuper, 0);
   int grid_p;
   if (int e = prep_grid<K>(sms, sm, &grid_p)) return e;
   void* kargs[] = {&PA};
   RS_CUDA(cudaLaunchCooperativeKernel((void*)k_prep<K>, dim3(grid_p), dim3(256), kargs, sm, st));
   prof_mark(1, st);
+  return launch_exec<K, TB>(keys, tags, n, w, classic, msuper, V, L, sms, st);
+}
 
-  // 7: execute
-  int grid_a, grid_m;
-  size_t smem_a, smem_m;
-  if (int e = exec_grid<K, TB>(sms, &grid_a, &smem_a, &grid_m, &smem_m)) return e;
-  ExecArgs E;
-  E.key[0] = keys;
-  E.key[1] = at(L.o_key1);
-  E.tag[0] = tags;
-  E.tag[1] = at(L.o_tag1);
-  E.n = n;
-  E.w = w;
-  E.classic = classic;
-  E.leaf_base = L.leaf_base;
-  E.leaf_start = leaf_start;
-  E.leaf_info = leaf_info;
-  E.leaf_depth = leaf_depth;
-  E.depth = depth;
-  E.node_a = node_a;
-  E.node_b = node_b;
-  E.node_s = node_s;
-  E.node_e = node_e;
-  E.child = child;
-  E.need = need;
-  E.done = done;
-  E.tasks = tasks;
-  E.met = met;
-  k_phaseA<K, TB><<<grid_a, kExecThreads, smem_a, st>>>(E);
-  RS_CUDA(cudaGetLastError());
-  prof_mark(2, st);
-  MergeArgs M;
-  M.key[0] = E.key[0];
-  M.key[1] = E.key[1];
-  M.tag[0] = E.tag[0];
-  M.tag[1] = E.tag[1];
-  M.classic = classic;
-  M.msuper = msuper;
-  M.leaf_start = leaf_start;
-  M.depth = depth;
-  M.node_s = node_s;
-  M.node_e = node_e;
-  M.child = child;
-  M.need = need;
-  M.done = done;
-  M.tasks = tasks;
-  M.met = met;
-  k_merge_exec<K, TB><<<grid_m, kMergeThreads, smem_m, st>>>(M);
-  RS_CUDA(cudaGetLastError());
-  prof_mark(3, st);
-  return RS_OK;
+template <typename K, int TB>
+int run_peeksort(K* keys, void* tags, int64_t n, int w, int classic, unsigned char* ws, const Layout& L,
+                 cudaStream_t st) {
+  int sms;
+  if (int e = device_sms(&sms)) return e;
+  WsView V = view(ws, L);
+  prof_mark(0, st);
+  prof_set_met(V.met);
+  auto at = [&](size_t o) { return ws + o; };
+  PeekArgs PK;
+  PK.keys = keys;
+  PK.tags = tags;
+  PK.tag_bytes = TB;
+  PK.n = n;
+  PK.w = w;
+  PK.ascw = V.ascw;
+  PK.no_zero = reinterpret_cast<uint32_t*>(at(L.o_nozero));
+  PK.no_one = reinterpret_cast<uint32_t*>(at(L.o_noone));
+  PK.front[0] = reinterpret_cast<PeekItem*>(at(L.o_front0));
+  PK.front[1] = reinterpret_cast<PeekItem*>(at(L.o_front1));
+  PK.front_cap = L.front_cap;
+  PK.nodes = reinterpret_cast<pos_t*>(at(L.o_pnodes));
+  PK.leaves = reinterpret_cast<pos_t*>(at(L.o_pleaves));
+  PK.revs = reinterpret_cast<pos_t*>(at(L.o_prevs));
+  PK.rec_cap = L.rec_cap;
+  PK.lbits = reinterpret_cast<uint32_t*>(at(L.o_lbits));
+  PK.wpre = reinterpret_cast<uint32_t*>(at(L.o_wpre));
+  PK.chunk = reinterpret_cast<uint32_t*>(at(L.o_wchunk));
+  PK.words = L.words;
+  PK.T = tree_arrays(V, L);
+  int msuper = merge_super<K, TB>(n, sms);
+  PK.CA = classify_args<K, TB>(V, L, n, w, classic, msuper, 1);
+  int64_t nch_max = (L.r_max + kOrdChunkMin - 1) / kOrdChunkMin;
+  PK.chunkdep = V.chunkdep;
+  PK.chunkdep_words = (nch_max + 1) * kMaxDepth;
+  PK.done = V.done;
+  PK.done_words = 2 * L.r_max + 2;
+  size_t sm = (size_t)kOrdChunkMax * 5 + 64;
+  static int occ[64] = {0};
+  int dev;
+  RS_CUDA(cudaGetDevice(&dev));
+  if (occ[dev] == 0) {
+    int o = 0;
+    RS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_peek<K, TB>, 256, sm));
+    if (o < 1) return fail(RS_ECUDA, "peeksort kernel does not fit on an SM");
+    occ[dev] = o;
+  }
+  void* kargs[] = {&PK};
+  RS_CUDA(cudaLaunchCooperativeKernel((void*)k_peek<K, TB>, dim3(sms * occ[dev]), dim3(256), kargs, sm, st));
+  prof_mark(1, st);
+  return launch_exec<K, TB>(keys, tags, n, w, classic, msuper, V, L, sms, st);
 }
 
 int validate(int algo, int key_dtype, int tag_bytes, int64_t n, int32_t w, int32_t merge_kind, int* kb) {
@@ -377,7 +489,6 @@ int validate(int algo, int key_dtype, int tag_bytes, int64_t n, int32_t w, int32
   if (w > exec_fcap(*kb, tag_bytes))
     return fail(RS_EUNSUPPORTED, "min_run_len exceeds the device path's fused-subtree capacity");
   if (n >= ((int64_t)1 << 40)) return fail(RS_EUNSUPPORTED, "n >= 2^40 is not supported");
-  if (algo == RS_ALGO_PEEKSORT) return fail(RS_EUNSUPPORTED, "peeksort device path not built yet");
   return RS_OK;
 }
 
@@ -404,25 +515,29 @@ int export_tree(const Layout& L, unsigned char* ws, cudaStream_t st, rs_tree* tr
   if (r > tree->capacity) return fail(RS_EINVAL, "tree capacity too small");
   std::vector<int64_t> starts(r + 1);
   RS_CUDA(cudaMemcpyAsync(starts.data(), ws + L.o_leaf_start, (r + 1) * 8, cudaMemcpyDeviceToHost, st));
-  std::vector<uint8_t> P(r), la(r), ra(r);
+  std::vector<uint8_t> P(r), D(r);
   if (r > 1) {
     RS_CUDA(cudaMemcpyAsync(P.data(), ws + L.o_P, r, cudaMemcpyDeviceToHost, st));
-    RS_CUDA(cudaMemcpyAsync(la.data(), ws + L.o_la, r, cudaMemcpyDeviceToHost, st));
-    RS_CUDA(cudaMemcpyAsync(ra.data(), ws + L.o_ra, r, cudaMemcpyDeviceToHost, st));
+    RS_CUDA(cudaMemcpyAsync(D.data(), ws + L.o_depth, r, cudaMemcpyDeviceToHost, st));
   }
   RS_CUDA(cudaStreamSynchronize(st));
   for (int64_t i = 0; i < r; ++i)
     if (tree->leaf_len) tree->leaf_len[i] = starts[i + 1] - starts[i];
   for (int64_t j = 1; j < r; ++j) {
-    if (tree->node_power) tree->node_power[j - 1] = P[j];
-    if (tree->node_depth) tree->node_depth[j - 1] = (uint8_t)(la[j] + ra[j]);
+    if (tree->node_power) tree->node_power[j - 1] = L.algo == RS_ALGO_POWERSORT ? P[j] : 0;
+    if (tree->node_depth) tree->node_depth[j - 1] = D[j];
   }
   return RS_OK;
 }
 
 template <typename K>
-int dispatch_tags(K* keys, int tb, void* tags, int64_t n, int w, int classic, unsigned char* ws, const Layout& L,
-                  cudaStream_t st) {
+int dispatch_tags(int algo, K* keys, int tb, void* tags, int64_t n, int w, int classic, unsigned char* ws,
+                  const Layout& L, cudaStream_t st) {
+  if (algo == RS_ALGO_PEEKSORT) {
+    if (tb == 0) return run_peeksort<K, 0>(keys, nullptr, n, w, classic, ws, L, st);
+    if (tb == 4) return run_peeksort<K, 4>(keys, tags, n, w, classic, ws, L, st);
+    return run_peeksort<K, 8>(keys, tags, n, w, classic, ws, L, st);
+  }
   if (tb == 0) return run_powersort<K, 0>(keys, nullptr, n, w, classic, ws, L, st);
   if (tb == 4) return run_powersort<K, 4>(keys, tags, n, w, classic, ws, L, st);
   return run_powersort<K, 8>(keys, tags, n, w, classic, ws, L, st);
@@ -437,7 +552,7 @@ size_t rs_workspace_bytes(int algo, int key_dtype, int tag_bytes, int64_t n, int
   int kb = key_dtype == RS_KEY_I64 ? 8 : 4;
   if (n <= 1) return 256;
   if (min_run_len < 1) min_run_len = 1;
-  return make_layout(n, min_run_len, kb, tag_bytes).total;
+  return make_layout(n, min_run_len, kb, tag_bytes, algo).total;
 }
 
 int rs_sort(int algo, int key_dtype, void* keys, int tag_bytes, void* tags, int64_t n, int32_t min_run_len,
@@ -454,15 +569,15 @@ int rs_sort(int algo, int key_dtype, void* keys, int tag_bytes, void* tags, int6
     return RS_OK;
   }
   if (!keys || !workspace) return fail(RS_EINVAL, "null keys or workspace");
-  Layout L = make_layout(n, min_run_len, kb, tag_bytes);
+  Layout L = make_layout(n, min_run_len, kb, tag_bytes, algo);
   if (ws_bytes < L.total) return fail(RS_ENOMEM, "workspace too small");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   unsigned char* ws = reinterpret_cast<unsigned char*>(workspace);
   int e;
-  if (kb == 4) e = dispatch_tags<int32_t>(reinterpret_cast<int32_t*>(keys), tag_bytes, tags, n, min_run_len,
+  if (kb == 4) e = dispatch_tags<int32_t>(algo, reinterpret_cast<int32_t*>(keys), tag_bytes, tags, n, min_run_len,
                                         merge_kind, ws, L, st);
-  else e = dispatch_tags<int64_t>(reinterpret_cast<int64_t*>(keys), tag_bytes, tags, n, min_run_len, merge_kind,
-                                  ws, L, st);
+  else e = dispatch_tags<int64_t>(algo, reinterpret_cast<int64_t*>(keys), tag_bytes, tags, n, min_run_len,
+                                  merge_kind, ws, L, st);
   if (e) return e;
   if (out || tree) {
     if ((e = read_metrics(L, ws, st, out))) return e;
@@ -479,7 +594,7 @@ int rs_fetch_metrics(int algo, int key_dtype, int tag_bytes, int64_t n, int32_t 
     return RS_OK;
   }
   int kb = key_dtype == RS_KEY_I64 ? 8 : 4;
-  Layout L = make_layout(n, min_run_len, kb, tag_bytes);
+  Layout L = make_layout(n, min_run_len, kb, tag_bytes, algo);
   return read_metrics(L, reinterpret_cast<unsigned char*>(workspace), reinterpret_cast<cudaStream_t>(stream), out);
 }
 
@@ -528,7 +643,7 @@ int rs_debug_counters(int key_dtype, int tag_bytes, int64_t n, int32_t min_run_l
                       int cap) {
   if (n <= 1 || !workspace || !out) return 0;
   int kb = key_dtype == RS_KEY_I64 ? 8 : 4;
-  Layout L = make_layout(n, min_run_len, kb, tag_bytes);
+  Layout L = make_layout(n, min_run_len, kb, tag_bytes, RS_ALGO_POWERSORT);
   DevMetrics hm;
   RS_CUDA(cudaDeviceSynchronize());
   RS_CUDA(cudaMemcpy(&hm, reinterpret_cast<unsigned char*>(workspace) + L.o_met, sizeof(DevMetrics),

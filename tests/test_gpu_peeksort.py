@@ -1,0 +1,90 @@
+"""GPU parity for peeksort (reference sorters.py:146-361): outputs, all Metrics
+(runs_detected is assigned, max_stack_height untouched) and recorded trees vs
+the reference fixtures and the C oracle."""
+import numpy as np
+import pytest
+
+import paper_1805_04154_b200 as rs
+from oracle import oracle
+from paper_1805_04154_b200 import workloads
+from tests import golden_data as G
+
+pytestmark = pytest.mark.gpu
+
+
+def _shape(t):
+    if isinstance(t, rs.MergeLeaf):
+        return ("L", t.length)
+    return ("N", _shape(t.left), _shape(t.right))
+
+
+def _run(a, w, mk, tags=None, record=False):
+    work = a.copy()
+    tw = tags.copy() if tags is not None else None
+    m = rs.peeksort(work, rs.SortConfig(min_run_len=w, merge_kind=mk, record_tree=record), tags=tw)
+    return work, tw, m
+
+
+def _mt(m):
+    return (m.merge_cost, m.comparisons, m.runs_detected, m.max_stack_height)
+
+
+def test_golden_peeksort_matches_reference():
+    meta, arrays = G.load()
+    bad = []
+    n_cases = 0
+    for case in meta["cases"]:
+        if case["algo"] != "peeksort":
+            continue
+        a, tags = G.case_inputs(case, arrays)
+        work, tw, m = _run(a, case["w"], case["merge_kind"], tags)
+        got_sha = G.sha(work) if tw is None else G.sha(work, tw)
+        if _mt(m) != G.metrics_of(case) or got_sha != case["out_sha"]:
+            bad.append((case["input"], case["w"], case["merge_kind"], _mt(m), G.metrics_of(case)))
+        n_cases += 1
+    assert not bad, f"{len(bad)}/{n_cases} mismatches, first: {bad[:4]}"
+
+
+def test_golden_peeksort_trees():
+    meta, arrays = G.load()
+    for case in meta["cases"]:
+        if case["algo"] != "peeksort" or "tree" not in case:
+            continue
+        a, _ = G.case_inputs(case, arrays)
+        _, _, m = _run(a, case["w"], case["merge_kind"], record=True)
+        assert _shape(m.merge_tree) == G.tree_shape(case["tree"]), case["input"]
+
+
+@pytest.mark.parametrize("key_dtype", [np.int32, np.int64])
+def test_peeksort_random_vs_oracle(key_dtype):
+    rng = np.random.default_rng(5 + (key_dtype == np.int64))
+    for trial in range(40):
+        n = int(rng.choice([2, 3, 7, 50, 1000, 5000, 20000, 70000]))
+        kind = trial % 4
+        if kind == 0:
+            a = rng.permutation(n)
+        elif kind == 1:
+            a = rng.integers(0, max(2, n // 50), size=n)
+        elif kind == 2:
+            a = workloads.config4(n, seed=trial, mean=float(rng.integers(2, 300)))[0]
+        else:
+            a = workloads.config3(n, seed=trial)
+        a = a.astype(key_dtype)
+        tags = np.arange(n, dtype=np.int64)
+        w = int(rng.choice([1, 2, 3, 7, 24, 100]))
+        mk = "classic" if trial % 2 else "bitonic"
+        ref_a, ref_t = a.copy(), tags.copy()
+        ref = oracle.peeksort(ref_a, w, mk, ref_t)
+        work, tw, m = _run(a, w, mk, tags)
+        assert np.array_equal(work, ref_a) and np.array_equal(tw, ref_t), (n, kind, w, mk)
+        assert _mt(m) == ref.metrics_tuple(), (n, kind, w, mk)
+
+
+@pytest.mark.slow
+def test_peeksort_config2_full():
+    a, _ = workloads.generate(2)
+    ref_a = a.copy()
+    ref = oracle.peeksort(ref_a, 24, "bitonic")
+    work, _, m = _run(a, 24, "bitonic")
+    assert np.array_equal(work, ref_a)
+    assert _mt(m) == ref.metrics_tuple()
