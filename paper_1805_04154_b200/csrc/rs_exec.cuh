@@ -103,8 +103,11 @@ __device__ __forceinline__ int classify_leaf(const ClassifyArgs& A, int64_t i, i
   pos_t len = A.leaf_start[i + 1] - A.leaf_start[i];
   uint32_t lid = A.leaf_base + (uint32_t)i;
   *tiles = 0;
-  if (len <= A.fcap) return parent_small(A, A.parent[lid]) ? 0 : 1;
-  bool desc = (A.leaf_info[i] >> 31) != 0;
+  if (len <= A.fcap && parent_small(A, A.parent[lid])) return 0;  // inside a fused subtree
+  uint32_t info = A.leaf_info[i];
+  uint32_t nl = info & 0x7fffffffu;
+  if (nl < (uint32_t)A.w && (pos_t)nl < len) return 1;  // extended by insertion sort: fused task
+  bool desc = (info >> 31) != 0;
   int mode = leaf_mode(desc, A.leaf_depth[i] & 1);
   *tiles = leaf_tiles(len, mode, A.tile);
   return *tiles > 0 ? 2 : 0;
