@@ -27,7 +27,6 @@ namespace rs {
 
 constexpr int kSuperMax = 15;          // tiles per merge task: runtime, <= 15 (lane groups of >= 2)
 constexpr int kStages = 2;             // smem ring depth
-constexpr int kHold = 1;               // producer's out-of-order task window
 constexpr int kConsumerThreads = 256;  // 8 consumer warps
 constexpr int kMergeThreads = kConsumerThreads + 64;  // + producer warp + signaller warp
 
@@ -75,62 +74,129 @@ struct MergeArgs {
   DevMetrics* met;
 };
 
-__device__ __forceinline__ bool counter_ready(const uint32_t* done, const uint32_t* need, uint32_t id) {
-  uint32_t nd = need[id];
-  return nd == 0 || ld_acquire_u32(done + id) >= nd;
-}
-
-__device__ __forceinline__ void wait_counter(const uint32_t* done, const uint32_t* need, uint32_t id) {
-  uint32_t nd = need[id];
-  if (nd == 0) return;
-  unsigned ns = 32;
-  while (ld_acquire_u32(done + id) < nd) {
-    __nanosleep(ns);
-    if (ns < 512) ns <<= 1;
-  }
-}
-
 // Lane-group merge-path search: lanes [g*G, g*G+G) cooperate on diagonal `diag`
-// of group g.  Returns the split (number of A elements) in every lane.
-template <typename K>
+// of group g.  Returns the split (number of A elements) in every lane.  `side`
+// runs once per round trip, between issuing the step's loads and consuming
+// them, so another dependent load chain can overlap the search's latency.
+struct NoSide {
+  __device__ __forceinline__ void operator()() const {}
+};
+template <typename K, typename Side = NoSide>
 __device__ __forceinline__ int64_t group_merge_path(const K* A, int64_t na, const K* B, int64_t nb, int64_t diag,
-                                                    bool active, int G) {
+                                                    bool active, int G, Side&& side = Side()) {
+  // Each lane probes kProbe positions per round trip: a group of G lanes cuts
+  // the interval (G * kProbe + 1) ways.  The predicate A[i] <= B[diag-1-i] is
+  // monotone in i, so the number of true probes locates the split.
+#ifndef RS_PROBE
+#define RS_PROBE 2
+#endif
+  constexpr int kProbe = RS_PROBE;
   int lane = threadIdx.x & 31;
   int g = lane / G, gl = lane % G;
+  const int GP = G * kProbe;
+  const uint32_t gmask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << (g * G);
   int64_t lo = 0, hi = 0;
   if (active) {
     lo = diag - nb > 0 ? diag - nb : 0;
     hi = diag < na ? diag : na;
   }
   for (;;) {
-    bool need = active && (hi - lo > G);
+    bool need = active && (hi - lo > GP);
     if (!__any_sync(0xffffffffu, need)) break;
-    int64_t idx = 0;
-    bool pred = false;
-    if (need) {
-      int64_t span = hi - lo;
-      idx = lo + (span * (gl + 1)) / (G + 1);
-      pred = ldcg(A + idx) <= ldcg(B + (diag - 1 - idx));
+    // probes at lo + k*step, k = 1..GP (step >= 1 since span > GP): one division
+    int64_t step = (hi - lo) / (GP + 1);
+    K xa[kProbe], xb[kProbe];
+#pragma unroll
+    for (int q = 0; q < kProbe; ++q) {
+      xa[q] = K(0);
+      xb[q] = K(0);
+      if (need) {
+        int64_t idx = lo + step * (gl * kProbe + q + 1);
+        xa[q] = ldcg(A + idx);
+        xb[q] = ldcg(B + (diag - 1 - idx));
+      }
     }
-    uint32_t bal = __ballot_sync(0xffffffffu, pred);
-    int base = g * G;
-    uint32_t mine = (bal >> base) & ((1u << G) - 1u);
-    int c = __popc(mine);
-    int64_t idx_lo = __shfl_sync(0xffffffffu, idx, base + (c > 0 ? c - 1 : 0));
-    int64_t idx_hi = __shfl_sync(0xffffffffu, idx, base + (c < G ? c : G - 1));
+    side();
+    int c = 0;
+#pragma unroll
+    for (int q = 0; q < kProbe; ++q) c += __popc(__ballot_sync(0xffffffffu, need && xa[q] <= xb[q]) & gmask);
     if (need) {
-      int64_t nlo = c > 0 ? idx_lo + 1 : lo;
-      int64_t nhi = c < G ? idx_hi : hi;
+      int64_t nlo = c > 0 ? lo + step * c + 1 : lo;
+      int64_t nhi = c < GP ? lo + step * (c + 1) : hi;
       lo = nlo;
       hi = nhi;
     }
   }
-  int64_t idx = lo + gl;
-  bool pred = active && idx < hi && ldcg(A + idx) <= ldcg(B + (diag - 1 - idx));
-  uint32_t bal = __ballot_sync(0xffffffffu, pred);
-  uint32_t mine = (bal >> (g * G)) & ((1u << G) - 1u);
-  return lo + __popc(mine);
+  K xa[kProbe], xb[kProbe];
+  bool fin[kProbe];
+#pragma unroll
+  for (int q = 0; q < kProbe; ++q) {
+    int64_t idx = lo + gl * kProbe + q;
+    fin[q] = active && idx < hi;
+    xa[q] = K(0);
+    xb[q] = K(0);
+    if (fin[q]) {
+      xa[q] = ldcg(A + idx);
+      xb[q] = ldcg(B + (diag - 1 - idx));
+    }
+  }
+  side();
+  int c = 0;
+#pragma unroll
+  for (int q = 0; q < kProbe; ++q) c += __popc(__ballot_sync(0xffffffffu, fin[q] && xa[q] <= xb[q]) & gmask);
+  return lo + c;
 }
+
+// The producer's view of one claimed merge task, fetched in dependent stages
+// (claim -> record -> node + children -> children's tile counts) so the chain
+// can be advanced one round trip at a time while other work is in flight.
+struct PTask {
+  unsigned long long t;
+  uint32_t j, sk, c0, c1, nd0, nd1;
+  pos_t s, e, m;
+  int d;
+  int st;  // stages done: 1 claimed, 2 record, 3 node, 4 need
+  bool valid;
+  __device__ __forceinline__ void claim(DevMetrics* met) {
+    t = 0;
+    if ((threadIdx.x & 31) == 0) t = atomicAdd(&met->task_ctr, 1ull);
+    st = 1;
+  }
+  template <typename Args>
+  __device__ __forceinline__ void advance(const Args& E, unsigned long long ntasks) {
+    if (st == 1) {
+      t = __shfl_sync(0xffffffffu, t, 0);
+      valid = t < ntasks;
+      uint64_t rec = valid ? E.tasks[t] : 0ull;
+      j = task_id(rec);
+      sk = task_tile(rec);
+    } else if (st == 2) {
+      if (valid) {
+        c0 = E.child[2 * j];
+        c1 = E.child[2 * j + 1];
+        s = E.node_s[j];
+        e = E.node_e[j];
+        m = E.leaf_start[j];
+        d = E.depth[j];
+      }
+    } else if (st == 3) {
+      if (valid) {
+        nd0 = E.need[c0];
+        nd1 = E.need[c1];
+      }
+    }
+    if (st < 4) ++st;
+  }
+  template <typename Args>
+  __device__ __forceinline__ void finish(const Args& E, unsigned long long ntasks) {
+    while (st < 4) advance(E, ntasks);
+  }
+  __device__ __forceinline__ bool ready(const uint32_t* done) const {
+    uint32_t a = nd0 ? ld_acquire_u32(done + c0) : 0u;
+    uint32_t b = nd1 ? ld_acquire_u32(done + c1) : 0u;
+    return a >= nd0 && b >= nd1;
+  }
+};
 
 template <typename K>
 __device__ int64_t warp_count(const K* A, int64_t len, K v, bool or_equal) {
@@ -188,68 +254,36 @@ __global__ void __launch_bounds__(kMergeThreads, 3) k_merge_exec(MergeArgs E) {
     uint32_t phase = 0;  // flips when stage wraps
     const int kSuper = E.msuper;
     const int G = 32 / (kSuper + 1);
-    // Small out-of-order window: up to kHold claimed tasks are held and the
-    // oldest one whose children are complete is prepared first.  Every held
-    // task depends only on earlier tasks, so the oldest held-but-unready task
-    // in the whole grid always becomes ready: no deadlock.
-    uint32_t hj[kHold], hsk[kHold];
-    bool hv[kHold];
-#pragma unroll
-    for (int w = 0; w < kHold; ++w) hv[w] = false;
-    bool exhausted = false;
-    for (;;) {
-#pragma unroll
-      for (int w = 0; w < kHold; ++w) {
-        if (!hv[w] && !exhausted) {
-          unsigned long long t = 0;
-          if (lane == 0) t = atomicAdd(&E.met->task_ctr, 1ull);
-          t = __shfl_sync(0xffffffffu, t, 0);
-          if (t >= ntasks) {
-            exhausted = true;
-          } else {
-            uint64_t rec = E.tasks[t];
-            hj[w] = task_id(rec);
-            hsk[w] = task_tile(rec);
-            hv[w] = true;
-          }
-        }
-      }
-      bool any = false;
-#pragma unroll
-      for (int w = 0; w < kHold; ++w) any |= hv[w];
-      if (!any) break;
+    // The next task is claimed and its descriptor fetched while the current
+    // task's merge-path search runs (each is a chain of dependent global round
+    // trips; interleaving hides one behind the other).  Claiming one task ahead
+    // cannot deadlock: the current task is ready, so it completes, and every
+    // task waits only on tasks claimed before it.
+    PTask cur, nxt;
+    cur.claim(E.met);
+    cur.finish(E, ntasks);
+    while (cur.valid) {
       RS_T0(tw);
-      int pick = -1;
-      unsigned ns = 32;
-      for (;;) {
-        if (lane == 0) {
-#pragma unroll
-          for (int w = 0; w < kHold; ++w) {
-            if (pick < 0 && hv[w] && counter_ready(E.done, E.need, E.child[2 * hj[w]]) &&
-                counter_ready(E.done, E.need, E.child[2 * hj[w] + 1]))
-              pick = w;
-          }
-        }
-        pick = __shfl_sync(0xffffffffu, pick, 0);
-        if (pick >= 0) break;
-        __nanosleep(ns);
-        if (ns < 256) ns <<= 1;
+      if (!cur.ready(E.done)) {
+        unsigned ns = 32;
+        do {
+          __nanosleep(ns);
+          if (ns < 256) ns <<= 1;
+        } while (!cur.ready(E.done));
       }
-      uint32_t j = 0, sk = 0;
-#pragma unroll
-      for (int w = 0; w < kHold; ++w)
-        if (w == pick) { j = hj[w]; sk = hsk[w]; hv[w] = false; }
+      nxt.claim(E.met);
+      const uint32_t j = cur.j, sk = cur.sk;
+      const pos_t s = cur.s, e = cur.e, m = cur.m;
+      const int d = cur.d;
       if (lane == 0) {
         fence_proxy_async();
 #ifdef RS_INSTR
-        atomicAdd(&E.met->depth_wait[E.depth[j]], (unsigned long long)(clock64() - tw));
+        atomicAdd(&E.met->depth_wait[d], (unsigned long long)(clock64() - tw));
 #endif
         RS_ACC(E.met, 0, tw);
       }
       __syncwarp();
       RS_T0(tsrch);
-      pos_t s = E.node_s[j], e = E.node_e[j], m = E.leaf_start[j];
-      int d = E.depth[j];
       const K* src = reinterpret_cast<const K*>(((d + 1) & 1) ? E.key[1] : E.key[0]);
       const T* tsrc = HT ? reinterpret_cast<const T*>(((d + 1) & 1) ? E.tag[1] : E.tag[0]) : nullptr;
       int64_t tot = e - s, na = m - s, nb = e - m;
@@ -261,7 +295,9 @@ __global__ void __launch_bounds__(kMergeThreads, 3) k_merge_exec(MergeArgs E) {
       if (diag > tot) diag = tot;
       bool in_range = g <= (kend - kbeg) && g < kSuper + 1 && lane < G * (kSuper + 1);
       bool trivial = diag == 0 || diag == tot;
-      int64_t split = group_merge_path(src + s, na, src + m, nb, diag, in_range && !trivial, G);
+      int64_t split = group_merge_path(src + s, na, src + m, nb, diag, in_range && !trivial, G,
+                                       [&]() { nxt.advance(E, ntasks); });
+      nxt.finish(E, ntasks);
       if (diag == 0) split = 0;
       else if (diag == tot) split = na;
       if (lane == 0) RS_ACC(E.met, 1, tsrch);
@@ -326,6 +362,7 @@ __global__ void __launch_bounds__(kMergeThreads, 3) k_merge_exec(MergeArgs E) {
         __syncwarp();
         if (++stage == kStages) { stage = 0; phase ^= 1; }
       }
+      cur = nxt;
     }
     if (lane == 0) {
       mbar_wait(&empty_bar[stage], phase ^ 1);

@@ -12,6 +12,7 @@
 //   7. k_execute       persistent dataflow executor (leaves + merges)
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -242,6 +243,7 @@ int merge_super(int64_t n, int sms) {
   int64_t ctas = (int64_t)sms * 3;
   int64_t per_level_tiles = n / MergeCfg<K, TB>::TILE;
   int64_t s = per_level_tiles / (8 * ctas);
+  if (const char* ov = getenv("RS_MERGE_SUPER")) s = atoi(ov);  // tuning override
   if (s < 1) s = 1;
   if (s > 7) s = 7;
   return (int)s;
