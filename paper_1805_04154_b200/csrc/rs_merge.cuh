@@ -152,10 +152,10 @@ __device__ __forceinline__ int64_t group_merge_path(const K* A, int64_t na, cons
 // can be advanced one round trip at a time while other work is in flight.
 struct PTask {
   unsigned long long t;
-  uint32_t j, sk, c0, c1, nd0, nd1;
+  uint32_t j, sk, c0, c1, nd0, nd1, dn0, dn1;
   pos_t s, e, m;
   int d;
-  int st;  // stages done: 1 claimed, 2 record, 3 node, 4 need
+  int st;  // stages done: 1 claimed, 2 record, 3 node, 4 need, 5 counters (speculative)
   bool valid;
   __device__ __forceinline__ void claim(DevMetrics* met) {
     t = 0;
@@ -184,17 +184,24 @@ struct PTask {
         nd0 = E.need[c0];
         nd1 = E.need[c1];
       }
+    } else if (st == 4) {
+      // early acquire of the children's counters (overlapping the search's
+      // loads): if they already read complete, ready() costs nothing
+      dn0 = valid && nd0 ? ld_acquire_u32(E.done + c0) : 0u;
+      dn1 = valid && nd1 ? ld_acquire_u32(E.done + c1) : 0u;
     }
-    if (st < 4) ++st;
+    if (st < 5) ++st;
   }
   template <typename Args>
   __device__ __forceinline__ void finish(const Args& E, unsigned long long ntasks) {
-    while (st < 4) advance(E, ntasks);
+    while (st < 5) advance(E, ntasks);
   }
-  __device__ __forceinline__ bool ready(const uint32_t* done) const {
-    uint32_t a = nd0 ? ld_acquire_u32(done + c0) : 0u;
-    uint32_t b = nd1 ? ld_acquire_u32(done + c1) : 0u;
-    return a >= nd0 && b >= nd1;
+  // Children complete (with acquire semantics)?
+  __device__ __forceinline__ bool ready(const uint32_t* done) {
+    if (dn0 >= nd0 && dn1 >= nd1) return true;
+    dn0 = nd0 ? ld_acquire_u32(done + c0) : 0u;
+    dn1 = nd1 ? ld_acquire_u32(done + c1) : 0u;
+    return dn0 >= nd0 && dn1 >= nd1;
   }
 };
 
@@ -271,12 +278,15 @@ __global__ void __launch_bounds__(kMergeThreads, 3) k_merge_exec(MergeArgs E) {
           if (ns < 256) ns <<= 1;
         } while (!cur.ready(E.done));
       }
+      if (lane == 0) RS_ACC(E.met, 5, tw);
       nxt.claim(E.met);
       const uint32_t j = cur.j, sk = cur.sk;
       const pos_t s = cur.s, e = cur.e, m = cur.m;
       const int d = cur.d;
       if (lane == 0) {
-        fence_proxy_async();
+        RS_T0(tf);
+        fence_proxy_async_global();  // acquired generic-proxy data -> TMA reads
+        RS_ACC(E.met, 6, tf);
 #ifdef RS_INSTR
         atomicAdd(&E.met->depth_wait[d], (unsigned long long)(clock64() - tw));
 #endif
@@ -301,6 +311,7 @@ __global__ void __launch_bounds__(kMergeThreads, 3) k_merge_exec(MergeArgs E) {
       if (diag == 0) split = 0;
       else if (diag == tot) split = na;
       if (lane == 0) RS_ACC(E.met, 1, tsrch);
+      RS_T0(tiss);
       if (E.classic && kbeg == 0) {
         // runcore.py:321-324
         K maxL = ldcg(src + m - 1), maxR = ldcg(src + e - 1);
@@ -362,6 +373,7 @@ __global__ void __launch_bounds__(kMergeThreads, 3) k_merge_exec(MergeArgs E) {
         __syncwarp();
         if (++stage == kStages) { stage = 0; phase ^= 1; }
       }
+      if (lane == 0) RS_ACC(E.met, 7, tiss);
       cur = nxt;
     }
     if (lane == 0) {
