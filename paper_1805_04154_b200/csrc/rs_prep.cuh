@@ -7,6 +7,7 @@
 
 #include "rs_chain.cuh"
 #include "rs_exec.cuh"
+#include "rs_small.cuh"
 #include "rs_tree.cuh"
 
 namespace rs {
@@ -85,6 +86,12 @@ __global__ void __launch_bounds__(256, 3) k_prep(PrepArgs P) {
   }
   grid.sync();
   RS_TS(met, 4);
+  // small trees: phases 5-9 in block 0 alone, out of shared memory (rs_small.cuh)
+  if ((int64_t)met->n_leaves <= kSmallR) {
+    extern __shared__ __align__(16) unsigned char smem_prep[];
+    if (blockIdx.x == 0) small_tree<256>(P.T, P.CA, P.F, smem_prep);
+    return;
+  }
   // 5. node powers + ancestor-count scan (chunk aggregates); last block scans them
   d_scan_reduce(P.T.leaf_start, P.n, P.F, const_cast<uint64_t*>(P.T.K), const_cast<uint8_t*>(P.T.P), met, P.agg,
                 P.nchunks);

@@ -388,6 +388,7 @@ int run_powersort(K* keys, void* tags, int64_t n, int w, int classic, unsigned c
   sm = std::max(sm, (size_t)gbatch * W1 * 8);
   sm = std::max(sm, (size_t)tbatch * W1 * 8);
   sm = std::max(sm, (size_t)8 * (maxw * 2 + (maxw + 1) / 2 + 1) * 4);
+  sm = std::max(sm, small_smem_bytes());
   int F = n <= ((int64_t)1 << 31) ? 32 : 63;
   int64_t nch_max = (L.r_max + kOrdChunkMin - 1) / kOrdChunkMin;
   PrepArgs PA;
