@@ -377,7 +377,7 @@ struct Exec {
 
   static constexpr size_t smem_merge() { return (size_t)C::TILE * (C::kb + TB) + 64; }
   static constexpr size_t smem_fuse() {
-    return 2 * (size_t)C::FCAP * (C::kb + TB) + (size_t)C::MAXB * (3 * 2 + 1 + 2 + 2) + 256;
+    return 2 * (size_t)C::FCAP * (C::kb + TB) + 64 + (size_t)C::MAXB * (3 * 2 + 1 + 2 + 2) + 256;
   }
   static constexpr size_t smem_bytes() { return smem_fuse(); }
 
@@ -535,18 +535,23 @@ struct Exec {
   }
 
   // --- fused subtree: form its leaves and run all of its merges in SMEM ---
-  __device__ static void fuse_task(const ExecArgs& E, uint32_t u, unsigned char* smem,
-                                   unsigned long long& comps) {
+  __device__ static void fuse_task(const ExecArgs& E, uint32_t u, unsigned char* smem, uint64_t* bar,
+                                   uint32_t& fphase, unsigned long long& comps) {
     __shared__ uint32_t s_scan[40];
     __shared__ int s_dmax;
+    __shared__ int32_t s_off[2];
+    // X[0]/Y[0] receive the span by 1D bulk copy of its 16B-aligned cover (32B slack)
+    unsigned char* p = smem;
+    unsigned char* x0raw = p;
+    p += (size_t)C::FCAP * C::kb + 32;
     K* X[2];
     T* Y[2];
-    X[0] = reinterpret_cast<K*>(smem);
-    X[1] = X[0] + C::FCAP;
-    unsigned char* p = smem + 2 * (size_t)C::FCAP * C::kb;
-    Y[0] = reinterpret_cast<T*>(p);
-    Y[1] = Y[0] + (HAS_TAGS ? C::FCAP : 0);
-    p += HAS_TAGS ? 2 * (size_t)C::FCAP * TB : 0;
+    X[1] = reinterpret_cast<K*>(p);
+    p += (size_t)C::FCAP * C::kb;
+    unsigned char* y0raw = p;
+    p += HAS_TAGS ? (size_t)C::FCAP * TB + 32 : 0;
+    Y[1] = reinterpret_cast<T*>(p);
+    p += HAS_TAGS ? (size_t)C::FCAP * TB : 0;
     uint16_t* ns = reinterpret_cast<uint16_t*>(p);
     uint16_t* nm = ns + C::MAXB;
     uint16_t* ne = nm + C::MAXB;
@@ -570,10 +575,47 @@ struct Exec {
       droot = E.depth[u];
     }
     int len = int(e - s);
-    const K* g0 = reinterpret_cast<const K*>(E.key[0]);
-    const T* h0 = HAS_TAGS ? reinterpret_cast<const T*>(E.tag[0]) : nullptr;
-    copy_g2s(X[0], g0 + s, len, threadIdx.x, blockDim.x);
-    if (HAS_TAGS) copy_g2s(Y[0], h0 + s, len, threadIdx.x, blockDim.x);
+    if (threadIdx.x == 0) {
+      // previous task's generic-proxy smem accesses are ordered before the bulk writes
+      fence_proxy_async_smem();
+      auto cover = [](const void* base, pos_t e0, pos_t e1, int es) {
+        uintptr_t a0 = reinterpret_cast<uintptr_t>(base) + (uintptr_t)e0 * es;
+        uintptr_t a1 = reinterpret_cast<uintptr_t>(base) + (uintptr_t)e1 * es;
+        return (uint32_t)(((a1 + 15) & ~(uintptr_t)15) - (a0 & ~(uintptr_t)15));
+      };
+      uint32_t tx = cover(E.key[0], s, e, C::kb) + (HAS_TAGS ? cover(E.tag[0], s, e, TB) : 0u);
+      mbar_arrive_tx(bar, tx);
+      int32_t ok, ot = 0;
+      tma_window(x0raw, E.key[0], s, e, C::kb, bar, &ok);
+      if (HAS_TAGS) tma_window(y0raw, E.tag[0], s, e, TB, bar, &ot);
+      s_off[0] = ok;
+      s_off[1] = ot;
+    }
+    // the subtree's node table while the span is in flight
+    int nbd = int(lb - la);
+    int dmax_local = droot;
+    if (threadIdx.x == 0) s_dmax = droot;
+    for (int x = threadIdx.x; x < nbd; x += blockDim.x) {
+      int64_t jj = la + 1 + x;
+      ns[x] = (uint16_t)(E.node_s[jj] - s);
+      nm[x] = (uint16_t)(E.leaf_start[jj] - s);
+      ne[x] = (uint16_t)(E.node_e[jj] - s);
+      int dd = E.depth[jj];
+      dep[x] = (uint8_t)dd;
+      dmax_local = dd > dmax_local ? dd : dmax_local;
+    }
+    __syncthreads();
+    if (nbd > 0) atomicMax(&s_dmax, dmax_local);
+    mbar_wait(bar, fphase);
+    fphase ^= 1u;
+    X[0] = reinterpret_cast<K*>(x0raw) + s_off[0];
+    Y[0] = HAS_TAGS ? reinterpret_cast<T*>(y0raw) + s_off[1] : nullptr;
+    __builtin_assume(__isShared(X[0]));
+    __builtin_assume(__isShared(X[1]));
+    if (HAS_TAGS) {
+      __builtin_assume(__isShared(Y[0]));
+      __builtin_assume(__isShared(Y[1]));
+    }
     __syncthreads();
     // leaves: warp per leaf
     int wid = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
@@ -657,22 +699,7 @@ struct Exec {
       __syncwarp();
     }
     __syncthreads();
-    int nbd = int(lb - la);
     if (nbd > 0) {
-      if (threadIdx.x == 0) s_dmax = droot;
-      __syncthreads();
-      int dmax_local = droot;
-      for (int x = threadIdx.x; x < nbd; x += blockDim.x) {
-        int64_t jj = la + 1 + x;
-        ns[x] = (uint16_t)(E.node_s[jj] - s);
-        nm[x] = (uint16_t)(E.leaf_start[jj] - s);
-        ne[x] = (uint16_t)(E.node_e[jj] - s);
-        int dd = E.depth[jj];
-        dep[x] = (uint8_t)dd;
-        dmax_local = dd > dmax_local ? dd : dmax_local;
-      }
-      atomicMax(&s_dmax, dmax_local);
-      __syncthreads();
       int dmax = s_dmax;
       const int per = (nbd + blockDim.x - 1) / blockDim.x;
       for (int dd = dmax; dd >= droot; --dd) {
@@ -701,6 +728,12 @@ struct Exec {
         K* Xd = X[dd & 1];
         const T* Ys = Y[(dd + 1) & 1];
         T* Yd = Y[dd & 1];
+        __builtin_assume(__isShared(Xs));  // keep LDS/STS (not generic) in the merge loop
+        __builtin_assume(__isShared(Xd));
+        if (HAS_TAGS) {
+          __builtin_assume(__isShared(Ys));
+          __builtin_assume(__isShared(Yd));
+        }
         for (int c = threadIdx.x; c < nchunk; c += blockDim.x) {
           // node: last level entry with loff <= c
           int lo = 0, hi = nlev - 1;
@@ -751,6 +784,13 @@ __global__ void __launch_bounds__(kExecThreads) k_phaseA(ExecArgs E) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ unsigned long long s_task;
   __shared__ unsigned long long sred[32];
+  __shared__ __align__(8) uint64_t s_bar;
+  if (threadIdx.x == 0) {
+    mbar_init(&s_bar, 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  uint32_t fphase = 0;
   unsigned long long comps = 0;
   unsigned long long ntasks = E.met->phaseA;
   for (;;) {
@@ -761,7 +801,7 @@ __global__ void __launch_bounds__(kExecThreads) k_phaseA(ExecArgs E) {
     uint64_t rec = E.tasks[t];
     uint32_t kind = task_kind(rec), id = task_id(rec), tile = task_tile(rec);
     if (kind == kTaskLeaf) Exec<K, TB>::leaf_task(E, id - E.leaf_base, tile);
-    else Exec<K, TB>::fuse_task(E, id, smem, comps);
+    else Exec<K, TB>::fuse_task(E, id, smem, &s_bar, fphase, comps);
     __syncthreads();
     if (threadIdx.x == 0) release_add_u32(E.done + id, 1u);
   }
