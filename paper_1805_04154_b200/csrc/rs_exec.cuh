@@ -30,7 +30,7 @@ struct ExecCfg {
   static constexpr int TILE = kExecThreads * IPT;
   static constexpr int FCAP = (eb <= 8) ? 4096 : 2048;  // fused-subtree capacity (elements)
   static constexpr int IPTF = 8;                        // outputs per fused merge chunk
-  static constexpr int MAXB = FCAP / 2 + 2;             // boundaries inside a fused subtree
+  static constexpr int MAXB = FCAP / 2 + 2;             // boundaries inside a fused subtree (any w)
 };
 
 template <int TB> struct TagT { using type = uint32_t; };
@@ -56,6 +56,7 @@ struct ExecArgs {
   uint32_t* done;
   const uint64_t* tasks;
   DevMetrics* met;
+  int maxb;  // node-table capacity of a fused subtree: FCAP / max(w, 2) + 2
 };
 
 __device__ __forceinline__ int leaf_mode(bool desc, int dpar) {
@@ -92,10 +93,18 @@ struct ClassifyArgs {
   uint8_t* cls;  // unified id -> 0 none, 1 fused root, 2 big (tiles in need[])
   uint64_t* tasks;
   DevMetrics* met;
+  const int32_t* node_a;
+  const int32_t* node_b;
+  int maxb;  // ExecArgs::maxb
 };
 
+// Node j can run as (part of) one fused phase-A task: its span fits FCAP and
+// its internal nodes fit the task's node table.
+__device__ __forceinline__ bool fusable(const ClassifyArgs& A, int32_t j) {
+  return (A.node_e[j] - A.node_s[j]) <= A.fcap && (A.node_b[j] - A.node_a[j]) <= A.maxb - 2;
+}
 __device__ __forceinline__ bool parent_small(const ClassifyArgs& A, int32_t par) {
-  return par >= 0 && (A.node_e[par] - A.node_s[par]) <= A.fcap;
+  return par >= 0 && fusable(A, par);
 }
 
 // Per element: 0 = nothing, 1 = fused root, 2 = big (tiles > 0).  *tiles out.
@@ -117,7 +126,7 @@ __device__ __forceinline__ int classify_node(const ClassifyArgs& A, int64_t j, i
   pos_t span = A.node_e[j] - A.node_s[j];
   *tiles = 0;
   *tasks = 0;
-  if (span <= A.fcap) return parent_small(A, A.parent[j]) ? 0 : 1;
+  if (fusable(A, (int32_t)j)) return parent_small(A, A.parent[j]) ? 0 : 1;
   *tiles = (span + A.mtile - 1) / A.mtile;
   *tasks = (*tiles + A.msuper - 1) / A.msuper;
   return 2;
@@ -376,10 +385,12 @@ struct Exec {
   static constexpr bool HAS_TAGS = TB != 0;
 
   static constexpr size_t smem_merge() { return (size_t)C::TILE * (C::kb + TB) + 64; }
-  static constexpr size_t smem_fuse() {
-    return 2 * (size_t)C::FCAP * (C::kb + TB) + 64 + (size_t)C::MAXB * (3 * 2 + 1 + 2 + 2) + 256;
+  // leaves of a fused subtree are >= max(w, 2) long except the array's last one
+  static constexpr int maxb_for(int w) { return C::FCAP / (w > 2 ? w : 2) + 2; }
+  static constexpr size_t smem_fuse(int maxb) {
+    return 2 * (size_t)C::FCAP * (C::kb + TB) + 64 + (size_t)maxb * (3 * 2 + 1 + 2 + 2) + 256;
   }
-  static constexpr size_t smem_bytes() { return smem_fuse(); }
+  static constexpr size_t smem_bytes(int w) { return smem_fuse(maxb_for(w)); }
 
   __device__ static void wait_ready(const ExecArgs& E, uint32_t id) {
     uint32_t need = E.need[id];
@@ -552,12 +563,13 @@ struct Exec {
     p += HAS_TAGS ? (size_t)C::FCAP * TB + 32 : 0;
     Y[1] = reinterpret_cast<T*>(p);
     p += HAS_TAGS ? (size_t)C::FCAP * TB : 0;
+    const int MB = E.maxb;
     uint16_t* ns = reinterpret_cast<uint16_t*>(p);
-    uint16_t* nm = ns + C::MAXB;
-    uint16_t* ne = nm + C::MAXB;
-    uint16_t* lst = ne + C::MAXB;   // level node list
-    uint16_t* loff = lst + C::MAXB; // level chunk offsets
-    uint8_t* dep = reinterpret_cast<uint8_t*>(loff + C::MAXB);
+    uint16_t* nm = ns + MB;
+    uint16_t* ne = nm + MB;
+    uint16_t* lst = ne + MB;   // level node list
+    uint16_t* loff = lst + MB; // level chunk offsets
+    uint8_t* dep = reinterpret_cast<uint8_t*>(loff + MB);
 
     int64_t la, lb;
     pos_t s, e;
@@ -780,7 +792,7 @@ struct Exec {
 
 // Phase A: fused subtrees and big-leaf tiles (no dependencies among them).
 template <typename K, int TB>
-__global__ void __launch_bounds__(kExecThreads) k_phaseA(ExecArgs E) {
+__global__ void __launch_bounds__(kExecThreads, 3) k_phaseA(ExecArgs E) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ unsigned long long s_task;
   __shared__ unsigned long long sred[32];

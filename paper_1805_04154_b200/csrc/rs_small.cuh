@@ -179,7 +179,8 @@ __device__ void small_tree(const TreeArrays& T, const ClassifyArgs& A, int F, un
       pos_t s0 = Ls[a], e0 = Ls[b + 1];
       T.node_s[j] = s0;
       T.node_e[j] = e0;
-      myspan[q] = e0 - s0;
+      // bit 62: not fusable (too many internal nodes for the phase-A node table)
+      myspan[q] = (e0 - s0) | ((b - a > A.maxb - 2) ? ((pos_t)1 << 62) : (pos_t)0);
       uint8_t dd = (uint8_t)(las[j] + ras[j]);
       T.depth[j] = dd;
       dep[j] = dd;
@@ -209,7 +210,9 @@ __device__ void small_tree(const TreeArrays& T, const ClassifyArgs& A, int F, un
   // ---- classification (d_classify), contiguous items per thread
   const int64_t per = (r + nt - 1) / nt;
   const int64_t i0 = (int64_t)tid * per;
-  auto parent_small_s = [&](int32_t p) { return p >= 0 && spans[p] <= A.fcap; };
+  constexpr pos_t kNoFuse = (pos_t)1 << 62;
+  auto fusable_s = [&](int64_t j) { return spans[j] <= A.fcap; };  // kNoFuse set -> > fcap
+  auto parent_small_s = [&](int32_t p) { return p >= 0 && fusable_s(p); };
   unsigned long long comps = 0, mcost = 0, mbig = 0;
   uint32_t cntA = 0;
   unsigned maxd = 0;
@@ -249,11 +252,12 @@ __device__ void small_tree(const TreeArrays& T, const ClassifyArgs& A, int F, un
     lcls[q] = (uint8_t)c;
     a_of[q] = c == 1 ? 1u : (uint32_t)tl;
     if (i >= 1) {
-      pos_t span = spans[i];
+      bool fz = fusable_s(i);
+      pos_t span = spans[i] & (kNoFuse - 1);
       mcost += span;
       if (!A.classic) comps += span;  // runcore.py:299-301
       int cn;
-      if (span <= A.fcap) cn = parent_small_s(par[r + i]) ? 0 : 1;
+      if (fz) cn = parent_small_s(par[r + i]) ? 0 : 1;
       else cn = 2;
       A.cls[i] = (uint8_t)cn;
       ncls[q] = (uint8_t)cn;

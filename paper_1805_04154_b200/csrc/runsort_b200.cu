@@ -195,22 +195,28 @@ int device_sms(int* sms) {
 }
 
 template <typename K, int TB>
-int exec_grid(int sms, int* grid_a, size_t* smem_a, int* grid_m, size_t* smem_m) {
+int exec_grid(int sms, int w, int* grid_a, size_t* smem_a, int* grid_m, size_t* smem_m) {
   static int occ_a[64] = {0}, occ_m[64] = {0};
+  static size_t occ_a_smem[64] = {0};
   int dev;
   RS_CUDA(cudaGetDevice(&dev));
-  *smem_a = Exec<K, TB>::smem_bytes();
+  *smem_a = Exec<K, TB>::smem_bytes(w);
   *smem_m = MergeCfg<K, TB>::SMEM;
-  if (occ_a[dev] == 0) {
-    RS_CUDA(cudaFuncSetAttribute(k_phaseA<K, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem_a));
+  if (occ_m[dev] == 0) {
+    RS_CUDA(cudaFuncSetAttribute(k_phaseA<K, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)Exec<K, TB>::smem_bytes(1)));
     RS_CUDA(cudaFuncSetAttribute(k_merge_exec<K, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem_m));
+    int o = 0;
+    RS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_merge_exec<K, TB>, kMergeThreads, *smem_m));
+    if (o < 1) return fail(RS_ECUDA, "merge executor does not fit on an SM");
+    occ_m[dev] = o;
+  }
+  if (occ_a_smem[dev] != *smem_a) {
     int o = 0;
     RS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_phaseA<K, TB>, kExecThreads, *smem_a));
     if (o < 1) return fail(RS_ECUDA, "phase-A kernel does not fit on an SM");
     occ_a[dev] = o;
-    RS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_merge_exec<K, TB>, kMergeThreads, *smem_m));
-    if (o < 1) return fail(RS_ECUDA, "merge executor does not fit on an SM");
-    occ_m[dev] = o;
+    occ_a_smem[dev] = *smem_a;
   }
   *grid_a = sms * occ_a[dev];
   *grid_m = sms * occ_m[dev];
@@ -308,7 +314,7 @@ template <typename K, int TB>
 ClassifyArgs classify_args(const WsView& V, const Layout& L, int64_t n, int w, int classic, int msuper, int peek) {
   return ClassifyArgs{n, w, classic, L.fcap, L.tile, MergeCfg<K, TB>::TILE, msuper, peek, L.leaf_base,
                       V.leaf_start, V.leaf_info, V.leaf_depth, V.depth, V.node_s, V.node_e, V.parent, V.need,
-                      V.cls, V.tasks, V.met};
+                      V.cls, V.tasks, V.met, V.node_a, V.node_b, Exec<K, TB>::maxb_for(w)};
 }
 
 // Phase A (fused subtrees, large leaves) + the merge executor.
@@ -317,7 +323,7 @@ int launch_exec(K* keys, void* tags, int64_t n, int w, int classic, int msuper, 
                 int sms, cudaStream_t st) {
   int grid_a, grid_m;
   size_t smem_a, smem_m;
-  if (int e = exec_grid<K, TB>(sms, &grid_a, &smem_a, &grid_m, &smem_m)) return e;
+  if (int e = exec_grid<K, TB>(sms, w, &grid_a, &smem_a, &grid_m, &smem_m)) return e;
   ExecArgs E;
   E.key[0] = keys;
   E.key[1] = V.key1;
@@ -340,6 +346,7 @@ int launch_exec(K* keys, void* tags, int64_t n, int w, int classic, int msuper, 
   E.done = V.done;
   E.tasks = V.tasks;
   E.met = V.met;
+  E.maxb = Exec<K, TB>::maxb_for(w);
   k_phaseA<K, TB><<<grid_a, kExecThreads, smem_a, st>>>(E);
   RS_CUDA(cudaGetLastError());
   prof_mark(2, st);
