@@ -29,7 +29,6 @@ struct ExecCfg {
   static constexpr int IPT = (kb == 4) ? 15 : 11;  // odd: conflict-free blocked->smem writes
   static constexpr int TILE = kExecThreads * IPT;
   static constexpr int FCAP = (eb <= 8) ? 4096 : 2048;  // fused-subtree capacity (elements)
-  static constexpr int IPTF = 8;                        // outputs per fused merge chunk
   static constexpr int MAXB = FCAP / 2 + 2;             // boundaries inside a fused subtree (any w)
 };
 
@@ -387,8 +386,11 @@ struct Exec {
   static constexpr size_t smem_merge() { return (size_t)C::TILE * (C::kb + TB) + 64; }
   // leaves of a fused subtree are >= max(w, 2) long except the array's last one
   static constexpr int maxb_for(int w) { return C::FCAP / (w > 2 ? w : 2) + 2; }
+  // two symmetric span buffers (keys, tags), each with 32 B of bulk-copy alignment slack
+  __host__ __device__ static constexpr size_t kbuf_bytes() { return (size_t)C::FCAP * C::kb + 32; }
+  __host__ __device__ static constexpr size_t tbuf_bytes() { return HAS_TAGS ? (size_t)C::FCAP * TB + 32 : 0; }
   static constexpr size_t smem_fuse(int maxb) {
-    return 2 * (size_t)C::FCAP * (C::kb + TB) + 64 + (size_t)maxb * (3 * 2 + 1 + 2 + 2) + 256;
+    return 2 * (kbuf_bytes() + tbuf_bytes()) + (size_t)(maxb + 1) * (3 * 2 + 1 + 2 + 2 + 2 + 4 + 1) + 256;
   }
   static constexpr size_t smem_bytes(int w) { return smem_fuse(maxb_for(w)); }
 
@@ -546,63 +548,78 @@ struct Exec {
   }
 
   // --- fused subtree: form its leaves and run all of its merges in SMEM ---
-  __device__ static void fuse_task(const ExecArgs& E, uint32_t u, unsigned char* smem, uint64_t* bar,
-                                   uint32_t& fphase, unsigned long long& comps) {
+  struct Span {
+    pos_t s, e;
+    int64_t la, lb;
+    int droot;
+  };
+  __device__ static Span span_of(const ExecArgs& E, uint32_t u) {
+    Span f;
+    if (u >= E.leaf_base) {
+      f.la = f.lb = u - E.leaf_base;
+      f.s = E.leaf_start[f.la];
+      f.e = E.leaf_start[f.la + 1];
+      f.droot = E.leaf_depth[f.la];
+    } else {
+      f.la = E.node_a[u];
+      f.lb = E.node_b[u];
+      f.s = E.node_s[u];
+      f.e = E.node_e[u];
+      f.droot = E.depth[u];
+    }
+    return f;
+  }
+  __device__ static unsigned char* kbuf(unsigned char* smem, int b) { return smem + (size_t)b * kbuf_bytes(); }
+  __device__ static unsigned char* tbuf(unsigned char* smem, int b) {
+    return smem + 2 * kbuf_bytes() + (size_t)b * tbuf_bytes();
+  }
+  // Thread 0: bulk-copy the span's 16B-aligned cover into buffer b; element
+  // offsets of the span inside it go to off[0] (keys) / off[1] (tags).
+  __device__ static void span_issue(const ExecArgs& E, const Span& f, unsigned char* smem, int b, uint64_t* bar,
+                                    int32_t* off) {
+    fence_proxy_async_smem();  // earlier generic accesses of the buffer come first
+    auto cover = [](const void* base, pos_t e0, pos_t e1, int es) {
+      uintptr_t a0 = reinterpret_cast<uintptr_t>(base) + (uintptr_t)e0 * es;
+      uintptr_t a1 = reinterpret_cast<uintptr_t>(base) + (uintptr_t)e1 * es;
+      return (uint32_t)(((a1 + 15) & ~(uintptr_t)15) - (a0 & ~(uintptr_t)15));
+    };
+    uint32_t tx = cover(E.key[0], f.s, f.e, C::kb) + (HAS_TAGS ? cover(E.tag[0], f.s, f.e, TB) : 0u);
+    mbar_arrive_tx(bar, tx);
+    int32_t ok, ot = 0;
+    tma_window(kbuf(smem, b), E.key[0], f.s, f.e, C::kb, bar, &ok);
+    if (HAS_TAGS) tma_window(tbuf(smem, b), E.tag[0], f.s, f.e, TB, bar, &ot);
+    off[0] = ok;
+    off[1] = ot;
+  }
+
+  // Runs fused task u whose span was issued into buffer ib (offsets in off[]).
+  // `hook()` runs in every thread once the span buffers are no longer read
+  // except for the write-back of the result (buffer returned by the call); the
+  // other buffer is then free.
+  template <typename Step, typename Hook>
+  __device__ static int fuse_task(const ExecArgs& E, const Span& f, int ib, unsigned char* smem, uint64_t* bar,
+                                  uint32_t& fphase, int32_t* off, Step&& step, Hook&& hook,
+                                  unsigned long long& comps) {
     __shared__ uint32_t s_scan[40];
     __shared__ int s_dmax;
-    __shared__ int32_t s_off[2];
-    // X[0]/Y[0] receive the span by 1D bulk copy of its 16B-aligned cover (32B slack)
-    unsigned char* p = smem;
-    unsigned char* x0raw = p;
-    p += (size_t)C::FCAP * C::kb + 32;
     K* X[2];
     T* Y[2];
-    X[1] = reinterpret_cast<K*>(p);
-    p += (size_t)C::FCAP * C::kb;
-    unsigned char* y0raw = p;
-    p += HAS_TAGS ? (size_t)C::FCAP * TB + 32 : 0;
-    Y[1] = reinterpret_cast<T*>(p);
-    p += HAS_TAGS ? (size_t)C::FCAP * TB : 0;
+    unsigned char* p = smem + 2 * (kbuf_bytes() + tbuf_bytes());
     const int MB = E.maxb;
     uint16_t* ns = reinterpret_cast<uint16_t*>(p);
     uint16_t* nm = ns + MB;
     uint16_t* ne = nm + MB;
-    uint16_t* lst = ne + MB;   // level node list
-    uint16_t* loff = lst + MB; // level chunk offsets
-    uint8_t* dep = reinterpret_cast<uint8_t*>(loff + MB);
+    uint16_t* lst = ne + MB;     // level node list
+    uint16_t* loff = lst + MB;   // level output offsets
+    uint16_t* lsv = loff + MB;   // leaf starts (MB + 1)
+    uint32_t* linf = reinterpret_cast<uint32_t*>(lsv + MB + 2);  // leaf info (MB + 1), 4B-aligned
+    uint8_t* ldpv = reinterpret_cast<uint8_t*>(linf + MB + 1);   // leaf depth parity
+    uint8_t* dep = ldpv + MB + 1;
 
-    int64_t la, lb;
-    pos_t s, e;
-    int droot;
-    if (u >= E.leaf_base) {
-      la = lb = u - E.leaf_base;
-      s = E.leaf_start[la];
-      e = E.leaf_start[la + 1];
-      droot = E.leaf_depth[la];
-    } else {
-      la = E.node_a[u];
-      lb = E.node_b[u];
-      s = E.node_s[u];
-      e = E.node_e[u];
-      droot = E.depth[u];
-    }
+    const int64_t la = f.la, lb = f.lb;
+    const pos_t s = f.s, e = f.e;
+    const int droot = f.droot;
     int len = int(e - s);
-    if (threadIdx.x == 0) {
-      // previous task's generic-proxy smem accesses are ordered before the bulk writes
-      fence_proxy_async_smem();
-      auto cover = [](const void* base, pos_t e0, pos_t e1, int es) {
-        uintptr_t a0 = reinterpret_cast<uintptr_t>(base) + (uintptr_t)e0 * es;
-        uintptr_t a1 = reinterpret_cast<uintptr_t>(base) + (uintptr_t)e1 * es;
-        return (uint32_t)(((a1 + 15) & ~(uintptr_t)15) - (a0 & ~(uintptr_t)15));
-      };
-      uint32_t tx = cover(E.key[0], s, e, C::kb) + (HAS_TAGS ? cover(E.tag[0], s, e, TB) : 0u);
-      mbar_arrive_tx(bar, tx);
-      int32_t ok, ot = 0;
-      tma_window(x0raw, E.key[0], s, e, C::kb, bar, &ok);
-      if (HAS_TAGS) tma_window(y0raw, E.tag[0], s, e, TB, bar, &ot);
-      s_off[0] = ok;
-      s_off[1] = ot;
-    }
     // the subtree's node table while the span is in flight
     int nbd = int(lb - la);
     int dmax_local = droot;
@@ -616,12 +633,36 @@ struct Exec {
       dep[x] = (uint8_t)dd;
       dmax_local = dd > dmax_local ? dd : dmax_local;
     }
+    const int nlf = nbd + 1;
+    __shared__ int s_nat;  // some leaf is a natural run needing a copy / reversal
+    if (threadIdx.x == 0) s_nat = 0;
+    __syncthreads();
+    bool nat = false;
+    for (int x = threadIdx.x; x < nlf; x += blockDim.x) {
+      int64_t li = la + x;
+      pos_t ls = E.leaf_start[li], le = E.leaf_start[li + 1];
+      uint32_t info = E.leaf_info[li];
+      uint8_t dp = (uint8_t)(E.leaf_depth[li] & 1);
+      lsv[x] = (uint16_t)(ls - s);
+      linf[x] = info;
+      ldpv[x] = dp;
+      uint32_t nl = info & 0x7fffffffu;
+      bool natural = nl >= (uint32_t)E.w || (pos_t)nl >= le - ls;
+      nat |= natural && ((info >> 31) != 0 || dp == 1);
+    }
+    if (nat) s_nat = 1;
+    if (threadIdx.x == 0) {
+      lsv[nlf] = (uint16_t)len;  // len <= FCAP < 65536
+      step();
+    }
     __syncthreads();
     if (nbd > 0) atomicMax(&s_dmax, dmax_local);
     mbar_wait(bar, fphase);
     fphase ^= 1u;
-    X[0] = reinterpret_cast<K*>(x0raw) + s_off[0];
-    Y[0] = HAS_TAGS ? reinterpret_cast<T*>(y0raw) + s_off[1] : nullptr;
+    X[0] = reinterpret_cast<K*>(kbuf(smem, ib)) + off[0];
+    X[1] = reinterpret_cast<K*>(kbuf(smem, ib ^ 1));
+    Y[0] = HAS_TAGS ? reinterpret_cast<T*>(tbuf(smem, ib)) + off[1] : nullptr;
+    Y[1] = HAS_TAGS ? reinterpret_cast<T*>(tbuf(smem, ib ^ 1)) : nullptr;
     __builtin_assume(__isShared(X[0]));
     __builtin_assume(__isShared(X[1]));
     if (HAS_TAGS) {
@@ -629,37 +670,50 @@ struct Exec {
       __builtin_assume(__isShared(Y[1]));
     }
     __syncthreads();
-    // leaves: warp per leaf
-    int wid = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
-    for (int64_t li = la + wid; li <= lb; li += nwarp) {
-      int ls = int(E.leaf_start[li] - s), le = int(E.leaf_start[li + 1] - s), ll = le - ls;
-      uint32_t info = E.leaf_info[li];
-      uint32_t nl = info & 0x7fffffffu;
-      bool desc = (info >> 31) != 0;
-      int L = (nl >= (uint32_t)E.w) ? ll : (int)nl;
-      int dp = E.leaf_depth[li] & 1;
-      if (L >= ll) {
-        if (desc) {
-          if (dp == 0) {
-            for (int x = lane; x < ll / 2; x += 32) {
-              K a = X[0][ls + x], b = X[0][le - 1 - x];
-              X[0][ls + x] = b;
-              X[0][le - 1 - x] = a;
-              if (HAS_TAGS) { T ta = Y[0][ls + x]; Y[0][ls + x] = Y[0][le - 1 - x]; Y[0][le - 1 - x] = ta; }
-            }
-          } else {
-            for (int x = lane; x < ll; x += 32) {
-              X[1][ls + x] = X[0][le - 1 - x];
-              if (HAS_TAGS) Y[1][ls + x] = Y[0][le - 1 - x];
-            }
+    // leaves.  Natural runs (copy / reversal into the depth-parity buffer):
+    // element-parallel over the whole span.  Runs extended by insertion sort
+    // (runcore.py:215-248): warp per leaf.
+    auto leaf_L = [&](int k, int ll) {
+      uint32_t nl = linf[k] & 0x7fffffffu;
+      return (nl >= (uint32_t)E.w) ? ll : (int)nl;
+    };
+    for (int x = s_nat ? (int)threadIdx.x : len; x < len; x += blockDim.x) {
+      int lo = 0, hi = nlf - 1;  // last leaf with start <= x
+      while (lo < hi) {
+        int md = (lo + hi + 1) >> 1;
+        if (lsv[md] <= x) lo = md; else hi = md - 1;
+      }
+      int ls = lsv[lo], le = lsv[lo + 1], ll = le - ls;
+      if (leaf_L(lo, ll) < ll) continue;  // insertion-sort leaf: below
+      bool desc = (linf[lo] >> 31) != 0;
+      int dp = ldpv[lo];
+      int r = x - ls;
+      if (desc) {
+        if (dp == 0) {
+          if (r < ll / 2) {
+            int y = le - 1 - r;
+            K a = X[0][x], b = X[0][y];
+            X[0][x] = b;
+            X[0][y] = a;
+            if (HAS_TAGS) { T ta = Y[0][x]; Y[0][x] = Y[0][y]; Y[0][y] = ta; }
           }
-        } else if (dp == 1) {
-          for (int x = lane; x < ll; x += 32) {
-            X[1][ls + x] = X[0][ls + x];
-            if (HAS_TAGS) Y[1][ls + x] = Y[0][ls + x];
-          }
+        } else {
+          X[1][x] = X[0][le - 1 - r];
+          if (HAS_TAGS) Y[1][x] = Y[0][le - 1 - r];
         }
-      } else {
+      } else if (dp == 1) {
+        X[1][x] = X[0][x];
+        if (HAS_TAGS) Y[1][x] = Y[0][x];
+      }
+    }
+    int wid = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
+    for (int k = wid; k < nlf; k += nwarp) {
+      int ls = lsv[k], le = lsv[k + 1], ll = le - ls;
+      int L = leaf_L(k, ll);
+      if (L >= ll) continue;
+      bool desc = (linf[k] >> 31) != 0;
+      int dp = ldpv[k];
+      {
         // insertionsort_presorted on the post-reversal chunk (runcore.py:215-248)
         int npre = L > 1 ? L : 1;
         auto vidx = [&](int t) { return (desc && t < L) ? ls + L - 1 - t : ls + t; };
@@ -710,32 +764,34 @@ struct Exec {
       }
       __syncwarp();
     }
+    if (threadIdx.x == 0) step();
     __syncthreads();
     if (nbd > 0) {
       int dmax = s_dmax;
       const int per = (nbd + blockDim.x - 1) / blockDim.x;
       for (int dd = dmax; dd >= droot; --dd) {
-        // compact this level's nodes and their chunk offsets (packed nodes<<16 | chunks)
+        // this level's nodes in position order with their output offsets
+        // (packed nodes << 16 | elements; a level's elements <= FCAP < 2^16)
         uint32_t mine = 0;
         int x0 = threadIdx.x * per;
         for (int q = 0; q < per; ++q) {
           int x = x0 + q;
-          if (x < nbd && dep[x] == dd) mine += (1u << 16) + (uint32_t)((ne[x] - ns[x] + C::IPTF - 1) / C::IPTF);
+          if (x < nbd && dep[x] == dd) mine += (1u << 16) + (uint32_t)(ne[x] - ns[x]);
         }
         uint32_t total;
         uint32_t pre = block_excl_scan_u32(mine, s_scan, &total);
-        uint32_t nidx = pre >> 16, coff = pre & 0xffffu;
+        uint32_t nidx = pre >> 16, eoff = pre & 0xffffu;
         for (int q = 0; q < per; ++q) {
           int x = x0 + q;
           if (x < nbd && dep[x] == dd) {
             lst[nidx] = (uint16_t)x;
-            loff[nidx] = (uint16_t)coff;
+            loff[nidx] = (uint16_t)eoff;
             ++nidx;
-            coff += (ne[x] - ns[x] + C::IPTF - 1) / C::IPTF;
+            eoff += ne[x] - ns[x];
           }
         }
         __syncthreads();
-        int nlev = int(total >> 16), nchunk = int(total & 0xffffu);
+        const int nlev = int(total >> 16), tot = int(total & 0xffffu);
         const K* Xs = X[(dd + 1) & 1];
         K* Xd = X[dd & 1];
         const T* Ys = Y[(dd + 1) & 1];
@@ -746,39 +802,46 @@ struct Exec {
           __builtin_assume(__isShared(Ys));
           __builtin_assume(__isShared(Yd));
         }
-        for (int c = threadIdx.x; c < nchunk; c += blockDim.x) {
-          // node: last level entry with loff <= c
-          int lo = 0, hi = nlev - 1;
+        // every thread merges one equal share of the level's concatenated output
+        const int cs = (tot + (int)blockDim.x - 1) / (int)blockDim.x;
+        int o0 = threadIdx.x * cs;
+        const int o1 = o0 + cs < tot ? o0 + cs : tot;
+        if (o0 < o1) {
+          int lo = 0, hi = nlev - 1;  // node: last level entry with loff <= o0
           while (lo < hi) {
             int md = (lo + hi + 1) >> 1;
-            if (loff[md] <= c) lo = md; else hi = md - 1;
+            if (loff[md] <= o0) lo = md; else hi = md - 1;
           }
-          int x = lst[lo];
-          int a0 = ns[x], mm = nm[x], e0 = ne[x];
-          int na = mm - a0, nb = e0 - mm, size = e0 - a0;
-          int o = (c - loff[lo]) * C::IPTF;
-          int cnt = size - o < C::IPTF ? size - o : C::IPTF;
-          int ai = smem_merge_path(Xs + a0, na, Xs + mm, nb, o);
-          int bi = o - ai;
-          for (int q = 0; q < cnt; ++q) {
-            bool takeA = (bi >= nb) || (ai < na && Xs[a0 + ai] <= Xs[mm + bi]);
-            int si = takeA ? a0 + ai : mm + bi;
-            Xd[a0 + o + q] = Xs[si];
-            if (HAS_TAGS) Yd[a0 + o + q] = Ys[si];
-            ai += takeA;
-            bi += !takeA;
-          }
-          if (E.classic && o == 0) {
-            K maxL = Xs[mm - 1], maxR = Xs[e0 - 1];
-            int rl = smem_count(Xs + mm, nb, maxL, false);
-            int lr = smem_count(Xs + a0, na, maxR, true);
-            int pl = na - 1 + rl, pr = nb - 1 + lr;
-            comps += (unsigned long long)((pl < pr ? pl : pr) + 1);
+          for (int k = lo; o0 < o1; ++k) {
+            int x = lst[k];
+            int a0 = ns[x], mm = nm[x], e0 = ne[x];
+            int na = mm - a0, nb = e0 - mm, size = e0 - a0;
+            int o = o0 - loff[k];
+            int cnt = size - o < o1 - o0 ? size - o : o1 - o0;
+            int ai = smem_merge_path(Xs + a0, na, Xs + mm, nb, o);
+            int bi = o - ai;
+            for (int q = 0; q < cnt; ++q) {
+              bool takeA = (bi >= nb) || (ai < na && Xs[a0 + ai] <= Xs[mm + bi]);
+              int si = takeA ? a0 + ai : mm + bi;
+              Xd[a0 + o + q] = Xs[si];
+              if (HAS_TAGS) Yd[a0 + o + q] = Ys[si];
+              ai += takeA;
+              bi += !takeA;
+            }
+            if (E.classic && o == 0) {
+              K maxL = Xs[mm - 1], maxR = Xs[e0 - 1];
+              int rl = smem_count(Xs + mm, nb, maxL, false);
+              int lr = smem_count(Xs + a0, na, maxR, true);
+              int pl = na - 1 + rl, pr = nb - 1 + lr;
+              comps += (unsigned long long)((pl < pr ? pl : pr) + 1);
+            }
+            o0 += cnt;
           }
         }
         __syncthreads();
       }
     }
+    hook();  // result in X[droot & 1]; the other buffer is free
     K* gd = reinterpret_cast<K*>(E.key[droot & 1]);
     T* hd = HAS_TAGS ? reinterpret_cast<T*>(E.tag[droot & 1]) : nullptr;
     const K* Xr = X[droot & 1];
@@ -787,38 +850,99 @@ struct Exec {
       gd[s + x] = Xr[x];
       if (HAS_TAGS) hd[s + x] = Yr[x];
     }
+    return ib ^ (droot & 1);
   }
 };
 
 // Phase A: fused subtrees and big-leaf tiles (no dependencies among them).
+// Thread 0 claims the next task and fetches its record and span while the
+// current one runs; a fused next task's span is bulk-copied into the span
+// buffer the current task has finished with, overlapping its write-back.
 template <typename K, int TB>
 __global__ void __launch_bounds__(kExecThreads, 3) k_phaseA(ExecArgs E) {
+  using X = Exec<K, TB>;
+  using Span = typename X::Span;
   extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ unsigned long long s_task;
   __shared__ unsigned long long sred[32];
   __shared__ __align__(8) uint64_t s_bar;
+  __shared__ uint64_t s_rec;       // record of the task to run next (kind 3: none)
+  __shared__ int32_t s_off[2];     // its span's offsets in buffer s_ib, if issued
+  __shared__ int s_ib, s_issued;
+  const unsigned long long ntasks = E.met->phaseA;
+  constexpr uint64_t kNone = ~0ull;
+  // thread 0's view of the next task
+  uint64_t nrec = kNone;
+  unsigned long long nt = 0;
+  Span nf{};
+  // the claim is a chain of dependent round trips; stage() advances it one
+  // step so thread 0 never waits on it in the middle of a task
+  int nst = 0;
+  auto stage = [&]() {
+    if (nst == 0) nt = atomicAdd(&E.met->task_ctr_A, 1ull);
+    else if (nst == 1) nrec = nt < ntasks ? E.tasks[nt] : kNone;
+    else if (nst == 2 && nrec != kNone && task_kind(nrec) == kTaskFuse) nf = X::span_of(E, task_id(nrec));
+    if (nst < 3) ++nst;
+  };
+  auto claim = [&]() {
+    nst = 0;
+    while (nst < 3) stage();
+  };
   if (threadIdx.x == 0) {
     mbar_init(&s_bar, 1);
     mbar_fence_init();
+    claim();
+    s_rec = nrec;
+    s_ib = 0;
+    s_issued = 0;
+    if (nrec != kNone && task_kind(nrec) == kTaskFuse) {
+      X::span_issue(E, nf, smem, 0, &s_bar, s_off);
+      s_issued = 1;
+    }
   }
   __syncthreads();
   uint32_t fphase = 0;
   unsigned long long comps = 0;
-  unsigned long long ntasks = E.met->phaseA;
   for (;;) {
-    if (threadIdx.x == 0) s_task = atomicAdd(&E.met->task_ctr_A, 1ull);
-    __syncthreads();
-    unsigned long long t = s_task;
-    if (t >= ntasks) break;
-    uint64_t rec = E.tasks[t];
+    uint64_t rec = s_rec;
+    int ib = s_ib;
+    int issued = s_issued;
+    if (rec == kNone) break;
     uint32_t kind = task_kind(rec), id = task_id(rec), tile = task_tile(rec);
-    if (kind == kTaskLeaf) Exec<K, TB>::leaf_task(E, id - E.leaf_base, tile);
-    else Exec<K, TB>::fuse_task(E, id, smem, &s_bar, fphase, comps);
+    __syncthreads();  // everyone has read the shared slots
+    if (threadIdx.x == 0) {
+      nst = 0;
+      stage();  // claim issued; record and span follow during the task
+    }
+    // thread 0 publishes the next task; a fused one is issued into buffer `fb`
+    auto publish = [&](int fb) {
+      if (threadIdx.x == 0) {
+        while (nst < 3) stage();
+        s_rec = nrec;
+        s_ib = fb;
+        s_issued = 0;
+        if (nrec != kNone && task_kind(nrec) == kTaskFuse) {
+          X::span_issue(E, nf, smem, fb, &s_bar, s_off);
+          s_issued = 1;
+        }
+      }
+    };
+    if (kind == kTaskLeaf) {
+      X::leaf_task(E, id - E.leaf_base, tile);
+      publish(ib);  // no buffer in use
+    } else {
+      Span f = X::span_of(E, id);
+      if (!issued) {  // (never: a fused task is always issued when published)
+        if (threadIdx.x == 0) X::span_issue(E, f, smem, ib, &s_bar, s_off);
+        __syncthreads();
+      }
+      X::fuse_task(E, f, ib, smem, &s_bar, fphase, s_off, stage,
+                   [&]() { publish(ib ^ (f.droot & 1) ^ 1); }, comps);
+    }
     __syncthreads();
     if (threadIdx.x == 0) release_add_u32(E.done + id, 1u);
   }
-  unsigned long long s = block_sum(comps, sred);
-  if (threadIdx.x == 0 && s) atomicAdd(&E.met->comparisons, s);
+  unsigned long long sum = block_sum(comps, sred);
+  if (threadIdx.x == 0 && sum) atomicAdd(&E.met->comparisons, sum);
 }
 
 }  // namespace rs
