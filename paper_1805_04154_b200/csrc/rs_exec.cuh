@@ -146,11 +146,17 @@ __host__ __device__ inline int64_t ord_chunk(int64_t r) {
 // task count to their (chunk, depth) cell for the ordered fill.
 __device__ void d_classify(ClassifyArgs A, uint32_t* __restrict__ chunk_depth) {
   __shared__ unsigned long long sred[32];
+  __shared__ uint32_t s_cd[kMaxDepth];  // this iteration's per-depth task counts (one chunk)
   int64_t r = (int64_t)A.met->n_leaves;
-  const int64_t ochunk = ord_chunk(r);
+  const int64_t ochunk = ord_chunk(r);  // a multiple of blockDim: one chunk per block iteration
   unsigned long long comps = 0, mcost = 0, cntA = 0, mbig = 0;
+  unsigned long long dtl = 0;  // thread d < kMaxDepth: tasks of depth d over all iterations
   unsigned maxd = 0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < r; i += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x; i0 < r; i0 += (int64_t)gridDim.x * blockDim.x) {
+    for (int d = threadIdx.x; d < kMaxDepth; d += blockDim.x) s_cd[d] = 0;
+    __syncthreads();
+    const int64_t i = i0 + threadIdx.x;
+    if (i < r) {
     // leaf: detection comparisons (runcore.py:154/157 closed form)
     pos_t s0 = A.leaf_start[i], len = A.leaf_start[i + 1] - s0;
     if (!A.peek && s0 < A.n - 1) {
@@ -177,12 +183,21 @@ __device__ void d_classify(ClassifyArgs A, uint32_t* __restrict__ chunk_depth) {
         A.need[i] = (uint32_t)tn;
         mbig += span;
         int d = A.depth[i];
-        atomicAdd(&chunk_depth[(i / ochunk) * kMaxDepth + d], (uint32_t)tk);
-        atomicAdd(&A.met->depth_tiles[d], (unsigned long long)tk);
+        atomicAdd(&s_cd[d], (uint32_t)tk);
         maxd = d > (int)maxd ? d : maxd;
       } else A.need[i] = 0;
     }
+    }
+    __syncthreads();
+    for (int d = threadIdx.x; d < kMaxDepth; d += blockDim.x) {
+      uint32_t v = s_cd[d];
+      if (v) {
+        atomicAdd(&chunk_depth[(i0 / ochunk) * kMaxDepth + d], v);
+        dtl += v;
+      }
+    }
   }
+  if (threadIdx.x < kMaxDepth && dtl) atomicAdd(&A.met->depth_tiles[threadIdx.x], dtl);
   unsigned long long s = block_sum(comps, sred);
   if (threadIdx.x == 0 && s) atomicAdd(&A.met->comparisons, s);
   s = block_sum(mcost, sred);
@@ -226,28 +241,45 @@ __device__ void d_order_scan(const DevMetrics* __restrict__ met, uint32_t* __res
 
 __device__ void d_task_fill(ClassifyArgs A, const uint32_t* __restrict__ chunk_depth) {
   __shared__ uint32_t run[kMaxDepth];
+  __shared__ uint32_t s_wsum[kMaxDepth * 8];  // [depth][warp]: warp totals, then warp offsets
   // staging lives in the kernel's dynamic shared memory (dead by this phase)
   extern __shared__ __align__(16) unsigned char smem_fill[];
   uint32_t* s_slot = reinterpret_cast<uint32_t*>(smem_fill);
-  uint8_t* s_dep = smem_fill + kOrdChunkMax * 4;
+  uint32_t* s_tk = s_slot + kOrdChunkMax;
+  uint8_t* s_dep = smem_fill + kOrdChunkMax * 8;
   int64_t r = (int64_t)A.met->n_leaves;
-  // phase-A tasks (any order), element-parallel
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < r; i += (int64_t)gridDim.x * blockDim.x) {
-    uint32_t lid = A.leaf_base + (uint32_t)i;
-    int c = A.cls[lid];
-    if (c == 1) {
-      unsigned long long slot = atomicAdd(&A.met->cursorA, 1ull);
-      A.tasks[slot] = make_task(kTaskFuse, 0, lid);
-    } else if (c == 2) {
-      uint32_t tl = A.need[lid];
-      unsigned long long slot = atomicAdd(&A.met->cursorA, (unsigned long long)tl);
-      for (uint32_t k = 0; k < tl; ++k) A.tasks[slot + k] = make_task(kTaskLeaf, k, lid);
+#ifdef RS_INSTR
+  unsigned long long tf0 = globaltimer_ns();
+#endif
+  // phase-A tasks (any order): element-parallel, slots from one atomic per block
+  __shared__ uint32_t s_sc[40];
+  __shared__ unsigned long long s_base;
+  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x; i0 < r; i0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = i0 + threadIdx.x;
+    int c = 0, cn = 0;
+    uint32_t tl = 0, lid = 0;
+    if (i < r) {
+      lid = A.leaf_base + (uint32_t)i;
+      c = A.cls[lid];
+      if (c == 2) tl = A.need[lid];
+      if (i >= 1) cn = A.cls[i];
     }
-    if (i >= 1 && A.cls[i] == 1) {
-      unsigned long long slot = atomicAdd(&A.met->cursorA, 1ull);
-      A.tasks[slot] = make_task(kTaskFuse, 0, (uint32_t)i);
-    }
+    uint32_t cnt = (c == 1 ? 1u : (c == 2 ? tl : 0u)) + (cn == 1 ? 1u : 0u);
+    uint32_t tot;
+    uint32_t pre = block_excl_scan_u32(cnt, s_sc, &tot);
+    if (threadIdx.x == 0) s_base = tot ? atomicAdd(&A.met->cursorA, (unsigned long long)tot) : 0ull;
+    __syncthreads();
+    unsigned long long slot = s_base + pre;
+    if (c == 1) A.tasks[slot++] = make_task(kTaskFuse, 0, lid);
+    else if (c == 2)
+      for (uint32_t k = 0; k < tl; ++k) A.tasks[slot++] = make_task(kTaskLeaf, k, lid);
+    if (cn == 1) A.tasks[slot++] = make_task(kTaskFuse, 0, (uint32_t)i);
+    __syncthreads();
   }
+#ifdef RS_INSTR
+  unsigned long long tf1 = globaltimer_ns();
+  if (threadIdx.x == 0) atomicMax(&A.met->prep_ts[12], tf1 - tf0);
+#endif
   // merge tasks: slots by (depth, position); chunk boundaries staged in smem,
   // warp 0 assigns ordered slots, all threads write.
   const int64_t oc = ord_chunk(r);
@@ -261,47 +293,72 @@ __device__ void d_task_fill(ClassifyArgs A, const uint32_t* __restrict__ chunk_d
     for (int64_t x = threadIdx.x; x < cnt_i; x += blockDim.x) {
       int64_t i = i0 + x;
       uint32_t dv = 0xffu, tv = 0;
-      if (i >= 1 && A.cls[i] == 2) {
-        dv = A.depth[i];
-        tv = (A.need[i] + A.msuper - 1) / A.msuper;
+      if (i >= 1) {
+        int c = A.cls[i];  // independent loads: one round trip
+        uint32_t dd = A.depth[i], nd = A.need[i];
+        if (c == 2) {
+          dv = dd;
+          tv = (nd + A.msuper - 1) / A.msuper;
+        }
       }
       s_dep[x] = (uint8_t)dv;
       s_slot[x] = tv;
+      s_tk[x] = tv;
     }
     __syncthreads();
-    if (threadIdx.x < 32) {
-      for (int64_t g = 0; g < cnt_i; g += 32) {
-        int64_t x = g + lane;
-        int d = x < cnt_i ? s_dep[x] : 255;
-        uint32_t tk = x < cnt_i ? s_slot[x] : 0;
-        uint32_t pre = 0;
+#ifdef RS_INSTR
+    unsigned long long tq0 = globaltimer_ns();
+    if (threadIdx.x == 0) atomicMax(&A.met->prep_ts[14], tq0 - tf1);
+#endif
+    // ordered slots, 256 nodes per round: every warp ranks its 32 nodes among
+    // same-depth peers (shuffle prefix), per-depth warp totals are scanned
+    // across warps, and `run` carries each depth's cursor to the next round
+    for (int64_t g = 0; g < cnt_i; g += blockDim.x) {
+      int64_t x = g + threadIdx.x;
+      int d = x < cnt_i ? s_dep[x] : 255;
+      uint32_t tk = x < cnt_i ? s_tk[x] : 0;
+      uint32_t pre = 0;
 #pragma unroll
-        for (int k = 1; k < 32; ++k) {
-          int dk = __shfl_up_sync(0xffffffffu, d, k);
-          uint32_t tkk = __shfl_up_sync(0xffffffffu, tk, k);
-          if (lane >= k && dk == d) pre += tkk;
-        }
-        uint32_t mask = __match_any_sync(0xffffffffu, d);
-        uint32_t slot = d != 255 ? run[d] + pre : 0;
-        __syncwarp();
-        if (d != 255) {
-          s_slot[x] = slot;
-          if (lane == 31 - __clz(mask)) run[d] = slot + tk;
-        }
-        __syncwarp();
+      for (int k = 1; k < 32; ++k) {
+        int dk = __shfl_up_sync(0xffffffffu, d, k);
+        uint32_t tkk = __shfl_up_sync(0xffffffffu, tk, k);
+        if (lane >= k && dk == d) pre += tkk;
       }
+      uint32_t mask = __match_any_sync(0xffffffffu, d);
+      const int wid = threadIdx.x >> 5;
+      for (int q = threadIdx.x; q < kMaxDepth * 8; q += blockDim.x) s_wsum[q] = 0;
+      __syncthreads();
+      if (d != 255 && lane == 31 - __clz(mask)) s_wsum[d * 8 + wid] = pre + tk;  // warp total per depth
+      __syncthreads();
+      if (threadIdx.x < kMaxDepth) {  // depth d: exclusive scan over the 8 warps, advance the cursor
+        uint32_t acc = run[threadIdx.x];
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+          uint32_t v = s_wsum[threadIdx.x * 8 + w];
+          s_wsum[threadIdx.x * 8 + w] = acc;
+          acc += v;
+        }
+        run[threadIdx.x] = acc;
+      }
+      __syncthreads();
+      if (d != 255) s_slot[x] = s_wsum[d * 8 + wid] + pre;
+      __syncthreads();
     }
-    __syncthreads();
+#ifdef RS_INSTR
+    if (threadIdx.x == 0) atomicMax(&A.met->prep_ts[15], globaltimer_ns() - tq0);
+#endif
     // one warp per big node writes its task records
     int wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     for (int64_t x = wid; x < cnt_i; x += nw) {
       if (s_dep[x] == 255) continue;
       int64_t i = i0 + x;
-      uint32_t tk = (A.need[i] + A.msuper - 1) / A.msuper;
+      uint32_t tk = s_tk[x];
       uint32_t slot = s_slot[x];
       for (uint32_t k = lane; k < tk; k += 32) A.tasks[slot + k] = make_task(kTaskMerge, k, (uint32_t)i);
     }
   }
+#ifdef RS_INSTR
+  if (threadIdx.x == 0) atomicMax(&A.met->prep_ts[13], globaltimer_ns() - tf1);
+#endif
 }
 
 // ---------------------------------------------------------------- searches

@@ -122,6 +122,13 @@ __global__ void __launch_bounds__(256, 3) k_prep(PrepArgs P) {
   d_task_fill(P.CA, P.chunkdep);
   grid.sync();
   RS_TS(met, 9);
+#ifdef RS_INSTR
+  // calibration: the cost of a bare grid barrier
+  grid.sync();
+  RS_TS(met, 10);
+  grid.sync();
+  RS_TS(met, 11);
+#endif
 }
 
 }  // namespace rs

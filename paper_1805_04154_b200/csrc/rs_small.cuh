@@ -33,9 +33,6 @@ __device__ void small_tree(const TreeArrays& T, const ClassifyArgs& A, int F, un
   const int64_t r = (int64_t)met->n_leaves;
   if (r > kSmallR || r < 1) return;
   RS_TS(met, 5);
-#ifdef RS_INSTR
-  if (threadIdx.x == 0) met->prep_ts[11] = clock64();
-#endif
   pos_t* Ls = reinterpret_cast<pos_t*>(smem_small);
   uint64_t* Ks = reinterpret_cast<uint64_t*>(Ls + kSmallR + 1);
   pos_t* spans = reinterpret_cast<pos_t*>(Ks);  // after the trie ranges
@@ -116,9 +113,6 @@ __device__ void small_tree(const TreeArrays& T, const ClassifyArgs& A, int F, un
     met->max_stack_height = b;  // sorters.py:500-502
   }
   RS_TS(met, 6);
-#ifdef RS_INSTR
-  if (tid == 0) met->prep_ts[12] = clock64();
-#endif
   // ---- trie ranges, parents, children, spans (d_tree)
   pos_t myspan[kSmallPer];
 #pragma unroll
@@ -204,9 +198,6 @@ __device__ void small_tree(const TreeArrays& T, const ClassifyArgs& A, int F, un
   }
   __syncthreads();
   RS_TS(met, 7);
-#ifdef RS_INSTR
-  if (tid == 0) met->prep_ts[13] = clock64();
-#endif
   // ---- classification (d_classify), contiguous items per thread
   const int64_t per = (r + nt - 1) / nt;
   const int64_t i0 = (int64_t)tid * per;
@@ -283,9 +274,6 @@ __device__ void small_tree(const TreeArrays& T, const ClassifyArgs& A, int F, un
   maxd = warp_max(maxd);
   if ((tid & 31) == 0 && maxd) atomicMax(&s_maxd, maxd);
   RS_TS(met, 8);
-#ifdef RS_INSTR
-  if (tid == 0) met->prep_ts[14] = clock64();
-#endif
   // ---- task records.  Slots come from block scans; the records are written
   // from a job list {first slot, id, count | kind << 30} (in the dead Ks / par
   // regions) by whole warps, so a node with many tiles is not written by one thread.
@@ -367,9 +355,6 @@ __device__ void small_tree(const TreeArrays& T, const ClassifyArgs& A, int F, un
     met->task_ctr_A = 0;
   }
   RS_TS(met, 9);
-#ifdef RS_INSTR
-  if (tid == 0) met->prep_ts[15] = clock64();
-#endif
 }
 
 }  // namespace rs

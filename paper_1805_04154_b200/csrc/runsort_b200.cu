@@ -390,7 +390,7 @@ int run_powersort(K* keys, void* tags, int64_t n, int w, int classic, unsigned c
   if (gbatch < 1) gbatch = 1;
   int tbatch = gbatch < kChainGroup ? gbatch : kChainGroup;
   size_t sm = 8 * (size_t)chain_warp_bytes(w, sizeof(K));
-  sm = std::max(sm, (size_t)kOrdChunkMax * 5 + 64);
+  sm = std::max(sm, (size_t)kOrdChunkMax * 9 + 64);
   sm = std::max(sm, (size_t)batch * W1 * 8 + (size_t)W1 * 8 + 64);
   sm = std::max(sm, (size_t)gbatch * W1 * 8);
   sm = std::max(sm, (size_t)tbatch * W1 * 8);
@@ -470,7 +470,7 @@ int run_peeksort(K* keys, void* tags, int64_t n, int w, int classic, unsigned ch
   PK.chunkdep_words = (nch_max + 1) * kMaxDepth;
   PK.done = V.done;
   PK.done_words = 2 * L.r_max + 2;
-  size_t sm = (size_t)kOrdChunkMax * 5 + 64;
+  size_t sm = (size_t)kOrdChunkMax * 9 + 64;
   static int occ[64] = {0};
   int dev;
   RS_CUDA(cudaGetDevice(&dev));
