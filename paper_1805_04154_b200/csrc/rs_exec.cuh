@@ -5,11 +5,16 @@
 // (stable two-run merge, ties to the left run; bitonic / classic comparison
 // accounting), sorters.py:474-516 (every pending run merged exactly once).
 //
-// Layout: keys/tags live in two HBM buffers, buf[0] = the caller's array and
-// buf[1] = scratch.  A node (or leaf) at tree depth d holds its sorted span in
-// buf[d & 1], so every merge reads buf[(d+1)&1] and writes buf[d&1]; the root
-// (depth 0) lands in the caller's array and no schedule can overwrite data that
-// is still to be read.
+// Layout: keys/tags live in three HBM buffers: buf[0] = the caller's array,
+// buf[1], buf[2] = scratch.  Phase-A items (leaves, fused subtrees) are formed
+// IN PLACE in buf[0], except at depth 1 where they go to buf[2]; a merge node
+// at depth d >= 1 writes buf[1 + (d & 1)] and the root writes buf[0].  So a
+// parent at depth d reads merge children from buf[node_buf(d + 1)], which it
+// does not write, and phase-A children from buf[0] (d >= 1) or buf[2] (root);
+// it overwrites only data of its grandchildren, already consumed by its
+// (complete) children; and the root, which runs last, is the only writer of
+// buf[0] after phase A.  Natural ascending leaves therefore cost nothing, and
+// descending ones one in-place reversal.
 //
 // One persistent kernel claims tasks in list order: first the "phase A" tasks
 // (fused subtrees whose span fits in shared memory -- leaves are formed and all
@@ -36,8 +41,8 @@ template <int TB> struct TagT { using type = uint32_t; };
 template <> struct TagT<8> { using type = uint64_t; };
 
 struct ExecArgs {
-  void* key[2];
-  void* tag[2];
+  void* key[3];
+  void* tag[3];
   pos_t n;
   int w;
   int classic;
@@ -58,8 +63,13 @@ struct ExecArgs {
   int maxb;  // node-table capacity of a fused subtree: FCAP / max(w, 2) + 2
 };
 
-__device__ __forceinline__ int leaf_mode(bool desc, int dpar) {
-  return desc ? (dpar ? kLeafRevCopy : kLeafSwap) : (dpar ? kLeafCopy : kLeafNone);
+// scratch buffer of a merge node at depth d (root: the caller's array)
+__device__ __forceinline__ int node_buf(int d) { return d == 0 ? 0 : 1 + (d & 1); }
+// where a phase-A item (leaf, fused subtree) at depth d leaves its sorted span
+__device__ __forceinline__ int item_buf(int d) { return d == 1 ? 2 : 0; }
+// big natural leaf at depth d: in place in buf[0], or (d == 1) copied to buf[2]
+__device__ __forceinline__ int leaf_mode(bool desc, int d) {
+  return d == 1 ? (desc ? kLeafRevCopy : kLeafCopy) : (desc ? kLeafSwap : kLeafNone);
 }
 __device__ __forceinline__ int64_t leaf_tiles(pos_t len, int mode, int tile) {
   if (mode == kLeafNone) return 0;
@@ -116,7 +126,7 @@ __device__ __forceinline__ int classify_leaf(const ClassifyArgs& A, int64_t i, i
   uint32_t nl = info & 0x7fffffffu;
   if (nl < (uint32_t)A.w && (pos_t)nl < len) return 1;  // extended by insertion sort: fused task
   bool desc = (info >> 31) != 0;
-  int mode = leaf_mode(desc, A.leaf_depth[i] & 1);
+  int mode = leaf_mode(desc, A.leaf_depth[i]);
   *tiles = leaf_tiles(len, mode, A.tile);
   return *tiles > 0 ? 2 : 0;
 }
@@ -451,106 +461,15 @@ struct Exec {
   }
   static constexpr size_t smem_bytes(int w) { return smem_fuse(maxb_for(w)); }
 
-  __device__ static void wait_ready(const ExecArgs& E, uint32_t id) {
-    uint32_t need = E.need[id];
-    if (need == 0) return;
-    unsigned ns = 32;
-    while (ld_acquire_u32(E.done + id) < need) {
-      __nanosleep(ns);
-      if (ns < 1024) ns <<= 1;
-    }
-  }
-
-  // --- big-node merge tile ---
-  __device__ static void merge_task(const ExecArgs& E, uint32_t j, uint32_t k, unsigned char* smem,
-                                    unsigned long long& comps) {
-    __shared__ int64_t s_i[2];
-    K* sk = reinterpret_cast<K*>(smem);
-    T* st = reinterpret_cast<T*>(smem + (size_t)C::TILE * C::kb);
-    pos_t s = E.node_s[j], e = E.node_e[j], m = E.leaf_start[j];
-    int d = E.depth[j];
-    const K* src = reinterpret_cast<const K*>(E.key[(d + 1) & 1]);
-    K* dst = reinterpret_cast<K*>(E.key[d & 1]);
-    const T* tsrc = HAS_TAGS ? reinterpret_cast<const T*>(E.tag[(d + 1) & 1]) : nullptr;
-    T* tdst = HAS_TAGS ? reinterpret_cast<T*>(E.tag[d & 1]) : nullptr;
-    if (threadIdx.x == 0) {
-      wait_ready(E, E.child[2 * j]);
-      wait_ready(E, E.child[2 * j + 1]);
-    }
-    __syncthreads();
-    int64_t tot = e - s, na = m - s, nb = e - m;
-    int64_t o0 = (int64_t)k * C::TILE;
-    int64_t o1 = o0 + C::TILE < tot ? o0 + C::TILE : tot;
-    int len = int(o1 - o0);
-    int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (wid == 0) {
-      int64_t v = o0 == 0 ? 0 : warp_merge_path(src + s, na, src + m, nb, o0);
-      if (lane == 0) s_i[0] = v;
-    } else if (wid == 1) {
-      int64_t v = o1 == tot ? na : warp_merge_path(src + s, na, src + m, nb, o1);
-      if (lane == 0) s_i[1] = v;
-    } else if (wid == 2 && E.classic && k == 0) {
-      // runcore.py:321-324
-      K maxL = ldcg(src + m - 1), maxR = ldcg(src + e - 1);
-      int64_t rl = warp_count_below(src + m, nb, maxL, false);
-      int64_t lr = warp_count_below(src + s, na, maxR, true);
-      int64_t pl = na - 1 + rl, pr = nb - 1 + lr;
-      if (lane == 0) comps += (unsigned long long)((pl < pr ? pl : pr) + 1);
-    }
-    __syncthreads();
-    int64_t i0 = s_i[0], i1 = s_i[1];
-    int la = int(i1 - i0), lb = len - la;
-    int64_t j0 = o0 - i0;
-    for (int x = threadIdx.x; x < len; x += blockDim.x) {
-      pos_t g = x < la ? s + i0 + x : m + j0 + (x - la);
-      sk[x] = ldcg(src + g);
-      if (HAS_TAGS) st[x] = ldcg(tsrc + g);
-    }
-    __syncthreads();
-    K rk[C::IPT];
-    T rt[HAS_TAGS ? C::IPT : 1];
-    int d0 = threadIdx.x * C::IPT;
-    int cnt = 0;
-    if (d0 < len) {
-      cnt = len - d0 < C::IPT ? len - d0 : C::IPT;
-      int ai = smem_merge_path(sk, la, sk + la, lb, d0);
-      int bi = d0 - ai;
-#pragma unroll
-      for (int q = 0; q < C::IPT; ++q) {
-        if (q < cnt) {
-          bool takeA = (bi >= lb) || (ai < la && sk[ai] <= sk[la + bi]);
-          int src_i = takeA ? ai : la + bi;
-          rk[q] = sk[src_i];
-          if (HAS_TAGS) rt[q] = st[src_i];
-          ai += takeA;
-          bi += !takeA;
-        }
-      }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int q = 0; q < C::IPT; ++q) {
-      if (q < cnt) {
-        sk[d0 + q] = rk[q];
-        if (HAS_TAGS) st[d0 + q] = rt[q];
-      }
-    }
-    __syncthreads();
-    for (int x = threadIdx.x; x < len; x += blockDim.x) {
-      dst[s + o0 + x] = sk[x];
-      if (HAS_TAGS) tdst[s + o0 + x] = st[x];
-    }
-  }
-
-  // --- big-leaf tile: reversal / copy into its depth-parity buffer ---
+  // --- big-leaf tile: in-place reversal, or copy / reversed copy to buf[2] ---
   __device__ static void leaf_task(const ExecArgs& E, uint32_t i, uint32_t k) {
     pos_t s0 = E.leaf_start[i], len = E.leaf_start[i + 1] - s0;
     bool desc = (E.leaf_info[i] >> 31) != 0;
-    int mode = leaf_mode(desc, E.leaf_depth[i] & 1);
+    int mode = leaf_mode(desc, E.leaf_depth[i]);
     K* k0 = reinterpret_cast<K*>(E.key[0]);
-    K* k1 = reinterpret_cast<K*>(E.key[1]);
+    K* k1 = reinterpret_cast<K*>(E.key[2]);  // copies go to the depth-1 buffer
     T* t0 = HAS_TAGS ? reinterpret_cast<T*>(E.tag[0]) : nullptr;
-    T* t1 = HAS_TAGS ? reinterpret_cast<T*>(E.tag[1]) : nullptr;
+    T* t1 = HAS_TAGS ? reinterpret_cast<T*>(E.tag[2]) : nullptr;
     constexpr int U = 8;
     if (mode == kLeafSwap) {
       int64_t half = C::TILE / 2;
@@ -899,8 +818,8 @@ struct Exec {
       }
     }
     hook();  // result in X[droot & 1]; the other buffer is free
-    K* gd = reinterpret_cast<K*>(E.key[droot & 1]);
-    T* hd = HAS_TAGS ? reinterpret_cast<T*>(E.tag[droot & 1]) : nullptr;
+    K* gd = reinterpret_cast<K*>(E.key[item_buf(droot)]);  // in place unless depth 1
+    T* hd = HAS_TAGS ? reinterpret_cast<T*>(E.tag[item_buf(droot)]) : nullptr;
     const K* Xr = X[droot & 1];
     const T* Yr = Y[droot & 1];
     for (int x = threadIdx.x; x < len; x += blockDim.x) {

@@ -59,8 +59,8 @@ struct StageHdr {
 __device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"r"(kConsumerThreads) : "memory"); }
 
 struct MergeArgs {
-  void* key[2];
-  void* tag[2];
+  void* key[3];
+  void* tag[3];
   int classic;
   int msuper;  // merge tiles per task (ClassifyArgs::msuper)
   const pos_t* leaf_start;
@@ -72,6 +72,8 @@ struct MergeArgs {
   uint32_t* done;
   const uint64_t* tasks;
   DevMetrics* met;
+  const uint8_t* cls;  // unified id -> class (2 = merge node for internal ids)
+  uint32_t leaf_base;
 };
 
 // Lane-group merge-path search: lanes [g*G, g*G+G) cooperate on diagonal `diag`
@@ -153,6 +155,7 @@ __device__ __forceinline__ int64_t group_merge_path(const K* A, int64_t na, cons
 struct PTask {
   unsigned long long t;
   uint32_t j, sk, c0, c1, nd0, nd1, dn0, dn1;
+  uint8_t cl0, cl1;  // class of internal children (2 = merge node), 0 for leaves
   pos_t s, e, m;
   int d;
   int st;  // stages done: 1 claimed, 2 record, 3 node, 4 need, 5 counters (speculative)
@@ -183,6 +186,8 @@ struct PTask {
       if (valid) {
         nd0 = E.need[c0];
         nd1 = E.need[c1];
+        cl0 = c0 < E.leaf_base ? E.cls[c0] : 0;
+        cl1 = c1 < E.leaf_base ? E.cls[c1] : 0;
       }
     } else if (st == 4) {
       // early acquire of the children's counters (overlapping the search's
@@ -294,8 +299,13 @@ __global__ void __launch_bounds__(kMergeThreads, 3) k_merge_exec(MergeArgs E) {
       }
       __syncwarp();
       RS_T0(tsrch);
-      const K* src = reinterpret_cast<const K*>(((d + 1) & 1) ? E.key[1] : E.key[0]);
-      const T* tsrc = HT ? reinterpret_cast<const T*>(((d + 1) & 1) ? E.tag[1] : E.tag[0]) : nullptr;
+      // children: merge nodes in buf[node_buf(d + 1)], phase-A items in buf[item_buf(d + 1)]
+      const int ba = cur.cl0 == 2 ? node_buf(d + 1) : item_buf(d + 1);
+      const int bb = cur.cl1 == 2 ? node_buf(d + 1) : item_buf(d + 1);
+      const K* srcA = reinterpret_cast<const K*>(E.key[ba]);
+      const K* srcB = reinterpret_cast<const K*>(E.key[bb]);
+      const T* tsrcA = HT ? reinterpret_cast<const T*>(E.tag[ba]) : nullptr;
+      const T* tsrcB = HT ? reinterpret_cast<const T*>(E.tag[bb]) : nullptr;
       int64_t tot = e - s, na = m - s, nb = e - m;
       int64_t ntile = (tot + C::TILE - 1) / C::TILE;
       int64_t kbeg = (int64_t)sk * kSuper;
@@ -305,7 +315,7 @@ __global__ void __launch_bounds__(kMergeThreads, 3) k_merge_exec(MergeArgs E) {
       if (diag > tot) diag = tot;
       bool in_range = g <= (kend - kbeg) && g < kSuper + 1 && lane < G * (kSuper + 1);
       bool trivial = diag == 0 || diag == tot;
-      int64_t split = group_merge_path(src + s, na, src + m, nb, diag, in_range && !trivial, G,
+      int64_t split = group_merge_path(srcA + s, na, srcB + m, nb, diag, in_range && !trivial, G,
                                        [&]() { nxt.advance(E, ntasks); });
       nxt.finish(E, ntasks);
       if (diag == 0) split = 0;
@@ -314,9 +324,9 @@ __global__ void __launch_bounds__(kMergeThreads, 3) k_merge_exec(MergeArgs E) {
       RS_T0(tiss);
       if (E.classic && kbeg == 0) {
         // runcore.py:321-324
-        K maxL = ldcg(src + m - 1), maxR = ldcg(src + e - 1);
-        int64_t rl = warp_count(src + m, nb, maxL, false);
-        int64_t lr = warp_count(src + s, na, maxR, true);
+        K maxL = ldcg(srcA + m - 1), maxR = ldcg(srcB + e - 1);
+        int64_t rl = warp_count(srcB + m, nb, maxL, false);
+        int64_t lr = warp_count(srcA + s, na, maxR, true);
         int64_t pl = na - 1 + rl, pr = nb - 1 + lr;
         if (lane == 0) comps += (unsigned long long)((pl < pr ? pl : pr) + 1);
       }
@@ -337,35 +347,35 @@ __global__ void __launch_bounds__(kMergeThreads, 3) k_merge_exec(MergeArgs E) {
           h.len = int32_t(o1 - o0);
           h.la = int32_t(i1 - i0);
           h.node = j;
-          h.parity = d & 1;
+          h.parity = node_buf(d);  // destination buffer index
           h.end = 0;
           // expected bytes first (tx count may complete before arrive otherwise)
-          uintptr_t ka0 = reinterpret_cast<uintptr_t>(src + s + i0), ka1 = reinterpret_cast<uintptr_t>(src + s + i1);
-          uintptr_t kb0 = reinterpret_cast<uintptr_t>(src + m + j0), kb1 = reinterpret_cast<uintptr_t>(src + m + j1);
+          uintptr_t ka0 = reinterpret_cast<uintptr_t>(srcA + s + i0), ka1 = reinterpret_cast<uintptr_t>(srcA + s + i1);
+          uintptr_t kb0 = reinterpret_cast<uintptr_t>(srcB + m + j0), kb1 = reinterpret_cast<uintptr_t>(srcB + m + j1);
           uint32_t bA = i1 > i0 ? (uint32_t)(((ka1 + 15) & ~(uintptr_t)15) - (ka0 & ~(uintptr_t)15)) : 0u;
           uint32_t bB = j1 > j0 ? (uint32_t)(((kb1 + 15) & ~(uintptr_t)15) - (kb0 & ~(uintptr_t)15)) : 0u;
           uint32_t tx = bA + bB;
           uint32_t tA = 0, tBb = 0;
           if (HT) {
-            uintptr_t ta0 = reinterpret_cast<uintptr_t>(tsrc + s + i0), ta1 = reinterpret_cast<uintptr_t>(tsrc + s + i1);
-            uintptr_t tb0 = reinterpret_cast<uintptr_t>(tsrc + m + j0), tb1 = reinterpret_cast<uintptr_t>(tsrc + m + j1);
+            uintptr_t ta0 = reinterpret_cast<uintptr_t>(tsrcA + s + i0), ta1 = reinterpret_cast<uintptr_t>(tsrcA + s + i1);
+            uintptr_t tb0 = reinterpret_cast<uintptr_t>(tsrcB + m + j0), tb1 = reinterpret_cast<uintptr_t>(tsrcB + m + j1);
             tA = i1 > i0 ? (uint32_t)(((ta1 + 15) & ~(uintptr_t)15) - (ta0 & ~(uintptr_t)15)) : 0u;
             tBb = j1 > j0 ? (uint32_t)(((tb1 + 15) & ~(uintptr_t)15) - (tb0 & ~(uintptr_t)15)) : 0u;
             tx += tA + tBb;
           }
           mbar_arrive_tx(&full_bar[stage], tx);
           int32_t offA, offB;
-          uint32_t gotA = tma_window(sk_base, src, s + i0, s + i1, sizeof(K), &full_bar[stage], &offA);
+          uint32_t gotA = tma_window(sk_base, srcA, s + i0, s + i1, sizeof(K), &full_bar[stage], &offA);
           uint32_t bstart = (gotA + 15) & ~15u;
-          tma_window(sk_base + bstart, src, m + j0, m + j1, sizeof(K), &full_bar[stage], &offB);
+          tma_window(sk_base + bstart, srcB, m + j0, m + j1, sizeof(K), &full_bar[stage], &offB);
           h.offA = offA;
           h.offB = offB + int32_t(bstart / sizeof(K));
           if (HT) {
             unsigned char* tg = sk_base + C::KBYTES;
             int32_t toA, toB;
-            uint32_t gtA = tma_window(tg, tsrc, s + i0, s + i1, TB, &full_bar[stage], &toA);
+            uint32_t gtA = tma_window(tg, tsrcA, s + i0, s + i1, TB, &full_bar[stage], &toA);
             uint32_t tbs = (gtA + 15) & ~15u;
-            tma_window(tg + tbs, tsrc, m + j0, m + j1, TB, &full_bar[stage], &toB);
+            tma_window(tg + tbs, tsrcB, m + j0, m + j1, TB, &full_bar[stage], &toB);
             h.toffA = toA;
             h.toffB = toB + int32_t(tbs / (TB ? TB : 1));
           }
@@ -481,9 +491,9 @@ __global__ void __launch_bounds__(kMergeThreads, 3) k_merge_exec(MergeArgs E) {
       }
     }
     // write back with the global 16B phase so the store loop can use 16B vectors
-    K* gdst = reinterpret_cast<K*>(h.parity ? E.key[1] : E.key[0]) + h.dst;
+    K* gdst = reinterpret_cast<K*>(E.key[h.parity]) + h.dst;
     int pad = int((reinterpret_cast<uintptr_t>(gdst) & 15) / sizeof(K));
-    T* tdst = HT ? reinterpret_cast<T*>(h.parity ? E.tag[1] : E.tag[0]) + h.dst : nullptr;
+    T* tdst = HT ? reinterpret_cast<T*>(E.tag[h.parity]) + h.dst : nullptr;
     int tpad = HT ? int((reinterpret_cast<uintptr_t>(tdst) & 15) / (HT ? TB : 1)) : 0;
     consumer_sync();
 #pragma unroll

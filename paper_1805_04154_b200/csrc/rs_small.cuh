@@ -233,7 +233,7 @@ __device__ void small_tree(const TreeArrays& T, const ClassifyArgs& A, int F, un
     if (!(len <= A.fcap && parent_small_s(par[i]))) {
       if (nl < (uint32_t)A.w && (pos_t)nl < len) c = 1;
       else {
-        int mode = leaf_mode((info >> 31) != 0, ldep[i] & 1);
+        int mode = leaf_mode((info >> 31) != 0, ldep[i]);
         tl = leaf_tiles(len, mode, A.tile);
         c = tl > 0 ? 2 : 0;
       }

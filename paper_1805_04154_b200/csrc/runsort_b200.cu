@@ -79,7 +79,7 @@ struct Layout {
   int64_t words, ntiles, ngroups, r_max, nchunks, max_tasks;
   uint32_t leaf_base;
   // offsets
-  size_t o_key1, o_tag1, o_ascw, o_tables, o_gtab, o_gentry, o_goff, o_tentry, o_toff;
+  size_t o_key1, o_tag1, o_key2, o_tag2, o_ascw, o_tables, o_gtab, o_gentry, o_goff, o_tentry, o_toff;
   size_t o_leaf_start, o_leaf_info, o_leaf_depth, o_K, o_P, o_la, o_ra, o_depth;
   size_t o_node_a, o_node_b, o_node_s, o_node_e, o_parent, o_child, o_need, o_done;
   size_t o_agg, o_tasks, o_chunkdep, o_cls, o_met, total;
@@ -107,6 +107,7 @@ Layout make_layout(int64_t n, int w, int kb, int tb, int algo) {
   L.tb = tb;
   L.tile = exec_tile(kb, tb);
   L.fcap = exec_fcap(kb, tb);
+  if (const char* ov = getenv("RS_FCAP")) L.fcap = std::max(2, std::min(L.fcap, atoi(ov)));  // tuning override
   L.words = (n + 31) / 32 + 2;
   L.ntiles = (n + kChainT - 1) / kChainT;
   L.ngroups = (L.ntiles + kChainGroup - 1) / kChainGroup;
@@ -126,6 +127,8 @@ Layout make_layout(int64_t n, int w, int kb, int tb, int algo) {
   };
   L.o_key1 = take((size_t)n * kb + 64);
   L.o_tag1 = take((size_t)n * tb + 64);
+  L.o_key2 = take((size_t)n * kb + 64);
+  L.o_tag2 = take((size_t)n * tb + 64);
   L.o_ascw = take((size_t)L.words * 4);
   bool pk = algo == RS_ALGO_PEEKSORT;
   L.o_tables = take(pk ? 0 : (size_t)L.ntiles * (w + 1) * 8);
@@ -267,6 +270,8 @@ struct WsView {
   MC* agg;
   void* key1;
   void* tag1;
+  void* key2;
+  void* tag2;
 };
 
 WsView view(unsigned char* ws, const Layout& L) {
@@ -302,6 +307,8 @@ WsView view(unsigned char* ws, const Layout& L) {
   V.cls = reinterpret_cast<uint8_t*>(at(L.o_cls));
   V.key1 = at(L.o_key1);
   V.tag1 = at(L.o_tag1);
+  V.key2 = at(L.o_key2);
+  V.tag2 = at(L.o_tag2);
   return V;
 }
 
@@ -327,6 +334,8 @@ int launch_exec(K* keys, void* tags, int64_t n, int w, int classic, int msuper, 
   ExecArgs E;
   E.key[0] = keys;
   E.key[1] = V.key1;
+  E.key[2] = V.key2;
+  E.tag[2] = V.tag2;
   E.tag[0] = tags;
   E.tag[1] = V.tag1;
   E.n = n;
@@ -355,6 +364,10 @@ int launch_exec(K* keys, void* tags, int64_t n, int w, int classic, int msuper, 
   M.key[1] = E.key[1];
   M.tag[0] = E.tag[0];
   M.tag[1] = E.tag[1];
+  M.key[2] = E.key[2];
+  M.tag[2] = E.tag[2];
+  M.cls = V.cls;
+  M.leaf_base = L.leaf_base;
   M.classic = classic;
   M.msuper = msuper;
   M.leaf_start = V.leaf_start;
