@@ -104,13 +104,24 @@ struct ClassifyArgs {
   DevMetrics* met;
   const int32_t* node_a;
   const int32_t* node_b;
-  int maxb;  // ExecArgs::maxb
+  int maxb;      // ExecArgs::maxb
+  int fuse_avg;  // fused subtrees: average leaf length below this
 };
 
-// Node j can run as (part of) one fused phase-A task: its span fits FCAP and
-// its internal nodes fit the task's node table.
+// Node j can run as (part of) one fused phase-A task: its span fits the fused
+// capacity and its internal nodes fit the task's node table (both monotone, so
+// "parent fusable" decides membership).
+__device__ __forceinline__ bool fusable_span(const ClassifyArgs& A, pos_t span, int64_t nodes) {
+  return span <= A.fcap && nodes <= A.maxb - 2;
+}
+// Fused subtrees pay for short leaves (insertion sorts, several merge levels in
+// SMEM); runs averaging >= fuse_avg elements merge faster in the pipelined
+// executor, so then only insertion-sort leaves are phase-A tasks (fcap -> 0).
+__device__ __forceinline__ void set_fuse_policy(ClassifyArgs& A, int64_t r) {
+  if (A.n >= (pos_t)A.fuse_avg * r) A.fcap = 0;
+}
 __device__ __forceinline__ bool fusable(const ClassifyArgs& A, int32_t j) {
-  return (A.node_e[j] - A.node_s[j]) <= A.fcap && (A.node_b[j] - A.node_a[j]) <= A.maxb - 2;
+  return fusable_span(A, A.node_e[j] - A.node_s[j], A.node_b[j] - A.node_a[j]);
 }
 __device__ __forceinline__ bool parent_small(const ClassifyArgs& A, int32_t par) {
   return par >= 0 && fusable(A, par);
@@ -158,6 +169,7 @@ __device__ void d_classify(ClassifyArgs A, uint32_t* __restrict__ chunk_depth) {
   __shared__ unsigned long long sred[32];
   __shared__ uint32_t s_cd[kMaxDepth];  // this iteration's per-depth task counts (one chunk)
   int64_t r = (int64_t)A.met->n_leaves;
+  set_fuse_policy(A, r);
   const int64_t ochunk = ord_chunk(r);  // a multiple of blockDim: one chunk per block iteration
   unsigned long long comps = 0, mcost = 0, cntA = 0, mbig = 0;
   unsigned long long dtl = 0;  // thread d < kMaxDepth: tasks of depth d over all iterations

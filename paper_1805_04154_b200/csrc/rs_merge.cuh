@@ -397,19 +397,56 @@ __global__ void __launch_bounds__(kMergeThreads, 3) k_merge_exec(MergeArgs E) {
 
   if (warp == 1) {
     // ------------------------------------------------------------ signaller
-    // Publishes finished tiles (release fence + counter add) off the consumers'
-    // critical path, then hands the stage back to the producer.
+    // Streams each merged tile from its stage to HBM (bulk store of the 16B-
+    // aligned middle, lanes store the unaligned head / tail), hands the stage
+    // back once the copy engine has read it, and publishes the tile (counter
+    // add) after the writes are complete and fenced -- the consumers never
+    // wait on global stores.
+    constexpr int VK = 16 / sizeof(K);
+    constexpr int VT = HT ? 16 / (HT ? TB : 1) : 1;
     int stage = 0;
     uint32_t phase = 0;
     for (;;) {
       mbar_wait(&stored_bar[stage], phase);
-      int end = hdr[stage].end;
-      uint32_t node = hdr[stage].node;
-      if (end) break;
-      if (lane == 0) {
-        release_add_u32(E.done + node, 1u);
-        mbar_arrive(&empty_bar[stage]);
+      const StageHdr h = hdr[stage];
+      if (h.end) break;
+      unsigned char* base = smem + (size_t)stage * C::STAGE;
+      K* sk = reinterpret_cast<K*>(base);
+      T* st = reinterpret_cast<T*>(base + C::KBYTES);
+      const int len = h.len;
+      K* gdst = reinterpret_cast<K*>(E.key[h.parity]) + h.dst;
+      const int pad = int((reinterpret_cast<uintptr_t>(gdst) & 15) / sizeof(K));
+      int h0 = (VK - pad) % VK;
+      if (h0 > len) h0 = len;
+      const int nvec = (len - h0) / VK;
+      const int tail0 = h0 + nvec * VK;
+      if (lane < h0) gdst[lane] = sk[pad + lane];
+      if (lane < len - tail0) gdst[tail0 + lane] = sk[pad + tail0 + lane];
+      T* tdst = nullptr;
+      int th0 = 0, tnvec = 0, ttail0 = 0, tpad = 0;
+      if (HT) {
+        tdst = reinterpret_cast<T*>(E.tag[h.parity]) + h.dst;
+        tpad = int((reinterpret_cast<uintptr_t>(tdst) & 15) / (HT ? TB : 1));
+        th0 = (VT - tpad) % VT;
+        if (th0 > len) th0 = len;
+        tnvec = (len - th0) / VT;
+        ttail0 = th0 + tnvec * VT;
+        if (lane < th0) tdst[lane] = st[tpad + lane];
+        if (lane < len - ttail0) tdst[ttail0 + lane] = st[tpad + ttail0 + lane];
       }
+      __syncwarp();
+      if (lane == 0) {
+        if (nvec > 0) tma_store_1d(gdst + h0, sk + pad + h0, (uint32_t)nvec * 16u);
+        if (HT && tnvec > 0) tma_store_1d(tdst + th0, st + tpad + th0, (uint32_t)tnvec * 16u);
+        bulk_commit();
+        bulk_wait_read0();
+        mbar_arrive(&empty_bar[stage]);  // the stage may be refilled
+        bulk_wait0();                    // the tile's bulk writes are performed
+        fence_proxy_async_global();      // async-proxy writes -> generic / other proxies
+      }
+      __syncwarp();
+      __threadfence();  // this warp's head / tail stores and the bulk writes, GPU-wide
+      if (lane == 0) asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(E.done + h.node) : "memory");
       __syncwarp();
       if (++stage == kStages) { stage = 0; phase ^= 1; }
     }
@@ -419,8 +456,6 @@ __global__ void __launch_bounds__(kMergeThreads, 3) k_merge_exec(MergeArgs E) {
   // --------------------------------------------------------------- consumers
   int ct = threadIdx.x - 64;
   int cl = ct & 31;
-  constexpr int VK = 16 / sizeof(K);
-  constexpr int VT = HT ? 16 / (HT ? TB : 1) : 1;
   int stage = 0;
   uint32_t phase = 0;
   for (;;) {
@@ -490,12 +525,14 @@ __global__ void __launch_bounds__(kMergeThreads, 3) k_merge_exec(MergeArgs E) {
         }
       }
     }
-    // write back with the global 16B phase so the store loop can use 16B vectors
-    K* gdst = reinterpret_cast<K*>(E.key[h.parity]) + h.dst;
-    int pad = int((reinterpret_cast<uintptr_t>(gdst) & 15) / sizeof(K));
-    T* tdst = HT ? reinterpret_cast<T*>(E.tag[h.parity]) + h.dst : nullptr;
-    int tpad = HT ? int((reinterpret_cast<uintptr_t>(tdst) & 15) / (HT ? TB : 1)) : 0;
-    consumer_sync();
+    // stage the merged tile in SMEM with the destination's 16B phase; the
+    // signaller streams it out with bulk stores and publishes it
+    const int pad = int((reinterpret_cast<uintptr_t>(reinterpret_cast<K*>(E.key[h.parity]) + h.dst) & 15) /
+                        sizeof(K));
+    const int tpad = HT ? int((reinterpret_cast<uintptr_t>(reinterpret_cast<T*>(E.tag[h.parity]) + h.dst) & 15) /
+                              (HT ? TB : 1))
+                        : 0;
+    consumer_sync();  // every thread's merge has read the stage's inputs
 #pragma unroll
     for (int q = 0; q < C::IPT; ++q) {
       if (q < cnt) {
@@ -503,30 +540,7 @@ __global__ void __launch_bounds__(kMergeThreads, 3) k_merge_exec(MergeArgs E) {
         if (HT) st[tpad + d0 + q] = rt[q];
       }
     }
-    consumer_sync();
-    {
-      int h0 = (VK - pad) % VK;
-      if (h0 > len) h0 = len;
-      int nvec = (len - h0) / VK;
-      int tail0 = h0 + nvec * VK;
-      if (ct < h0) gdst[ct] = sk[pad + ct];
-      const uint4* sv = reinterpret_cast<const uint4*>(sk + pad + h0);
-      uint4* gv = reinterpret_cast<uint4*>(gdst + h0);
-      for (int v = ct; v < nvec; v += kConsumerThreads) gv[v] = sv[v];
-      if (ct < len - tail0) gdst[tail0 + ct] = sk[pad + tail0 + ct];
-    }
-    if (HT) {
-      int h0 = (VT - tpad) % VT;
-      if (h0 > len) h0 = len;
-      int nvec = (len - h0) / VT;
-      int tail0 = h0 + nvec * VT;
-      if (ct < h0) tdst[ct] = st[tpad + ct];
-      const uint4* sv = reinterpret_cast<const uint4*>(st + tpad + h0);
-      uint4* gv = reinterpret_cast<uint4*>(tdst + h0);
-      for (int v = ct; v < nvec; v += kConsumerThreads) gv[v] = sv[v];
-      if (ct < len - tail0) tdst[tail0 + ct] = st[tpad + tail0 + ct];
-    }
-    // each warp: order its lanes' stores (syncwarp), then one arrival per warp
+    // generic SMEM writes -> visible to the bulk copy engine, then one arrival per warp
     fence_proxy_async_smem();
     __syncwarp();
     if (cl == 0) mbar_arrive(&stored_bar[stage]);

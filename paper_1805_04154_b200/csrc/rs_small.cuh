@@ -27,11 +27,12 @@ __host__ __device__ constexpr size_t small_smem_bytes() {
 // Run by one CTA of NT threads (block 0 of k_prep after its leaf phase);
 // smem_small: small_smem_bytes() of dynamic shared memory.
 template <int NT>
-__device__ void small_tree(const TreeArrays& T, const ClassifyArgs& A, int F, unsigned char* smem_small) {
+__device__ void small_tree(const TreeArrays& T, ClassifyArgs A, int F, unsigned char* smem_small) {
   constexpr int kSmallPer = (kSmallR + NT - 1) / NT;  // items per thread
   DevMetrics* met = A.met;
   const int64_t r = (int64_t)met->n_leaves;
   if (r > kSmallR || r < 1) return;
+  set_fuse_policy(A, r);
   RS_TS(met, 5);
   pos_t* Ls = reinterpret_cast<pos_t*>(smem_small);
   uint64_t* Ks = reinterpret_cast<uint64_t*>(Ls + kSmallR + 1);
@@ -173,8 +174,8 @@ __device__ void small_tree(const TreeArrays& T, const ClassifyArgs& A, int F, un
       pos_t s0 = Ls[a], e0 = Ls[b + 1];
       T.node_s[j] = s0;
       T.node_e[j] = e0;
-      // bit 62: not fusable (too many internal nodes for the phase-A node table)
-      myspan[q] = (e0 - s0) | ((b - a > A.maxb - 2) ? ((pos_t)1 << 62) : (pos_t)0);
+      // bit 62: not fusable (fusable_span: node table, average leaf length)
+      myspan[q] = (e0 - s0) | (fusable_span(A, e0 - s0, b - a) ? (pos_t)0 : ((pos_t)1 << 62));
       uint8_t dd = (uint8_t)(las[j] + ras[j]);
       T.depth[j] = dd;
       dep[j] = dd;

@@ -317,11 +317,19 @@ TreeArrays tree_arrays(const WsView& V, const Layout& L) {
                     V.node_b, V.parent, V.child, V.node_s, V.node_e, L.leaf_base};
 }
 
+// Fused phase-A subtrees only for short leaves on average (measured on B200:
+// cfg1's 24-element leaves gain 2x from fusing, cfg2/cfg4's ~1-3K-element runs
+// merge faster in the executor).
+int fuse_avg() {
+  if (const char* ov = getenv("RS_FUSE_AVG")) return atoi(ov);  // tuning override
+  return 256;
+}
+
 template <typename K, int TB>
 ClassifyArgs classify_args(const WsView& V, const Layout& L, int64_t n, int w, int classic, int msuper, int peek) {
   return ClassifyArgs{n, w, classic, L.fcap, L.tile, MergeCfg<K, TB>::TILE, msuper, peek, L.leaf_base,
                       V.leaf_start, V.leaf_info, V.leaf_depth, V.depth, V.node_s, V.node_e, V.parent, V.need,
-                      V.cls, V.tasks, V.met, V.node_a, V.node_b, Exec<K, TB>::maxb_for(w)};
+                      V.cls, V.tasks, V.met, V.node_a, V.node_b, Exec<K, TB>::maxb_for(w), fuse_avg()};
 }
 
 // Phase A (fused subtrees, large leaves) + the merge executor.
