@@ -164,7 +164,7 @@ __host__ __device__ inline int chain_warp_bytes(int w, int kb) {
 
 template <typename K>
 __device__ void d_scan_tables_tma(const K* __restrict__ a, pos_t n, int w, uint32_t* __restrict__ ascw,
-                                  uint2* __restrict__ tables, int64_t ntiles) {
+                                  uint2* __restrict__ tables, int64_t ntiles, DevMetrics* imet = nullptr) {
   extern __shared__ __align__(128) unsigned char smem_tab[];
   __shared__ __align__(8) uint64_t kbar[32];
   int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -179,7 +179,13 @@ __device__ void d_scan_tables_tma(const K* __restrict__ a, pos_t n, int w, uint3
   }
   __syncwarp();
   uint32_t ph = 0;
+#ifdef RS_INSTR
+  unsigned long long c_wait = 0, c_bits = 0, c_bw = 0, c_walk = 0;
+#endif
   for (int64_t tile = (int64_t)blockIdx.x * nw + wid; tile < ntiles; tile += (int64_t)gridDim.x * nw) {
+#ifdef RS_INSTR
+    unsigned long long c0 = clock64();
+#endif
     pos_t t0, t1;
     int64_t q0, q1;
     chain_window(tile, n, w, &q0, &q1, &t0, &t1);
@@ -196,12 +202,18 @@ __device__ void d_scan_tables_tma(const K* __restrict__ a, pos_t n, int w, uint3
     koff = __shfl_sync(0xffffffffu, koff, 0);
     mbar_wait(&kbar[wid], ph);
     ph ^= 1u;
+#ifdef RS_INSTR
+    unsigned long long c1 = clock64();
+    c_wait += c1 - c0;
+#endif
     const K* sk = reinterpret_cast<const K*>(kbuf) + koff;  // element 32*q0
     int64_t own0 = t0 >> 5, own1 = (t1 + 31) >> 5;
     constexpr int VEC = 16 / sizeof(K);  // elements per 16B lane load = words per warp load
     constexpr int LPW = 32 / VEC;        // lanes per word
     if (koff % VEC == 0) {
-      // vector path: one LDS.128 per lane covers VEC words per warp step
+      // vector path: one LDS.128 per lane covers VEC words per warp step;
+      // steps are independent, unrolled so their shuffle chains overlap
+#pragma unroll 4
       for (int vb = 0; vb < nwords; vb += VEC) {
         const uint4 raw = reinterpret_cast<const uint4*>(sk + 32 * vb)[lane];
         const K* x = reinterpret_cast<const K*>(&raw);
@@ -240,8 +252,16 @@ __device__ void d_scan_tables_tma(const K* __restrict__ a, pos_t n, int w, uint3
       }
     }
     __syncwarp();
+#ifdef RS_INSTR
+    unsigned long long c2 = clock64();
+    c_bits += c2 - c1;
+#endif
     pos_t base = 32 * q0;
     build_bwords_warp(asc, 0u, bw, nz, nwords, base, n, t0 > 0);
+#ifdef RS_INSTR
+    unsigned long long c3 = clock64();
+    c_bw += c3 - c2;
+#endif
     for (int c = lane; c <= w; c += 32) {
       pos_t p;
       if (c < w) p = t0 + c;
@@ -263,7 +283,18 @@ __device__ void d_scan_tables_tma(const K* __restrict__ a, pos_t n, int w, uint3
       tables[tile * (w + 1) + c] = make_uint2(ex, cnt);
     }
     __syncwarp();
+#ifdef RS_INSTR
+    c_walk += clock64() - c3;
+#endif
   }
+#ifdef RS_INSTR
+  if (lane == 0 && imet) {  // max over warps of the per-part cycle sums
+    atomicMax(&imet->prep_ts[12], c_wait);
+    atomicMax(&imet->prep_ts[13], c_bits);
+    atomicMax(&imet->prep_ts[14], c_bw);
+    atomicMax(&imet->prep_ts[15], c_walk);
+  }
+#endif
 }
 
 // K2b: compose the tables of each group of kChainGroup tiles.

@@ -270,9 +270,6 @@ __device__ void d_task_fill(ClassifyArgs A, const uint32_t* __restrict__ chunk_d
   uint32_t* s_tk = s_slot + kOrdChunkMax;
   uint8_t* s_dep = smem_fill + kOrdChunkMax * 8;
   int64_t r = (int64_t)A.met->n_leaves;
-#ifdef RS_INSTR
-  unsigned long long tf0 = globaltimer_ns();
-#endif
   // phase-A tasks (any order): element-parallel, slots from one atomic per block
   __shared__ uint32_t s_sc[40];
   __shared__ unsigned long long s_base;
@@ -298,10 +295,6 @@ __device__ void d_task_fill(ClassifyArgs A, const uint32_t* __restrict__ chunk_d
     if (cn == 1) A.tasks[slot++] = make_task(kTaskFuse, 0, (uint32_t)i);
     __syncthreads();
   }
-#ifdef RS_INSTR
-  unsigned long long tf1 = globaltimer_ns();
-  if (threadIdx.x == 0) atomicMax(&A.met->prep_ts[12], tf1 - tf0);
-#endif
   // merge tasks: slots by (depth, position); chunk boundaries staged in smem,
   // warp 0 assigns ordered slots, all threads write.
   const int64_t oc = ord_chunk(r);
@@ -328,10 +321,6 @@ __device__ void d_task_fill(ClassifyArgs A, const uint32_t* __restrict__ chunk_d
       s_tk[x] = tv;
     }
     __syncthreads();
-#ifdef RS_INSTR
-    unsigned long long tq0 = globaltimer_ns();
-    if (threadIdx.x == 0) atomicMax(&A.met->prep_ts[14], tq0 - tf1);
-#endif
     // ordered slots, 256 nodes per round: every warp ranks its 32 nodes among
     // same-depth peers (shuffle prefix), per-depth warp totals are scanned
     // across warps, and `run` carries each depth's cursor to the next round
@@ -365,9 +354,6 @@ __device__ void d_task_fill(ClassifyArgs A, const uint32_t* __restrict__ chunk_d
       if (d != 255) s_slot[x] = s_wsum[d * 8 + wid] + pre;
       __syncthreads();
     }
-#ifdef RS_INSTR
-    if (threadIdx.x == 0) atomicMax(&A.met->prep_ts[15], globaltimer_ns() - tq0);
-#endif
     // one warp per big node writes its task records
     int wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     for (int64_t x = wid; x < cnt_i; x += nw) {
@@ -378,9 +364,6 @@ __device__ void d_task_fill(ClassifyArgs A, const uint32_t* __restrict__ chunk_d
       for (uint32_t k = lane; k < tk; k += 32) A.tasks[slot + k] = make_task(kTaskMerge, k, (uint32_t)i);
     }
   }
-#ifdef RS_INSTR
-  if (threadIdx.x == 0) atomicMax(&A.met->prep_ts[13], globaltimer_ns() - tf1);
-#endif
 }
 
 // ---------------------------------------------------------------- searches

@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(256, 3) k_prep(PrepArgs P) {
   }
   // 1. pair-type bits + candidate tables (sorters.py:462-470, runcore.py:137-159)
   const K* a = reinterpret_cast<const K*>(P.keys);
-  d_scan_tables_tma<K>(a, P.n, P.w, P.ascw, P.tables, P.ntiles);
+  d_scan_tables_tma<K>(a, P.n, P.w, P.ascw, P.tables, P.ntiles, met);
   grid.sync();
   RS_TS(met, 1);
 #ifdef RS_INSTR

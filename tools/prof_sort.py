@@ -34,7 +34,7 @@ if __import__('os').environ.get('RS_LIB'):
     buf = (ctypes.c_uint64 * 154)()
     k = L.rs_debug_counters(kc, tb, n, a.w, ws.data_ptr(), buf, 154)
     ts = list(buf[138:154]); print('prep phase us', [round((ts[i] - ts[i-1]) / 1e3, 1) for i in range(1, 12) if ts[i] and ts[i-1]])
-    print('max-over-blocks section ns', ts[12:16])
+    print('phase-1 max-warp cycles wait/bits/bwords/walk', ts[12:16])
     dw = list(buf[10:74]); dt = list(buf[74:138])
     print('depth: wait_cycles(M) tasks', [(d, round(dw[d] / 1e6, 1), dt[d]) for d in range(64) if dt[d]])
     names = ['prod_dep_wait', 'prod_search', 'prod_stage_wait', 'cons_full_wait', 'cons_tile_work', 'prod_ready', 'prod_pfence', 'prod_issue', 'n_tasks', 'phaseA']
