@@ -65,6 +65,21 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
   return t;
 }
 
+// Debug builds (-DRS_DEBUG_CHECKS): device invariant checks that print and trap.
+#ifdef RS_DEBUG_CHECKS
+#define RS_CHECK(cond, ...)                                                   \
+  do {                                                                        \
+    if (!(cond)) {                                                            \
+      printf("RS_CHECK %s:%d %s | ", __FILE__, __LINE__, #cond);              \
+      printf(__VA_ARGS__);                                                    \
+      printf("\n");                                                          \
+      __trap();                                                               \
+    }                                                                         \
+  } while (0)
+#else
+#define RS_CHECK(cond, ...) do { } while (0)
+#endif
+
 #ifdef RS_INSTR
 #define RS_TS(met, i) do { if (blockIdx.x == 0 && threadIdx.x == 0) (met)->prep_ts[i] = globaltimer_ns(); } while (0)
 #define RS_T0(v) long long v = clock64()
@@ -270,6 +285,8 @@ __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.comm
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 // all committed bulk stores are complete (writes performed)
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+// all but the most recent committed group are complete
+__device__ __forceinline__ void bulk_wait1() { asm volatile("cp.async.bulk.wait_group 1;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");

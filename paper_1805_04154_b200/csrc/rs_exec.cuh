@@ -591,6 +591,8 @@ struct Exec {
     const pos_t s = f.s, e = f.e;
     const int droot = f.droot;
     int len = int(e - s);
+    RS_CHECK(0 < len && len <= C::FCAP && lb >= la && lb - la <= E.maxb - 2, "fuse task s %lld e %lld la %lld lb %lld",
+             (long long)s, (long long)e, (long long)la, (long long)lb);
     // the subtree's node table while the span is in flight
     int nbd = int(lb - la);
     int dmax_local = droot;

@@ -54,6 +54,11 @@ struct StageHdr {
   int32_t parity;  // destination buffer
   int32_t end;
   int32_t pad;
+#ifdef RS_DEBUG_CHECKS
+  const void* dbg_srcB;  // global address of the B window's first element
+  uint32_t dbg_cB;       // right child id
+  uint32_t dbg_dnB;      // its counter when the producer found it ready
+#endif
 };
 
 __device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"r"(kConsumerThreads) : "memory"); }
@@ -80,6 +85,8 @@ struct MergeArgs {
 // of group g.  Returns the split (number of A elements) in every lane.  `side`
 // runs once per round trip, between issuing the step's loads and consuming
 // them, so another dependent load chain can overlap the search's latency.
+template <typename K>
+__device__ __forceinline__ K ld_volatile_k(const K* p) { return *reinterpret_cast<const volatile K*>(p); }
 struct NoSide {
   __device__ __forceinline__ void operator()() const {}
 };
@@ -341,6 +348,12 @@ __global__ void __launch_bounds__(kMergeThreads, 3) k_merge_exec(MergeArgs E) {
           int64_t o0 = k * (int64_t)C::TILE;
           int64_t o1 = o0 + C::TILE < tot ? o0 + C::TILE : tot;
           int64_t j0 = o0 - i0, j1 = o1 - i1;
+          RS_CHECK(0 <= i0 && i0 <= i1 && i1 <= na && 0 <= j0 && j0 <= j1 && j1 <= nb && o1 - o0 <= C::TILE,
+                   "node %u k %lld s %lld m %lld e %lld i0 %lld i1 %lld j0 %lld j1 %lld", j, (long long)k,
+                   (long long)s, (long long)m, (long long)e, (long long)i0, (long long)i1, (long long)j0,
+                   (long long)j1);
+          RS_CHECK(j < E.leaf_base && s < m && m < e, "bad node %u s %lld m %lld e %lld", j, (long long)s,
+                   (long long)m, (long long)e);
           unsigned char* sk_base = smem + (size_t)stage * C::STAGE;
           StageHdr& h = hdr[stage];
           h.dst = s + o0;
@@ -348,6 +361,11 @@ __global__ void __launch_bounds__(kMergeThreads, 3) k_merge_exec(MergeArgs E) {
           h.la = int32_t(i1 - i0);
           h.node = j;
           h.parity = node_buf(d);  // destination buffer index
+#ifdef RS_DEBUG_CHECKS
+          h.dbg_srcB = srcB + m + j0;
+          h.dbg_cB = cur.c1;
+          h.dbg_dnB = cur.dn1;
+#endif
           h.end = 0;
           // expected bytes first (tx count may complete before arrive otherwise)
           uintptr_t ka0 = reinterpret_cast<uintptr_t>(srcA + s + i0), ka1 = reinterpret_cast<uintptr_t>(srcA + s + i1);
@@ -363,21 +381,33 @@ __global__ void __launch_bounds__(kMergeThreads, 3) k_merge_exec(MergeArgs E) {
             tBb = j1 > j0 ? (uint32_t)(((tb1 + 15) & ~(uintptr_t)15) - (tb0 & ~(uintptr_t)15)) : 0u;
             tx += tA + tBb;
           }
+#ifdef RS_DEBUG_CHECKS
+          // poison the head of the stage so a copy that never landed is recognizable
+          {
+            K* pk = reinterpret_cast<K*>(sk_base);
+            for (int q = 0; q < 96; ++q) pk[q] = (K)0x7eadbeef;
+            fence_proxy_async_smem();
+          }
+#endif
+          // the whole header (window offsets included) is written BEFORE the
+          // arrival: the phase can complete as soon as the bytes land, and the
+          // arrival's release is what makes these writes visible to consumers
+          h.offA = i1 > i0 ? int32_t((ka0 & 15) / sizeof(K)) : 0;
+          h.offB = (j1 > j0 ? int32_t((kb0 & 15) / sizeof(K)) : 0) + int32_t(bA / sizeof(K));
+          if (HT) {
+            uintptr_t ta0 = reinterpret_cast<uintptr_t>(tsrcA + s + i0);
+            uintptr_t tb0 = reinterpret_cast<uintptr_t>(tsrcB + m + j0);
+            h.toffA = i1 > i0 ? int32_t((ta0 & 15) / (TB ? TB : 1)) : 0;
+            h.toffB = (j1 > j0 ? int32_t((tb0 & 15) / (TB ? TB : 1)) : 0) + int32_t(tA / (TB ? TB : 1));
+          }
           mbar_arrive_tx(&full_bar[stage], tx);
-          int32_t offA, offB;
-          uint32_t gotA = tma_window(sk_base, srcA, s + i0, s + i1, sizeof(K), &full_bar[stage], &offA);
-          uint32_t bstart = (gotA + 15) & ~15u;
-          tma_window(sk_base + bstart, srcB, m + j0, m + j1, sizeof(K), &full_bar[stage], &offB);
-          h.offA = offA;
-          h.offB = offB + int32_t(bstart / sizeof(K));
+          int32_t o_;
+          tma_window(sk_base, srcA, s + i0, s + i1, sizeof(K), &full_bar[stage], &o_);
+          tma_window(sk_base + bA, srcB, m + j0, m + j1, sizeof(K), &full_bar[stage], &o_);
           if (HT) {
             unsigned char* tg = sk_base + C::KBYTES;
-            int32_t toA, toB;
-            uint32_t gtA = tma_window(tg, tsrcA, s + i0, s + i1, TB, &full_bar[stage], &toA);
-            uint32_t tbs = (gtA + 15) & ~15u;
-            tma_window(tg + tbs, tsrcB, m + j0, m + j1, TB, &full_bar[stage], &toB);
-            h.toffA = toA;
-            h.toffB = toB + int32_t(tbs / (TB ? TB : 1));
+            tma_window(tg, tsrcA, s + i0, s + i1, TB, &full_bar[stage], &o_);
+            tma_window(tg + tA, tsrcB, m + j0, m + j1, TB, &full_bar[stage], &o_);
           }
         }
         __syncwarp();
@@ -442,6 +472,17 @@ __global__ void __launch_bounds__(kMergeThreads, 3) k_merge_exec(MergeArgs E) {
         bulk_wait_read0();
         mbar_arrive(&empty_bar[stage]);  // the stage may be refilled
         bulk_wait0();                    // the tile's bulk writes are performed
+#ifdef RS_DEBUG_CHECKS
+        for (int i = 0; i + 1 < len; ++i) {
+          K x0 = ld_volatile_k(gdst + i), x1 = ld_volatile_k(gdst + i + 1);
+          if (!(x0 <= x1)) {
+            printf("tile unsorted in global after store: node %u dst %lld i %d len %d h0 %d nvec %d pad %d smem %lld %lld glob %lld %lld\n",
+                   h.node, (long long)h.dst, i, len, h0, nvec, pad, (long long)sk[pad + i], (long long)sk[pad + i + 1],
+                   (long long)x0, (long long)x1);
+            __trap();
+          }
+        }
+#endif
         fence_proxy_async_global();      // async-proxy writes -> generic / other proxies
       }
       __syncwarp();
@@ -476,6 +517,21 @@ __global__ void __launch_bounds__(kMergeThreads, 3) k_merge_exec(MergeArgs E) {
     const T* TA = HT ? st + h.toffA : nullptr;
     const T* TBp = HT ? st + h.toffB : nullptr;
     int len = h.len, la = h.la, lb = len - la;
+#ifdef RS_DEBUG_CHECKS
+    for (int i = ct; i + 1 < la; i += kConsumerThreads)
+      RS_CHECK(A[i] <= A[i + 1], "A window unsorted: node %u dst %lld i %d la %d", h.node, (long long)h.dst, i, la);
+    for (int i = ct; i + 1 < lb; i += kConsumerThreads) {
+      if (!(B[i] <= B[i + 1])) {
+        const K* gB = reinterpret_cast<const K*>(h.dbg_srcB);
+        K g0 = ld_volatile_k(gB + i), g1 = ld_volatile_k(gB + i + 1);
+        printf("B window unsorted: node %u dst %lld i %d lb %d smem %lld %lld global-now %lld %lld child %u dn@ready %u "
+               "done-now %u need %u\n",
+               h.node, (long long)h.dst, i, lb, (long long)B[i], (long long)B[i + 1], (long long)g0, (long long)g1,
+               h.dbg_cB, h.dbg_dnB, ld_acquire_u32(E.done + h.dbg_cB), E.need[h.dbg_cB]);
+        __trap();
+      }
+    }
+#endif
     int d0 = ct * C::IPT;
     int cnt = len - d0;
     cnt = cnt < 0 ? 0 : (cnt > C::IPT ? C::IPT : cnt);
@@ -540,6 +596,13 @@ __global__ void __launch_bounds__(kMergeThreads, 3) k_merge_exec(MergeArgs E) {
         if (HT) st[tpad + d0 + q] = rt[q];
       }
     }
+#ifdef RS_DEBUG_CHECKS
+    consumer_sync();
+    for (int i = ct; i + 1 < len; i += kConsumerThreads)
+      RS_CHECK(sk[pad + i] <= sk[pad + i + 1], "merged tile unsorted in smem: node %u dst %lld i %d len %d la %d",
+               h.node, (long long)h.dst, i, len, la);
+    consumer_sync();
+#endif
     // generic SMEM writes -> visible to the bulk copy engine, then one arrival per warp
     fence_proxy_async_smem();
     __syncwarp();

@@ -365,7 +365,8 @@ int launch_exec(K* keys, void* tags, int64_t n, int w, int classic, int msuper, 
   E.met = V.met;
   E.maxb = Exec<K, TB>::maxb_for(w);
   k_phaseA<K, TB><<<grid_a, kExecThreads, smem_a, st>>>(E);
-  RS_CUDA(cudaGetLastError());
+  if (cudaError_t e_ = cudaGetLastError())
+    return fail(RS_ECUDA, std::string("k_phaseA launch/exec failed: ") + cudaGetErrorString(e_));
   prof_mark(2, st);
   MergeArgs M;
   M.key[0] = E.key[0];
@@ -388,7 +389,8 @@ int launch_exec(K* keys, void* tags, int64_t n, int w, int classic, int msuper, 
   M.tasks = V.tasks;
   M.met = V.met;
   k_merge_exec<K, TB><<<grid_m, kMergeThreads, smem_m, st>>>(M);
-  RS_CUDA(cudaGetLastError());
+  if (cudaError_t e_ = cudaGetLastError())
+    return fail(RS_ECUDA, std::string("k_merge_exec launch/exec failed: ") + cudaGetErrorString(e_));
   prof_mark(3, st);
   return RS_OK;
 }
