@@ -28,7 +28,11 @@ namespace rs {
 constexpr int kSuperMax = 15;          // tiles per merge task: runtime, <= 15 (lane groups of >= 2)
 constexpr int kStages = 2;             // smem ring depth
 constexpr int kConsumerThreads = 256;  // 8 consumer warps
-constexpr int kMergeThreads = kConsumerThreads + 64;  // + producer warp + signaller warp
+#ifndef RS_PRODUCERS
+#define RS_PRODUCERS 1
+#endif
+constexpr int kProducers = RS_PRODUCERS;  // 1: one producer feeds both stages; 2: one stage each
+constexpr int kMergeThreads = kConsumerThreads + 32 * (kProducers + 1);  // + producers + signaller
 
 template <typename K, int TB>
 struct MergeCfg {
@@ -266,11 +270,11 @@ __global__ void __launch_bounds__(kMergeThreads, 3) k_merge_exec(MergeArgs E) {
   __syncthreads();
   unsigned long long ntasks = E.met->n_tasks;
 
-  if (warp == 0) {
+  if (warp < kProducers) {
     // ------------------------------------------------------------- producer
     unsigned long long comps = 0;
-    int stage = 0;
-    uint32_t phase = 0;  // flips when stage wraps
+    int stage = kProducers == 1 ? 0 : warp;
+    uint32_t phase = 0;  // flips when stage wraps (kProducers 2: every tile of its stage)
     const int kSuper = E.msuper;
     const int G = 32 / (kSuper + 1);
     // The next task is claimed and its descriptor fetched while the current
@@ -411,7 +415,11 @@ __global__ void __launch_bounds__(kMergeThreads, 3) k_merge_exec(MergeArgs E) {
           }
         }
         __syncwarp();
-        if (++stage == kStages) { stage = 0; phase ^= 1; }
+        if (kProducers == 1) {
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        } else {
+          phase ^= 1;
+        }
       }
       if (lane == 0) RS_ACC(E.met, 7, tiss);
       cur = nxt;
@@ -425,7 +433,7 @@ __global__ void __launch_bounds__(kMergeThreads, 3) k_merge_exec(MergeArgs E) {
     return;
   }
 
-  if (warp == 1) {
+  if (warp == kProducers) {
     // ------------------------------------------------------------ signaller
     // Streams each merged tile from its stage to HBM (bulk store of the 16B-
     // aligned middle, lanes store the unaligned head / tail), hands the stage
@@ -436,10 +444,29 @@ __global__ void __launch_bounds__(kMergeThreads, 3) k_merge_exec(MergeArgs E) {
     constexpr int VT = HT ? 16 / (HT ? TB : 1) : 1;
     int stage = 0;
     uint32_t phase = 0;
+    uint32_t sph[kStages] = {0, 0};
+    int nalive = kStages;
+    bool alive[kStages] = {true, true};
     for (;;) {
-      mbar_wait(&stored_bar[stage], phase);
+      if (kProducers == 1) {
+        mbar_wait(&stored_bar[stage], phase);
+      } else {  // the stage the consumers finished (any order)
+        if (nalive == 0) break;
+        stage = -1;
+        while (stage < 0) {
+#pragma unroll
+          for (int q = 0; q < kStages; ++q)
+            if (stage < 0 && alive[q] && mbar_test_wait(&stored_bar[q], sph[q])) stage = q;
+        }
+        sph[stage] ^= 1;
+      }
       const StageHdr h = hdr[stage];
-      if (h.end) break;
+      if (h.end) {
+        if (kProducers == 1) break;
+        alive[stage] = false;
+        --nalive;
+        continue;
+      }
       unsigned char* base = smem + (size_t)stage * C::STAGE;
       K* sk = reinterpret_cast<K*>(base);
       T* st = reinterpret_cast<T*>(base + C::KBYTES);
@@ -489,25 +516,52 @@ __global__ void __launch_bounds__(kMergeThreads, 3) k_merge_exec(MergeArgs E) {
       __threadfence();  // this warp's head / tail stores and the bulk writes, GPU-wide
       if (lane == 0) asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(E.done + h.node) : "memory");
       __syncwarp();
-      if (++stage == kStages) { stage = 0; phase ^= 1; }
+      if (kProducers == 1 && ++stage == kStages) { stage = 0; phase ^= 1; }
     }
     return;
   }
 
   // --------------------------------------------------------------- consumers
-  int ct = threadIdx.x - 64;
+  int ct = threadIdx.x - 32 * (kProducers + 1);
   int cl = ct & 31;
   int stage = 0;
   uint32_t phase = 0;
+  __shared__ int s_pick;
+  uint32_t cph[kStages] = {0, 0};
+  bool alive[kStages] = {true, true};
+  int nalive = kStages;
   for (;;) {
     RS_T0(tf);
-    mbar_wait(&full_bar[stage], phase);
+    if (kProducers == 1) {
+      mbar_wait(&full_bar[stage], phase);
+    } else {
+      // the first stage to fill (independent producers: a fixed order could wait
+      // on a task whose dependency sits in the other stage)
+      if (nalive == 0) break;
+      if (ct == 0) {
+        int q0 = -1;
+        while (q0 < 0) {
+#pragma unroll
+          for (int q = 0; q < kStages; ++q)
+            if (q0 < 0 && alive[q] && mbar_test_wait(&full_bar[q], cph[q])) q0 = q;
+        }
+        s_pick = q0;
+      }
+      consumer_sync();
+      stage = s_pick;
+      mbar_wait(&full_bar[stage], cph[stage]);  // completed: orders the bulk data for this thread
+      cph[stage] ^= 1;
+    }
     if (ct == 0) RS_ACC(E.met, 3, tf);
     RS_T0(tk);
     const StageHdr h = hdr[stage];
     if (h.end) {
       if (cl == 0) mbar_arrive(&stored_bar[stage]);
-      break;
+      if (kProducers == 1) break;
+      alive[stage] = false;
+      --nalive;
+      consumer_sync();  // s_pick read by all before it is rewritten
+      continue;
     }
     unsigned char* base = smem + (size_t)stage * C::STAGE;
     K* sk = reinterpret_cast<K*>(base);
@@ -608,7 +662,7 @@ __global__ void __launch_bounds__(kMergeThreads, 3) k_merge_exec(MergeArgs E) {
     __syncwarp();
     if (cl == 0) mbar_arrive(&stored_bar[stage]);
     if (ct == 0) RS_ACC(E.met, 4, tk);
-    if (++stage == kStages) { stage = 0; phase ^= 1; }
+    if (kProducers == 1 && ++stage == kStages) { stage = 0; phase ^= 1; }
   }
 }
 
