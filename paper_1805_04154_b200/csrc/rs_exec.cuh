@@ -232,18 +232,37 @@ __device__ void d_classify(ClassifyArgs A, uint32_t* __restrict__ chunk_depth) {
   if ((threadIdx.x & 31) == 0 && maxd) atomicMax(&A.met->max_depth, (unsigned long long)maxd);
 }
 
+// Run by one whole block: per-depth slot bases (deepest first, after the
+// phase-A tasks), then per depth the exclusive scan of the chunk task counts.
+// Loads are issued in parallel / in batches (a load-store loop over global
+// memory would serialize one round trip per iteration).
 __device__ void d_task_offsets(DevMetrics* met) {
-  if (threadIdx.x != 0) return;
-  unsigned long long base = met->phaseA;
-  for (int d = (int)met->max_depth; d >= 0; --d) {
-    met->depth_base[d] = base;
-    met->depth_cursor[d] = base;
-    base += met->depth_tiles[d];
+  __shared__ unsigned long long s_dt[kMaxDepth];
+  __shared__ unsigned long long s_pa;
+  __shared__ int s_md;
+  for (int d = threadIdx.x; d < kMaxDepth; d += blockDim.x) s_dt[d] = met->depth_tiles[d];
+  if (threadIdx.x == 0) {
+    s_pa = met->phaseA;
+    s_md = (int)met->max_depth;
   }
-  met->n_tasks = base;
-  met->cursorA = 0;
-  met->task_ctr = met->phaseA;
-  met->task_ctr_A = 0;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long base = s_pa;
+    for (int d = s_md; d >= 0; --d) {
+      unsigned long long v = s_dt[d];
+      s_dt[d] = base;
+      base += v;
+    }
+    met->n_tasks = base;
+    met->cursorA = 0;
+    met->task_ctr = s_pa;
+    met->task_ctr_A = 0;
+  }
+  __syncthreads();
+  for (int d = threadIdx.x; d <= s_md; d += blockDim.x) {
+    met->depth_base[d] = s_dt[d];
+    met->depth_cursor[d] = s_dt[d];
+  }
 }
 
 // Per depth: exclusive scan of the chunk task counts, offset by depth_base.
