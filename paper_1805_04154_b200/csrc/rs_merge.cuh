@@ -26,7 +26,19 @@
 namespace rs {
 
 constexpr int kSuperMax = 15;          // tiles per merge task: runtime, <= 15 (lane groups of >= 2)
-constexpr int kStages = 2;             // smem ring depth
+#ifndef RS_STAGES
+#define RS_STAGES 2
+#endif
+#ifndef RS_IPT8
+#define RS_IPT8 15
+#endif
+#ifndef RS_IPT4
+#define RS_IPT4 31
+#endif
+#ifndef RS_MERGE_CTAS
+#define RS_MERGE_CTAS 3
+#endif
+constexpr int kStages = RS_STAGES;     // smem ring depth
 constexpr int kConsumerThreads = 256;  // 8 consumer warps
 #ifndef RS_PRODUCERS
 #define RS_PRODUCERS 1
@@ -38,7 +50,7 @@ template <typename K, int TB>
 struct MergeCfg {
   static constexpr int kb = sizeof(K);
   static constexpr int eb = kb + TB;
-  static constexpr int IPT = eb == 4 ? 31 : (eb <= 8 ? 15 : (eb <= 12 ? 11 : 7));  // odd: conflict-free write-back
+  static constexpr int IPT = eb == 4 ? RS_IPT4 : (eb <= 8 ? RS_IPT8 : (eb <= 12 ? 11 : 7));  // odd: conflict-free write-back
   static constexpr int TILE = kConsumerThreads * IPT;
   static constexpr int KBYTES = TILE * kb + 128;
   static constexpr int TBYTES = TB ? TILE * TB + 128 : 0;
@@ -247,7 +259,7 @@ __device__ int64_t warp_count(const K* A, int64_t len, K v, bool or_equal) {
 }
 
 template <typename K, int TB>
-__global__ void __launch_bounds__(kMergeThreads, 3) k_merge_exec(MergeArgs E) {
+__global__ void __launch_bounds__(kMergeThreads, RS_MERGE_CTAS) k_merge_exec(MergeArgs E) {
   using C = MergeCfg<K, TB>;
   using T = typename TagT<TB>::type;
   constexpr bool HT = TB != 0;
@@ -444,9 +456,11 @@ __global__ void __launch_bounds__(kMergeThreads, 3) k_merge_exec(MergeArgs E) {
     constexpr int VT = HT ? 16 / (HT ? TB : 1) : 1;
     int stage = 0;
     uint32_t phase = 0;
-    uint32_t sph[kStages] = {0, 0};
+    uint32_t sph[kStages];
+    bool alive[kStages];
+#pragma unroll
+    for (int q = 0; q < kStages; ++q) { sph[q] = 0; alive[q] = true; }
     int nalive = kStages;
-    bool alive[kStages] = {true, true};
     for (;;) {
       if (kProducers == 1) {
         mbar_wait(&stored_bar[stage], phase);
@@ -527,8 +541,10 @@ __global__ void __launch_bounds__(kMergeThreads, 3) k_merge_exec(MergeArgs E) {
   int stage = 0;
   uint32_t phase = 0;
   __shared__ int s_pick;
-  uint32_t cph[kStages] = {0, 0};
-  bool alive[kStages] = {true, true};
+  uint32_t cph[kStages];
+  bool alive[kStages];
+#pragma unroll
+  for (int q = 0; q < kStages; ++q) { cph[q] = 0; alive[q] = true; }
   int nalive = kStages;
   for (;;) {
     RS_T0(tf);
