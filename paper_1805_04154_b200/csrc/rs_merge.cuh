@@ -258,7 +258,9 @@ __device__ int64_t warp_count(const K* A, int64_t len, K v, bool or_equal) {
   return lo + __popc(__ballot_sync(0xffffffffu, pred));
 }
 
-template <typename K, int TB>
+// AHEAD: claim the next task during the current one's search (chosen at launch:
+// multi-tile tasks only, see the producer).
+template <typename K, int TB, bool AHEAD>
 __global__ void __launch_bounds__(kMergeThreads, RS_MERGE_CTAS) k_merge_exec(MergeArgs E) {
   using C = MergeCfg<K, TB>;
   using T = typename TagT<TB>::type;
@@ -289,11 +291,17 @@ __global__ void __launch_bounds__(kMergeThreads, RS_MERGE_CTAS) k_merge_exec(Mer
     uint32_t phase = 0;  // flips when stage wraps (kProducers 2: every tile of its stage)
     const int kSuper = E.msuper;
     const int G = 32 / (kSuper + 1);
-    // The next task is claimed and its descriptor fetched while the current
-    // task's merge-path search runs (each is a chain of dependent global round
-    // trips; interleaving hides one behind the other).  Claiming one task ahead
-    // cannot deadlock: the current task is ready, so it completes, and every
-    // task waits only on tasks claimed before it.
+    // The next task may be claimed and its descriptor fetched while the
+    // current task's merge-path search runs (each is a chain of dependent global
+    // round trips; interleaving hides one behind the other).  Claiming one task
+    // ahead cannot deadlock: the current task is ready, so it completes, and
+    // every task waits only on tasks claimed before it.
+    // Multi-tile tasks (long searches) claim the next task ahead and hide its
+    // fetch chain in the search; single-tile tasks claim just in time -- a task
+    // held ahead adds to the waits at level transitions (measured: cfg1-3 6-13%
+    // faster just in time, cfg4 (7 tiles/task) 2% faster ahead).  A compile-time
+    // choice: a runtime flag costs the just-in-time path its gain.
+    constexpr bool ahead = AHEAD;
     PTask cur, nxt;
     cur.claim(E.met);
     cur.finish(E, ntasks);
@@ -307,7 +315,7 @@ __global__ void __launch_bounds__(kMergeThreads, RS_MERGE_CTAS) k_merge_exec(Mer
         } while (!cur.ready(E.done));
       }
       if (lane == 0) RS_ACC(E.met, 5, tw);
-      nxt.claim(E.met);
+      if (ahead) nxt.claim(E.met);
       const uint32_t j = cur.j, sk = cur.sk;
       const pos_t s = cur.s, e = cur.e, m = cur.m;
       const int d = cur.d;
@@ -339,8 +347,10 @@ __global__ void __launch_bounds__(kMergeThreads, RS_MERGE_CTAS) k_merge_exec(Mer
       bool in_range = g <= (kend - kbeg) && g < kSuper + 1 && lane < G * (kSuper + 1);
       bool trivial = diag == 0 || diag == tot;
       int64_t split = group_merge_path(srcA + s, na, srcB + m, nb, diag, in_range && !trivial, G,
-                                       [&]() { nxt.advance(E, ntasks); });
-      nxt.finish(E, ntasks);
+                                       [&]() {
+                                         if (ahead) nxt.advance(E, ntasks);
+                                       });
+      if (ahead) nxt.finish(E, ntasks);
       if (diag == 0) split = 0;
       else if (diag == tot) split = na;
       if (lane == 0) RS_ACC(E.met, 1, tsrch);
@@ -434,6 +444,10 @@ __global__ void __launch_bounds__(kMergeThreads, RS_MERGE_CTAS) k_merge_exec(Mer
         }
       }
       if (lane == 0) RS_ACC(E.met, 7, tiss);
+      if (!ahead) {  // just in time: no task held ahead
+        nxt.claim(E.met);
+        nxt.finish(E, ntasks);
+      }
       cur = nxt;
     }
     if (lane == 0) {

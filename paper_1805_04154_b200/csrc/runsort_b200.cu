@@ -208,9 +208,12 @@ int exec_grid(int sms, int w, int* grid_a, size_t* smem_a, int* grid_m, size_t* 
   if (occ_m[dev] == 0) {
     RS_CUDA(cudaFuncSetAttribute(k_phaseA<K, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)Exec<K, TB>::smem_bytes(1)));
-    RS_CUDA(cudaFuncSetAttribute(k_merge_exec<K, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem_m));
+    RS_CUDA(cudaFuncSetAttribute(k_merge_exec<K, TB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)*smem_m));
+    RS_CUDA(cudaFuncSetAttribute(k_merge_exec<K, TB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)*smem_m));
     int o = 0;
-    RS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_merge_exec<K, TB>, kMergeThreads, *smem_m));
+    RS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_merge_exec<K, TB, false>, kMergeThreads, *smem_m));
     if (o < 1) return fail(RS_ECUDA, "merge executor does not fit on an SM");
     occ_m[dev] = o;
   }
@@ -388,7 +391,8 @@ int launch_exec(K* keys, void* tags, int64_t n, int w, int classic, int msuper, 
   M.done = V.done;
   M.tasks = V.tasks;
   M.met = V.met;
-  k_merge_exec<K, TB><<<grid_m, kMergeThreads, smem_m, st>>>(M);
+  if (msuper > 1) k_merge_exec<K, TB, true><<<grid_m, kMergeThreads, smem_m, st>>>(M);
+  else k_merge_exec<K, TB, false><<<grid_m, kMergeThreads, smem_m, st>>>(M);
   if (cudaError_t e_ = cudaGetLastError())
     return fail(RS_ECUDA, std::string("k_merge_exec launch/exec failed: ") + cudaGetErrorString(e_));
   prof_mark(3, st);
