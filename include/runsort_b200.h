@@ -21,6 +21,7 @@
  *   RS_ECUDA       -> RuntimeError
  *   RS_EUNSUPPORTED-> TypeError / NotImplementedError (dtype or size outside
  *                     the device path; never a silent CPU fallback)
+ *   RS_EIO         -> OSError         (gen.py:226-236 load_array file errors)
  */
 #ifndef RUNSORT_B200_H
 #define RUNSORT_B200_H
@@ -38,6 +39,7 @@ extern "C" {
 #define RS_ENOMEM 3
 #define RS_ECUDA 4
 #define RS_EUNSUPPORTED 5
+#define RS_EIO 6
 
 #define RS_ALGO_POWERSORT 0
 #define RS_ALGO_PEEKSORT 1
@@ -111,6 +113,15 @@ int rs_debug_counters(int key_dtype, int tag_bytes, int64_t n, int32_t min_run_l
 
 /* Largest min_run_len the device path accepts for this element type. */
 int32_t rs_max_min_run_len(int key_dtype, int tag_bytes);
+
+/* Input format of the reference's generators (gen.py:210-236 save_array /
+ * load_array): a ".bin" file is a little-endian uint64 element count followed
+ * by that many little-endian int64 values.  Reads the file straight into device
+ * memory (pinned staging, chunked async copies on `stream`; synchronizes before
+ * returning).  `*n_out` receives the count; with dst == NULL only the header is
+ * read.  RS_EINVAL: truncated / malformed file or count > capacity;
+ * RS_EIO: the file cannot be opened. */
+int rs_load_bin(const char* path, int64_t* n_out, void* dst, int64_t capacity, void* stream);
 
 /* Thread-local message for the last non-RS_OK return. */
 const char* rs_last_error(void);

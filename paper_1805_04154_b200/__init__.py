@@ -9,9 +9,13 @@ behind the C ABI in ``include/runsort_b200.h``.
 """
 from .opttree import MergeLeaf, MergeNode, internal_nodes_inorder
 from .runcore import Metrics, Run
+from .io import load_array, load_array_device, save_array
 from .sorters import SORTERS, SortConfig, node_power_bitwise, node_power_def, peeksort, powersort
 
 __all__ = [
+    "load_array",
+    "load_array_device",
+    "save_array",
     "Metrics", "Run", "SortConfig", "SORTERS",
     "peeksort", "powersort",
     "node_power_def", "node_power_bitwise",

@@ -15,10 +15,12 @@ RS_OK, RS_EINVAL, RS_EINVARIANT, RS_ENOMEM, RS_ECUDA, RS_EUNSUPPORTED = range(6)
 RS_ALGO_POWERSORT, RS_ALGO_PEEKSORT = 0, 1
 RS_KEY_I32, RS_KEY_I64 = 1, 2
 RS_MERGE_BITONIC, RS_MERGE_CLASSIC = 0, 1
+RS_EIO = 6
 
 # every symbol include/runsort_b200.h declares
 EXPORTS = ("rs_workspace_bytes", "rs_sort", "rs_fetch_metrics", "rs_sort_host", "rs_profile",
-           "rs_profile_read", "rs_debug_counters", "rs_max_min_run_len", "rs_last_error", "rs_version")
+           "rs_profile_read", "rs_debug_counters", "rs_max_min_run_len", "rs_load_bin", "rs_last_error",
+           "rs_version")
 
 
 class RsMetrics(ctypes.Structure):
@@ -65,6 +67,9 @@ def lib():
                                         ctypes.POINTER(ctypes.c_uint64), ctypes.c_int]
         L.rs_max_min_run_len.restype = ctypes.c_int32
         L.rs_max_min_run_len.argtypes = [ctypes.c_int, ctypes.c_int]
+        L.rs_load_bin.restype = ctypes.c_int
+        L.rs_load_bin.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_int64), ctypes.c_void_p, ctypes.c_int64,
+                                  ctypes.c_void_p]
         L.rs_last_error.restype = ctypes.c_char_p
         L.rs_last_error.argtypes = []
         L.rs_version.restype = ctypes.c_int
@@ -82,6 +87,8 @@ def check(rc: int) -> None:
         raise ValueError(msg)
     if rc == RS_EINVARIANT:
         raise AssertionError(msg)
+    if rc == RS_EIO:
+        raise OSError(msg)
     if rc == RS_ENOMEM:
         raise MemoryError(msg)
     if rc == RS_EUNSUPPORTED:

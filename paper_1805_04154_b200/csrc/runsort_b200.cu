@@ -721,6 +721,69 @@ int rs_profile_read(double* ms, int cap) {
   return k;
 }
 
+int rs_load_bin(const char* path, int64_t* n_out, void* dst, int64_t capacity, void* stream) {
+  // gen.py:210-236: "<Q" count, then count "<i8" values (this code assumes a
+  // little-endian host, as every CUDA host is)
+  if (!path || !n_out) return fail(RS_EINVAL, "rs_load_bin: null path or n_out");
+  FILE* f = fopen(path, "rb");
+  if (!f) return fail(RS_EIO, std::string("rs_load_bin: cannot open ") + path);
+  uint64_t count = 0;
+  if (fread(&count, 8, 1, f) != 1) {
+    fclose(f);
+    return fail(RS_EINVAL, std::string("rs_load_bin: missing header in ") + path);
+  }
+  if (count > (uint64_t)INT64_MAX / 8) {
+    fclose(f);
+    return fail(RS_EINVAL, "rs_load_bin: element count out of range");
+  }
+  *n_out = (int64_t)count;
+  if (!dst) {
+    fclose(f);
+    return RS_OK;
+  }
+  if ((int64_t)count > capacity) {
+    fclose(f);
+    return fail(RS_EINVAL, "rs_load_bin: file holds more elements than capacity");
+  }
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const size_t kChunk = (size_t)32 << 20;  // bytes per staging buffer (double-buffered)
+  void* stage[2] = {nullptr, nullptr};
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  int rc = RS_OK;
+  for (int i = 0; i < 2 && rc == RS_OK; ++i) {
+    if (cudaMallocHost(&stage[i], kChunk) != cudaSuccess || cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming) != cudaSuccess)
+      rc = fail(RS_ENOMEM, "rs_load_bin: pinned staging allocation failed");
+  }
+  size_t total = (size_t)count * 8, done = 0;
+  int b = 0;
+  while (rc == RS_OK && done < total) {
+    size_t len = total - done < kChunk ? total - done : kChunk;
+    if (cudaEventSynchronize(ev[b]) != cudaSuccess) {  // this buffer's previous copy finished
+      rc = fail(RS_ECUDA, "rs_load_bin: event synchronize failed");
+      break;
+    }
+    if (fread(stage[b], 1, len, f) != len) {
+      rc = fail(RS_EINVAL, std::string("rs_load_bin: truncated data in ") + path);
+      break;
+    }
+    if (cudaMemcpyAsync(static_cast<unsigned char*>(dst) + done, stage[b], len, cudaMemcpyHostToDevice, st) !=
+            cudaSuccess ||
+        cudaEventRecord(ev[b], st) != cudaSuccess) {
+      rc = fail(RS_ECUDA, "rs_load_bin: host-to-device copy failed");
+      break;
+    }
+    done += len;
+    b ^= 1;
+  }
+  cudaStreamSynchronize(st);
+  for (int i = 0; i < 2; ++i) {
+    if (ev[i]) cudaEventDestroy(ev[i]);
+    if (stage[i]) cudaFreeHost(stage[i]);
+  }
+  fclose(f);
+  return rc;
+}
+
 const char* rs_last_error(void) { return g_err.c_str(); }
 
 int rs_version(void) { return 100; }
