@@ -73,6 +73,11 @@ def lib():
             ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(OrcMetrics),
             ctypes.c_void_p, ctypes.c_int64,
         ]
+        L.orc_baseline.restype = ctypes.c_int64
+        L.orc_baseline.argtypes = [
+            ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_int64,
+            ctypes.c_int32, ctypes.c_int32, ctypes.c_double, ctypes.POINTER(OrcMetrics),
+        ]
         L.orc_node_power_def.restype = ctypes.c_int
         L.orc_node_power_def.argtypes = [ctypes.c_int64] * 5
         L.orc_node_power0.restype = ctypes.c_int
@@ -144,6 +149,22 @@ def peeksort(a: np.ndarray, min_run_len: int = 24, merge_kind: str = "bitonic",
     if want_tree and n > 0:
         res.merges = merges[:k].copy()
     return res
+
+
+BASELINES = {"top-down": 2, "bottom-up": 3, "alpha-stack": 4, "alpha-merge": 5}
+
+
+def baseline(name: str, a: np.ndarray, min_run_len: int = 24, merge_kind: str = "bitonic",
+             tags: Optional[np.ndarray] = None, alpha: float = 2.0) -> OracleResult:
+    """Reference baseline sorters (sorters.py:524-660) on the CPU, in place."""
+    _check(a, tags)
+    m = OrcMetrics()
+    r = lib().orc_baseline(BASELINES[name], _key_kind(a), a.ctypes.data, tags.itemsize if tags is not None else 0,
+                           tags.ctypes.data if tags is not None else None, len(a), int(min_run_len),
+                           1 if merge_kind == "classic" else 0, float(alpha), ctypes.byref(m))
+    if r < 0:
+        raise AssertionError(f"oracle baseline failure ({r})")
+    return OracleResult(m.merge_cost, m.comparisons, m.runs_detected, m.max_stack_height)
 
 
 def node_power_def(s1, e1, s2, e2, n) -> int:

@@ -262,6 +262,91 @@ static int64_t powersort_##SFX(KT *a, tagv t, int64_t n, int32_t w, int classic,
     return nleaves;                                                                     \
 }                                                                                       \
                                                                                         \
+/* ---- elementary baselines, sorters.py:524-581 ---- */                              \
+/* top_down_mergesort (sorters.py:524-552): midpoint split, insertion sort of      \
+ * ranges of <= w elements, one comparison to skip an in-order merge. */             \
+static void td_sort_##SFX(KT *a, tagv t, int64_t l, int64_t r, int32_t w, KT *buf,      \
+                          unsigned char *tbuf, int classic, orc_metrics *m) {           \
+    if (r - l + 1 <= w) { insertion_##SFX(a, t, l, r, 1, m); return; }                 \
+    int64_t mid = l + (r - l) / 2;                                                      \
+    td_sort_##SFX(a, t, l, mid, w, buf, tbuf, classic, m);                              \
+    td_sort_##SFX(a, t, mid + 1, r, w, buf, tbuf, classic, m);                          \
+    m->comparisons += 1;                                                                \
+    if (a[mid] <= a[mid + 1]) return;                                                   \
+    merge_##SFX(a, t, l, mid + 1, r, buf, tbuf, classic, m);                            \
+}                                                                                       \
+/* bottom_up_mergesort (sorters.py:555-581): insertion-sorted chunks of w, then     \
+ * passes of doubling width with the same skip check. */                               \
+static void bu_sort_##SFX(KT *a, tagv t, int64_t n, int32_t w, KT *buf,                 \
+                          unsigned char *tbuf, int classic, orc_metrics *m) {           \
+    if (w > 1)                                                                          \
+        for (int64_t c = 0; c < n; c += w)                                              \
+            insertion_##SFX(a, t, c, (c + w < n ? c + w : n) - 1, 1, m);                \
+    for (int64_t width = w; width < n; width *= 2) {                                    \
+        for (int64_t l = 0; l < n - width; l += 2 * width) {                            \
+            int64_t mid = l + width;                                                    \
+            int64_t r = l + 2 * width - 1 < n - 1 ? l + 2 * width - 1 : n - 1;          \
+            m->comparisons += 1;                                                        \
+            if (a[mid - 1] <= a[mid]) continue;                                         \
+            merge_##SFX(a, t, l, mid, r, buf, tbuf, classic, m);                        \
+        }                                                                               \
+    }                                                                                   \
+}                                                                                       \
+/* _stack_natural_sort (sorters.py:587-635): detect + extend runs like powersort,  \
+ * push, merge the top two while len_below < alpha * len_top (alpha-merge also      \
+ * merges the top two before the push while the top is shorter than the new run),   \
+ * finally merge the stack bottom-up, left to right. */                                \
+static int64_t alpha_sort_##SFX(KT *a, tagv t, int64_t n, int32_t w, int classic,       \
+                                double alpha, int pre_push, orc_metrics *m) {           \
+    if (n <= 1) { m->runs_detected = (uint64_t)n; return 0; }                           \
+    KT *buf = (KT *)malloc((size_t)n * sizeof(KT));                                     \
+    unsigned char *tbuf = t.bytes ? (unsigned char *)malloc((size_t)n * t.bytes) : 0;   \
+    int64_t cap = 64, h = 0;                                                            \
+    int64_t *ss = (int64_t *)malloc(cap * sizeof(int64_t));                             \
+    int64_t *se = (int64_t *)malloc(cap * sizeof(int64_t));                             \
+    int64_t pos = 0;                                                                    \
+    while (pos < n) {                                                                   \
+        int desc; int64_t e = find_run_right_##SFX(a, t, pos, n - 1, m, &desc);         \
+        m->runs_detected += 1;                                                          \
+        int64_t len = e - pos + 1;                                                      \
+        if (len < w) { e = (pos + w - 1 < n - 1) ? pos + w - 1 : n - 1;                 \
+                       insertion_##SFX(a, t, pos, e, len, m); }                         \
+        int64_t s = pos;                                                                \
+        if (pre_push)                                                                   \
+            while (h >= 2 && se[h - 1] - ss[h - 1] + 1 < e - s + 1) {                   \
+                merge_##SFX(a, t, ss[h - 2], ss[h - 1], se[h - 1], buf, tbuf, classic, m); \
+                se[h - 2] = se[h - 1]; h--;                                             \
+            }                                                                           \
+        if (h == cap) { cap *= 2; ss = (int64_t *)realloc(ss, cap * sizeof(int64_t));   \
+                        se = (int64_t *)realloc(se, cap * sizeof(int64_t)); }           \
+        ss[h] = s; se[h] = e; h++;                                                      \
+        while (h >= 2) {                                                                \
+            int64_t lb = se[h - 2] - ss[h - 2] + 1, lt = se[h - 1] - ss[h - 1] + 1;     \
+            if ((double)lb < alpha * (double)lt) {                                      \
+                merge_##SFX(a, t, ss[h - 2], ss[h - 1], se[h - 1], buf, tbuf, classic, m); \
+                se[h - 2] = se[h - 1]; h--;                                             \
+            } else break;                                                               \
+        }                                                                               \
+        if ((uint64_t)h > m->max_stack_height) m->max_stack_height = (uint64_t)h;       \
+        pos = e + 1;                                                                    \
+    }                                                                                   \
+    for (int64_t k = 1; k < h; k++) /* cleanup: bottom-up, left to right */             \
+        merge_##SFX(a, t, ss[0], ss[k], se[k], buf, tbuf, classic, m);                  \
+    free(ss); free(se); free(buf); free(tbuf);                                          \
+    return 0;                                                                           \
+}                                                                                       \
+static int64_t baseline_##SFX(int algo, KT *a, tagv t, int64_t n, int32_t w,            \
+                              int classic, double alpha, orc_metrics *m) {              \
+    if (algo == 4 || algo == 5) return alpha_sort_##SFX(a, t, n, w, classic, alpha, algo == 5, m); \
+    if (n <= 1) return 0;                                                               \
+    KT *buf = (KT *)malloc((size_t)n * sizeof(KT));                                     \
+    unsigned char *tbuf = t.bytes ? (unsigned char *)malloc((size_t)n * t.bytes) : 0;   \
+    if (algo == 2) td_sort_##SFX(a, t, 0, n - 1, w, buf, tbuf, classic, m);             \
+    else bu_sort_##SFX(a, t, n, w, buf, tbuf, classic, m);                              \
+    free(buf); free(tbuf);                                                              \
+    return 0;                                                                           \
+}                                                                                       \
+                                                                                        \
 /* ---- peeksort, sorters.py:146-361 ---- */                                           \
 typedef struct {                                                                        \
     KT *a; tagv t; KT *buf; unsigned char *tbuf; int classic; int32_t w;                \
@@ -473,6 +558,17 @@ int64_t orc_peeksort(int key_kind, void *keys, int tag_bytes, void *tags, int64_
     if (key_kind == 0)
         return peeksort_i32((int32_t *)keys, t, n, min_run_len, classic, m, merges_out, cap);
     return peeksort_i64((int64_t *)keys, t, n, min_run_len, classic, m, merges_out, cap);
+}
+
+/* algo: 2 top-down, 3 bottom-up, 4 alpha-stack, 5 alpha-merge (sorters.py:524-660).
+ * Returns 0, or < 0 on a bad algo code. */
+int64_t orc_baseline(int algo, int key_kind, void *keys, int tag_bytes, void *tags, int64_t n,
+                     int32_t min_run_len, int32_t classic, double alpha, orc_metrics *m) {
+    if (algo < 2 || algo > 5) return -1;
+    tagv t = {(unsigned char *)tags, tags ? tag_bytes : 0};
+    if (key_kind == 0)
+        return baseline_i32(algo, (int32_t *)keys, t, n, min_run_len, classic, alpha, m);
+    return baseline_i64(algo, (int64_t *)keys, t, n, min_run_len, classic, alpha, m);
 }
 
 int orc_node_power0(int64_t s1, int64_t e1, int64_t s2, int64_t e2, int64_t n) {
