@@ -43,6 +43,11 @@ extern "C" {
 
 #define RS_ALGO_POWERSORT 0
 #define RS_ALGO_PEEKSORT 1
+/* reference baseline sorters (sorters.py:524-660) on the same executor */
+#define RS_ALGO_TOP_DOWN 2
+#define RS_ALGO_BOTTOM_UP 3
+#define RS_ALGO_ALPHA_STACK 4
+#define RS_ALGO_ALPHA_MERGE 5
 
 #define RS_KEY_I32 1
 #define RS_KEY_I64 2
@@ -84,6 +89,12 @@ size_t rs_workspace_bytes(int algo, int key_dtype, int tag_bytes, int64_t n, int
 int rs_sort(int algo, int key_dtype, void* keys, int tag_bytes, void* tags, int64_t n,
             int32_t min_run_len, int32_t merge_kind, void* workspace, size_t ws_bytes,
             void* stream, rs_metrics* out, rs_tree* tree);
+
+/* rs_sort with the alpha-stack / alpha-merge growth ratio (SortConfig.alpha,
+ * sorters.py:73-87; must be > 1).  rs_sort uses alpha = 2.0. */
+int rs_sort_ex(int algo, int key_dtype, void* keys, int tag_bytes, void* tags, int64_t n,
+               int32_t min_run_len, int32_t merge_kind, double alpha, void* workspace, size_t ws_bytes,
+               void* stream, rs_metrics* out, rs_tree* tree);
 
 /* Synchronize `stream` and read the counters of the last rs_sort that used
  * `workspace` (same n / dtypes / min_run_len). */

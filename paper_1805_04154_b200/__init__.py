@@ -10,7 +10,8 @@ behind the C ABI in ``include/runsort_b200.h``.
 from .opttree import MergeLeaf, MergeNode, internal_nodes_inorder
 from .runcore import Metrics, Run
 from .io import load_array, load_array_device, save_array
-from .sorters import SORTERS, SortConfig, node_power_bitwise, node_power_def, peeksort, powersort
+from .sorters import (SORTERS, SortConfig, alpha_merge_sort, alpha_stack_sort, bottom_up_mergesort,
+                      node_power_bitwise, node_power_def, peeksort, powersort, top_down_mergesort)
 
 __all__ = [
     "load_array",
@@ -18,6 +19,7 @@ __all__ = [
     "save_array",
     "Metrics", "Run", "SortConfig", "SORTERS",
     "peeksort", "powersort",
+    "top_down_mergesort", "bottom_up_mergesort", "alpha_stack_sort", "alpha_merge_sort",
     "node_power_def", "node_power_bitwise",
     "MergeLeaf", "MergeNode", "internal_nodes_inorder",
 ]

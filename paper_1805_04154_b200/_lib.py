@@ -13,12 +13,13 @@ LIB_PATH = os.environ.get("RS_LIB") or os.path.join(HERE, "librunsort_b200.so")
 
 RS_OK, RS_EINVAL, RS_EINVARIANT, RS_ENOMEM, RS_ECUDA, RS_EUNSUPPORTED = range(6)
 RS_ALGO_POWERSORT, RS_ALGO_PEEKSORT = 0, 1
+RS_ALGO_TOP_DOWN, RS_ALGO_BOTTOM_UP, RS_ALGO_ALPHA_STACK, RS_ALGO_ALPHA_MERGE = 2, 3, 4, 5
 RS_KEY_I32, RS_KEY_I64 = 1, 2
 RS_MERGE_BITONIC, RS_MERGE_CLASSIC = 0, 1
 RS_EIO = 6
 
 # every symbol include/runsort_b200.h declares
-EXPORTS = ("rs_workspace_bytes", "rs_sort", "rs_fetch_metrics", "rs_sort_host", "rs_profile",
+EXPORTS = ("rs_workspace_bytes", "rs_sort", "rs_sort_ex", "rs_fetch_metrics", "rs_sort_host", "rs_profile",
            "rs_profile_read", "rs_debug_counters", "rs_max_min_run_len", "rs_load_bin", "rs_last_error",
            "rs_version")
 
@@ -51,6 +52,10 @@ def lib():
         L.rs_sort.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p,
                               ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p, ctypes.c_size_t,
                               ctypes.c_void_p, ctypes.POINTER(RsMetrics), ctypes.POINTER(RsTree)]
+        L.rs_sort_ex.restype = ctypes.c_int
+        L.rs_sort_ex.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p,
+                                 ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_double, ctypes.c_void_p,
+                                 ctypes.c_size_t, ctypes.c_void_p, ctypes.POINTER(RsMetrics), ctypes.POINTER(RsTree)]
         L.rs_fetch_metrics.restype = ctypes.c_int
         L.rs_fetch_metrics.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_int32,
                                        ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(RsMetrics)]

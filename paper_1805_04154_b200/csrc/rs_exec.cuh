@@ -89,7 +89,8 @@ struct ClassifyArgs {
   int tile;   // leaf-tile granularity (phase A)
   int mtile;  // merge-tile granularity (merge executor)
   int msuper; // merge tiles per merge task
-  int peek;   // peeksort: run-detection comparisons were counted during the replay
+  int peek;   // no run-detection comparison term (peeksort counted its scans; top-down/bottom-up detect none)
+  int runtime_merges;  // merges may be skipped at run time: merge_cost / merge comparisons counted by the executor
   uint32_t leaf_base;
   const pos_t* leaf_start;
   const uint32_t* leaf_info;
@@ -195,8 +196,10 @@ __device__ void d_classify(ClassifyArgs A, uint32_t* __restrict__ chunk_depth) {
     cntA += c == 1 ? 1 : (unsigned long long)tl;
     if (i >= 1) {
       pos_t span = A.node_e[i] - A.node_s[i];
-      mcost += span;
-      if (!A.classic) comps += span;  // runcore.py:299-301
+      if (!A.runtime_merges) {
+        mcost += span;
+        if (!A.classic) comps += span;  // runcore.py:299-301
+      }
       int64_t tn, tk;
       int cn = classify_node(A, i, &tn, &tk);
       A.cls[i] = (uint8_t)cn;

@@ -95,6 +95,7 @@ struct MergeArgs {
   DevMetrics* met;
   const uint8_t* cls;  // unified id -> class (2 = merge node for internal ids)
   uint32_t leaf_base;
+  int skipchk;  // top-down / bottom-up: one comparison per node, in-order merges skipped (sorters.py:545-550,575-578)
 };
 
 // Lane-group merge-path search: lanes [g*G, g*G+G) cooperate on diagonal `diag`
@@ -286,7 +287,7 @@ __global__ void __launch_bounds__(kMergeThreads, RS_MERGE_CTAS) k_merge_exec(Mer
 
   if (warp < kProducers) {
     // ------------------------------------------------------------- producer
-    unsigned long long comps = 0;
+    unsigned long long comps = 0, mcost = 0;
     int stage = kProducers == 1 ? 0 : warp;
     uint32_t phase = 0;  // flips when stage wraps (kProducers 2: every tile of its stage)
     const int kSuper = E.msuper;
@@ -355,7 +356,21 @@ __global__ void __launch_bounds__(kMergeThreads, RS_MERGE_CTAS) k_merge_exec(Mer
       else if (diag == tot) split = na;
       if (lane == 0) RS_ACC(E.met, 1, tsrch);
       RS_T0(tiss);
-      if (E.classic && kbeg == 0) {
+      bool merged = true;  // the reference performs this merge (Metrics)
+      if (E.skipchk && kbeg == 0) {
+        // sorters.py:545-550 / 575-578: one comparison; an in-order pair is not
+        // merged (the stable merge below then equals the concatenation)
+        K lastL = ldcg(srcA + m - 1), firstR = ldcg(srcB + m);
+        merged = !(lastL <= firstR);
+        if (lane == 0) {
+          comps += 1;
+          if (merged) {
+            mcost += (unsigned long long)tot;
+            if (!E.classic) comps += (unsigned long long)tot;  // runcore.py:299-301
+          }
+        }
+      }
+      if (E.classic && kbeg == 0 && merged) {
         // runcore.py:321-324
         K maxL = ldcg(srcA + m - 1), maxR = ldcg(srcB + e - 1);
         int64_t rl = warp_count(srcB + m, nb, maxL, false);
@@ -455,6 +470,7 @@ __global__ void __launch_bounds__(kMergeThreads, RS_MERGE_CTAS) k_merge_exec(Mer
       hdr[stage].end = 1;
       mbar_arrive(&full_bar[stage]);
       if (comps) atomicAdd(&E.met->comparisons, comps);
+      if (mcost) atomicAdd(&E.met->merge_cost, mcost);
     }
     return;
   }

@@ -33,6 +33,7 @@ struct PrepArgs {
   int64_t done_words;
   TreeArrays T;
   ClassifyArgs CA;
+  int leaves_only;  // stop after the leaf phase (alpha-stack sorts build their tree on the host)
 };
 
 template <typename K>
@@ -86,6 +87,7 @@ __global__ void __launch_bounds__(256, 3) k_prep(PrepArgs P) {
   }
   grid.sync();
   RS_TS(met, 4);
+  if (P.leaves_only) return;
   // small trees: phases 5-9 in block 0 alone, out of shared memory (rs_small.cuh)
   if ((int64_t)met->n_leaves <= kSmallR) {
     extern __shared__ __align__(16) unsigned char smem_prep[];

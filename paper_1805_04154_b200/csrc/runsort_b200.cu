@@ -11,6 +11,7 @@
 //   6. k_classify / k_task_offsets / k_task_fill   executor task list
 //   7. k_execute       persistent dataflow executor (leaves + merges)
 #include <algorithm>
+#include <functional>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -19,6 +20,7 @@
 #include <vector>
 
 #include "../../include/runsort_b200.h"
+#include "rs_baseline.cuh"
 #include "rs_chain.cuh"
 #include "rs_common.cuh"
 #include "rs_exec.cuh"
@@ -112,6 +114,8 @@ Layout make_layout(int64_t n, int w, int kb, int tb, int algo) {
   L.ntiles = (n + kChainT - 1) / kChainT;
   L.ngroups = (L.ntiles + kChainGroup - 1) / kChainGroup;
   int64_t minleaf = w > 2 ? w : 2;
+  if (algo == RS_ALGO_TOP_DOWN) minleaf = (w + 1) / 2;  // halves of ranges > w
+  if (algo == RS_ALGO_BOTTOM_UP) minleaf = w;            // chunks of w
   L.r_max = n / minleaf + 2;
   if (L.r_max > n + 1 || algo == RS_ALGO_PEEKSORT) L.r_max = n + 1;  // peeksort leaves can be single elements
   L.leaf_base = (uint32_t)(L.r_max + 1);
@@ -329,8 +333,10 @@ int fuse_avg() {
 }
 
 template <typename K, int TB>
-ClassifyArgs classify_args(const WsView& V, const Layout& L, int64_t n, int w, int classic, int msuper, int peek) {
-  return ClassifyArgs{n, w, classic, L.fcap, L.tile, MergeCfg<K, TB>::TILE, msuper, peek, L.leaf_base,
+ClassifyArgs classify_args(const WsView& V, const Layout& L, int64_t n, int w, int classic, int msuper, int peek,
+                           int runtime_merges = 0, int fcap = -1) {
+  return ClassifyArgs{n, w, classic, fcap >= 0 ? fcap : L.fcap, L.tile, MergeCfg<K, TB>::TILE, msuper, peek,
+                      runtime_merges, L.leaf_base,
                       V.leaf_start, V.leaf_info, V.leaf_depth, V.depth, V.node_s, V.node_e, V.parent, V.need,
                       V.cls, V.tasks, V.met, V.node_a, V.node_b, Exec<K, TB>::maxb_for(w), fuse_avg()};
 }
@@ -338,7 +344,7 @@ ClassifyArgs classify_args(const WsView& V, const Layout& L, int64_t n, int w, i
 // Phase A (fused subtrees, large leaves) + the merge executor.
 template <typename K, int TB>
 int launch_exec(K* keys, void* tags, int64_t n, int w, int classic, int msuper, const WsView& V, const Layout& L,
-                int sms, cudaStream_t st) {
+                int sms, cudaStream_t st, int skipchk = 0) {
   int grid_a, grid_m;
   size_t smem_a, smem_m;
   if (int e = exec_grid<K, TB>(sms, w, &grid_a, &smem_a, &grid_m, &smem_m)) return e;
@@ -382,6 +388,7 @@ int launch_exec(K* keys, void* tags, int64_t n, int w, int classic, int msuper, 
   M.leaf_base = L.leaf_base;
   M.classic = classic;
   M.msuper = msuper;
+  M.skipchk = skipchk;
   M.leaf_start = V.leaf_start;
   M.depth = V.depth;
   M.node_s = V.node_s;
@@ -401,7 +408,7 @@ int launch_exec(K* keys, void* tags, int64_t n, int w, int classic, int msuper, 
 
 template <typename K, int TB>
 int run_powersort(K* keys, void* tags, int64_t n, int w, int classic, unsigned char* ws, const Layout& L,
-                  cudaStream_t st) {
+                  cudaStream_t st, int leaves_only = 0) {
   int sms;
   if (int e = device_sms(&sms)) return e;
   WsView V = view(ws, L);
@@ -450,14 +457,226 @@ int run_powersort(K* keys, void* tags, int64_t n, int w, int classic, unsigned c
   PA.done = V.done;
   PA.done_words = 2 * L.r_max + 2;
   PA.T = tree_arrays(V, L);
+  PA.leaves_only = leaves_only;
   int msuper = merge_super<K, TB>(n, sms);
   PA.CA = classify_args<K, TB>(V, L, n, w, classic, msuper, 0);
   int grid_p;
   if (int e = prep_grid<K>(sms, sm, &grid_p)) return e;
   void* kargs[] = {&PA};
   RS_CUDA(cudaLaunchCooperativeKernel((void*)k_prep<K>, dim3(grid_p), dim3(256), kargs, sm, st));
+  if (leaves_only) return RS_OK;
   prof_mark(1, st);
   return launch_exec<K, TB>(keys, tags, n, w, classic, msuper, V, L, sms, st);
+}
+
+// ------------------------------------------------ baseline sorters' trees
+// Host-built merge trees in the workspace's tree format: leaves i = 0..r-1
+// (unified id leaf_base + i), internal node j = the boundary between leaf j-1
+// and leaf j (the first leaf of its right subtree), depth = distance from the
+// root.  Nodes are appended in creation order, children before parents.
+struct HostTree {
+  int64_t r = 0;
+  uint32_t leaf_base = 0;
+  std::vector<int64_t> start;    // r + 1 leaf starts
+  std::vector<int32_t> first, last;  // per unified id: first / last leaf (nodes: index j)
+  std::vector<int32_t> na, nb;   // [j] leaf range
+  std::vector<uint32_t> child;   // [2j + side]
+  std::vector<uint32_t> order;   // internal nodes in creation order
+  uint64_t max_stack = 0;
+  void init(int64_t r_, uint32_t lb) {
+    r = r_;
+    leaf_base = lb;
+    na.assign(r, 0);
+    nb.assign(r, 0);
+    child.assign(2 * (size_t)r, 0);
+    order.clear();
+  }
+  int32_t lfirst(uint32_t id) const { return id >= leaf_base ? (int32_t)(id - leaf_base) : na[id]; }
+  int32_t llast(uint32_t id) const { return id >= leaf_base ? (int32_t)(id - leaf_base) : nb[id]; }
+  uint32_t join(uint32_t lid, uint32_t rid) {  // merge two adjacent subtrees
+    uint32_t j = (uint32_t)lfirst(rid);
+    na[j] = lfirst(lid);
+    nb[j] = llast(rid);
+    child[2 * (size_t)j] = lid;
+    child[2 * (size_t)j + 1] = rid;
+    order.push_back(j);
+    return j;
+  }
+};
+
+// sorters.py:524-552: ranges of <= w elements are leaves, others split at the midpoint
+void build_top_down(HostTree& H, int64_t n, int w) {
+  H.start.clear();
+  std::vector<std::pair<int64_t, int64_t>> leaves;
+  // leaves in order (iterative DFS, left first)
+  std::vector<std::pair<int64_t, int64_t>> stk{{0, n - 1}};
+  while (!stk.empty()) {
+    auto [l, r] = stk.back();
+    stk.pop_back();
+    if (r - l + 1 <= w) { leaves.push_back({l, r}); continue; }
+    int64_t m = l + (r - l) / 2;
+    stk.push_back({m + 1, r});
+    stk.push_back({l, m});
+  }
+  H.init((int64_t)leaves.size(), H.leaf_base);
+  for (auto& lr : leaves) H.start.push_back(lr.first);
+  H.start.push_back(n);
+  // joins bottom-up: recurse again over positions, mapping ranges to leaf ids
+  std::function<uint32_t(int64_t, int64_t, int64_t&)> rec = [&](int64_t l, int64_t r, int64_t& next) -> uint32_t {
+    if (r - l + 1 <= w) return H.leaf_base + (uint32_t)(next++);
+    int64_t m = l + (r - l) / 2;
+    uint32_t a = rec(l, m, next);
+    uint32_t b = rec(m + 1, r, next);
+    return H.join(a, b);
+  };
+  int64_t next = 0;
+  rec(0, n - 1, next);
+}
+
+// sorters.py:555-581: chunks of w, then passes merging block pairs of width w, 2w, ...
+void build_bottom_up(HostTree& H, int64_t n, int w) {
+  int64_t r = (n + w - 1) / w;
+  H.init(r, H.leaf_base);
+  H.start.resize(r + 1);
+  for (int64_t k = 0; k < r; ++k) H.start[k] = k * w;
+  H.start[r] = n;
+  std::vector<uint32_t> cur(r);
+  for (int64_t k = 0; k < r; ++k) cur[k] = H.leaf_base + (uint32_t)k;
+  for (int64_t width = w; width < n; width *= 2) {
+    int64_t nb = (int64_t)cur.size();
+    std::vector<uint32_t> nxt;
+    for (int64_t k = 0; k < nb; k += 2) {
+      if (k + 1 < nb) nxt.push_back(H.join(cur[k], cur[k + 1]));
+      else nxt.push_back(cur[k]);
+    }
+    cur.swap(nxt);
+  }
+}
+
+// sorters.py:587-635 over the leaf lengths (runs already detected and extended)
+void build_alpha(HostTree& H, const std::vector<int64_t>& starts, double alpha, bool pre_push) {
+  int64_t r = (int64_t)starts.size() - 1;
+  H.init(r, H.leaf_base);
+  H.start = starts;
+  struct E { uint32_t id; int64_t len; };
+  std::vector<E> st;
+  uint64_t hmax = 0;
+  for (int64_t i = 0; i < r; ++i) {
+    int64_t len = starts[i + 1] - starts[i];
+    auto merge_top_two = [&]() {
+      E b = st.back(); st.pop_back();
+      E a = st.back(); st.pop_back();
+      st.push_back({H.join(a.id, b.id), a.len + b.len});
+    };
+    if (pre_push)
+      while (st.size() >= 2 && st.back().len < len) merge_top_two();
+    st.push_back({H.leaf_base + (uint32_t)i, len});
+    while (st.size() >= 2 && (double)st[st.size() - 2].len < alpha * (double)st.back().len) merge_top_two();
+    if (st.size() > hmax) hmax = st.size();
+  }
+  // cleanup: merge the stack bottom-up, left to right
+  while (st.size() >= 2) {
+    E a = st[0], b = st[1];
+    st.erase(st.begin(), st.begin() + 2);
+    st.insert(st.begin(), E{H.join(a.id, b.id), a.len + b.len});
+  }
+  H.max_stack = hmax;
+}
+
+// Depths (root = 0) and the workspace arrays; uploads on `st`.
+int upload_tree(const HostTree& H, const WsView& V, const Layout& L, cudaStream_t st, bool write_leaves) {
+  int64_t r = H.r;
+  std::vector<uint8_t> depth(r > 0 ? r : 1, 0), ldepth(r, 0);
+  std::vector<int32_t> parent(L.leaf_base + r, -1);
+  std::vector<pos_t> ns(r, 0), ne(r, 0);
+  for (int64_t k = (int64_t)H.order.size() - 1; k >= 0; --k) {  // parents before children
+    uint32_t j = H.order[k];
+    int d = parent[j] < 0 ? 0 : depth[parent[j]] + 1;
+    if (d > 63) return fail(RS_EUNSUPPORTED, "merge tree deeper than 63 levels");
+    depth[j] = (uint8_t)d;
+    ns[j] = H.start[H.na[j]];
+    ne[j] = H.start[H.nb[j] + 1];
+    for (int side = 0; side < 2; ++side) {
+      uint32_t c = H.child[2 * (size_t)j + side];
+      parent[c] = (int32_t)j;
+      if (c >= H.leaf_base) ldepth[c - H.leaf_base] = (uint8_t)(d + 1);
+    }
+  }
+  if (write_leaves) {
+    std::vector<uint32_t> info(r, 1u);  // natural run of length 1: insertion sort from one presorted element
+    RS_CUDA(cudaMemcpyAsync(V.leaf_start, H.start.data(), (r + 1) * sizeof(pos_t), cudaMemcpyHostToDevice, st));
+    RS_CUDA(cudaMemcpyAsync(V.leaf_info, info.data(), r * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+  }
+  RS_CUDA(cudaMemcpyAsync(V.leaf_depth, ldepth.data(), r, cudaMemcpyHostToDevice, st));
+  RS_CUDA(cudaMemcpyAsync(V.depth, depth.data(), r, cudaMemcpyHostToDevice, st));
+  RS_CUDA(cudaMemcpyAsync(V.node_a, H.na.data(), r * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  RS_CUDA(cudaMemcpyAsync(V.node_b, H.nb.data(), r * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  RS_CUDA(cudaMemcpyAsync(V.node_s, ns.data(), r * sizeof(pos_t), cudaMemcpyHostToDevice, st));
+  RS_CUDA(cudaMemcpyAsync(V.node_e, ne.data(), r * sizeof(pos_t), cudaMemcpyHostToDevice, st));
+  RS_CUDA(cudaMemcpyAsync(V.parent, parent.data(), parent.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  RS_CUDA(cudaMemcpyAsync(V.child, H.child.data(), H.child.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+  RS_CUDA(cudaStreamSynchronize(st));  // the host vectors go out of scope
+  return RS_OK;
+}
+
+template <typename K, int TB>
+int run_baseline(int algo, K* keys, void* tags, int64_t n, int w, int classic, double alpha, unsigned char* ws,
+                 const Layout& L, cudaStream_t st) {
+  int sms;
+  if (int e = device_sms(&sms)) return e;
+  WsView V = view(ws, L);
+  HostTree H;
+  H.leaf_base = L.leaf_base;
+  const bool fixed = algo == RS_ALGO_TOP_DOWN || algo == RS_ALGO_BOTTOM_UP;
+  if (fixed) {
+    prof_mark(0, st);
+    prof_set_met(V.met);
+    RS_CUDA(cudaMemsetAsync(V.met, 0, sizeof(DevMetrics), st));
+    RS_CUDA(cudaMemsetAsync(V.done, 0, (2 * L.r_max + 2) * sizeof(uint32_t), st));
+    int64_t nch_max = (L.r_max + kOrdChunkMin - 1) / kOrdChunkMin;
+    RS_CUDA(cudaMemsetAsync(V.chunkdep, 0, (nch_max + 1) * kMaxDepth * sizeof(uint32_t), st));
+    if (algo == RS_ALGO_TOP_DOWN) build_top_down(H, n, w);
+    else build_bottom_up(H, n, w);
+    if (H.r > L.r_max) return fail(RS_EINVARIANT, "baseline tree exceeds the leaf bound");
+    uint64_t r64 = (uint64_t)H.r;
+    RS_CUDA(cudaMemcpyAsync(&V.met->n_leaves, &r64, 8, cudaMemcpyHostToDevice, st));
+    if (int e = upload_tree(H, V, L, st, true)) return e;
+  } else {
+    // runs detected and extended exactly like powersort (sorters.py:595-604)
+    if (int e = run_powersort<K, TB>(keys, tags, n, w, classic, ws, L, st, 1)) return e;
+    DevMetrics hm;
+    RS_CUDA(cudaMemcpyAsync(&hm, V.met, sizeof(DevMetrics), cudaMemcpyDeviceToHost, st));
+    RS_CUDA(cudaStreamSynchronize(st));
+    if (hm.error) return fail(RS_EINVARIANT, "device invariant failure (leaf count exceeded bound)");
+    std::vector<int64_t> starts(hm.n_leaves + 1);
+    RS_CUDA(cudaMemcpyAsync(starts.data(), V.leaf_start, starts.size() * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    RS_CUDA(cudaStreamSynchronize(st));
+    build_alpha(H, starts, alpha, algo == RS_ALGO_ALPHA_MERGE);
+    RS_CUDA(cudaMemcpyAsync(&V.met->max_stack_height, &H.max_stack, 8, cudaMemcpyHostToDevice, st));
+    if (int e = upload_tree(H, V, L, st, false)) return e;
+  }
+  int msuper = merge_super<K, TB>(n, sms);
+  // top-down / bottom-up: no run detection term, merges counted at run time, no
+  // fused subtrees (their merges may be skipped); alpha sorts: powersort's accounting
+  ClassifyArgs CA = classify_args<K, TB>(V, L, n, w, classic, msuper, fixed ? 1 : 0, fixed ? 1 : 0, fixed ? 0 : -1);
+  int64_t nch_max = (L.r_max + kOrdChunkMin - 1) / kOrdChunkMin;
+  (void)nch_max;
+  size_t sm = (size_t)kOrdChunkMax * 9 + 64;
+  static int occ[64] = {0};
+  int dev;
+  RS_CUDA(cudaGetDevice(&dev));
+  if (occ[dev] == 0) {
+    RS_CUDA(cudaFuncSetAttribute(k_tree_tasks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    int o = 0;
+    RS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_tree_tasks, 256, sm));
+    if (o < 1) return fail(RS_ECUDA, "task-list kernel does not fit on an SM");
+    occ[dev] = o;
+  }
+  uint32_t* cd = V.chunkdep;
+  void* kargs[] = {&CA, &cd};
+  RS_CUDA(cudaLaunchCooperativeKernel((void*)k_tree_tasks, dim3(sms * occ[dev]), dim3(256), kargs, sm, st));
+  prof_mark(1, st);
+  return launch_exec<K, TB>(keys, tags, n, w, classic, msuper, V, L, sms, st, fixed ? 1 : 0);
 }
 
 template <typename K, int TB>
@@ -514,7 +733,7 @@ int run_peeksort(K* keys, void* tags, int64_t n, int w, int classic, unsigned ch
 }
 
 int validate(int algo, int key_dtype, int tag_bytes, int64_t n, int32_t w, int32_t merge_kind, int* kb) {
-  if (algo != RS_ALGO_POWERSORT && algo != RS_ALGO_PEEKSORT) return fail(RS_EINVAL, "unknown algorithm");
+  if (algo < RS_ALGO_POWERSORT || algo > RS_ALGO_ALPHA_MERGE) return fail(RS_EINVAL, "unknown algorithm");
   if (key_dtype == RS_KEY_I32) *kb = 4;
   else if (key_dtype == RS_KEY_I64) *kb = 8;
   else return fail(RS_EUNSUPPORTED, "keys must be int32 or int64");
@@ -568,8 +787,13 @@ int export_tree(const Layout& L, unsigned char* ws, cudaStream_t st, rs_tree* tr
 }
 
 template <typename K>
-int dispatch_tags(int algo, K* keys, int tb, void* tags, int64_t n, int w, int classic, unsigned char* ws,
-                  const Layout& L, cudaStream_t st) {
+int dispatch_tags(int algo, K* keys, int tb, void* tags, int64_t n, int w, int classic, double alpha,
+                  unsigned char* ws, const Layout& L, cudaStream_t st) {
+  if (algo >= RS_ALGO_TOP_DOWN) {
+    if (tb == 0) return run_baseline<K, 0>(algo, keys, nullptr, n, w, classic, alpha, ws, L, st);
+    if (tb == 4) return run_baseline<K, 4>(algo, keys, tags, n, w, classic, alpha, ws, L, st);
+    return run_baseline<K, 8>(algo, keys, tags, n, w, classic, alpha, ws, L, st);
+  }
   if (algo == RS_ALGO_PEEKSORT) {
     if (tb == 0) return run_peeksort<K, 0>(keys, nullptr, n, w, classic, ws, L, st);
     if (tb == 4) return run_peeksort<K, 4>(keys, tags, n, w, classic, ws, L, st);
@@ -594,11 +818,23 @@ size_t rs_workspace_bytes(int algo, int key_dtype, int tag_bytes, int64_t n, int
 
 int rs_sort(int algo, int key_dtype, void* keys, int tag_bytes, void* tags, int64_t n, int32_t min_run_len,
             int32_t merge_kind, void* workspace, size_t ws_bytes, void* stream, rs_metrics* out, rs_tree* tree) {
+  return rs_sort_ex(algo, key_dtype, keys, tag_bytes, tags, n, min_run_len, merge_kind, 2.0, workspace, ws_bytes,
+                    stream, out, tree);
+}
+
+int rs_sort_ex(int algo, int key_dtype, void* keys, int tag_bytes, void* tags, int64_t n, int32_t min_run_len,
+               int32_t merge_kind, double alpha, void* workspace, size_t ws_bytes, void* stream, rs_metrics* out,
+               rs_tree* tree) {
   int kb;
   if (int e = validate(algo, key_dtype, tag_bytes, n, min_run_len, merge_kind, &kb)) return e;
+  if (!(alpha > 1.0)) return fail(RS_EINVAL, "alpha must be > 1");
+  if (tree && algo >= RS_ALGO_TOP_DOWN) return fail(RS_EUNSUPPORTED, "the baseline sorters record no merge tree");
   if (tags == nullptr) tag_bytes = 0;
-  if (n <= 1) {  // sorters.py:445-450
-    if (out) { memset(out, 0, sizeof(*out)); out->runs_detected = (uint64_t)n; }
+  if (n <= 1) {  // sorters.py:445-450 (top-down / bottom-up leave the counters alone, :534/:565)
+    if (out) {
+      memset(out, 0, sizeof(*out));
+      out->runs_detected = (algo == RS_ALGO_TOP_DOWN || algo == RS_ALGO_BOTTOM_UP) ? 0 : (uint64_t)n;
+    }
     if (tree) {
       tree->n_leaves = n;
       if (n == 1 && tree->capacity >= 1 && tree->leaf_len) tree->leaf_len[0] = 1;
@@ -612,9 +848,9 @@ int rs_sort(int algo, int key_dtype, void* keys, int tag_bytes, void* tags, int6
   unsigned char* ws = reinterpret_cast<unsigned char*>(workspace);
   int e;
   if (kb == 4) e = dispatch_tags<int32_t>(algo, reinterpret_cast<int32_t*>(keys), tag_bytes, tags, n, min_run_len,
-                                        merge_kind, ws, L, st);
+                                        merge_kind, alpha, ws, L, st);
   else e = dispatch_tags<int64_t>(algo, reinterpret_cast<int64_t*>(keys), tag_bytes, tags, n, min_run_len,
-                                  merge_kind, ws, L, st);
+                                  merge_kind, alpha, ws, L, st);
   if (e) return e;
   if (out || tree) {
     if ((e = read_metrics(L, ws, st, out))) return e;

@@ -235,14 +235,14 @@ def _device_sort(algo: int, a, cfg: SortConfig, metrics: Metrics, tags) -> Metri
     out = _lib.RsMetrics()
     tree = None
     bufs = None
-    if cfg.record_tree and n > 1:
+    if cfg.record_tree and n > 1 and algo in (_lib.RS_ALGO_POWERSORT, _lib.RS_ALGO_PEEKSORT):
         cap = n
         bufs = (np.zeros(cap, dtype=np.int64), np.zeros(cap, dtype=np.uint8), np.zeros(cap, dtype=np.uint8))
         tree = _lib.RsTree(cap, 0, bufs[0].ctypes.data, bufs[1].ctypes.data, bufs[2].ctypes.data)
-    rc = L.rs_sort(algo, keys.code, keys.dev_t.data_ptr(), tb,
-                   tg.dev_t.data_ptr() if tg is not None else None, n, w, kind,
-                   ws.data_ptr(), ws_bytes, keys.stream.cuda_stream, ctypes.byref(out),
-                   ctypes.byref(tree) if tree is not None else None)
+    rc = L.rs_sort_ex(algo, keys.code, keys.dev_t.data_ptr(), tb,
+                      tg.dev_t.data_ptr() if tg is not None else None, n, w, kind, float(cfg.alpha),
+                      ws.data_ptr(), ws_bytes, keys.stream.cuda_stream, ctypes.byref(out),
+                      ctypes.byref(tree) if tree is not None else None)
     _lib.check(rc)
     keys.finish()
     if tg is not None:
@@ -270,9 +270,11 @@ def _entry(algo, a, cfg, metrics, tags):
     cfg = cfg or SortConfig()
     metrics = metrics or Metrics()
     n = len(a)
-    if n <= 1:  # sorters.py:445-450 / :168-173
-        metrics.runs_detected = n
-        if cfg.record_tree and n == 1:
+    if n <= 1:
+        if algo in (_lib.RS_ALGO_TOP_DOWN, _lib.RS_ALGO_BOTTOM_UP):  # sorters.py:533-535, :564-566
+            return metrics
+        metrics.runs_detected = n  # sorters.py:445-450 / :168-173 / :588-590
+        if cfg.record_tree and n == 1 and algo in (_lib.RS_ALGO_POWERSORT, _lib.RS_ALGO_PEEKSORT):
             metrics.merge_tree = MergeLeaf(0, 1)
         return metrics
     return _device_sort(algo, a, cfg, metrics, tags)
@@ -292,7 +294,41 @@ def peeksort(a, cfg: Optional[SortConfig] = None, metrics: Optional[Metrics] = N
     return _entry(_lib.RS_ALGO_PEEKSORT, a, cfg, metrics, tags)
 
 
+def top_down_mergesort(a, cfg: Optional[SortConfig] = None, metrics: Optional[Metrics] = None,
+                       tags=None) -> Metrics:
+    """Plain top-down mergesort: midpoint split, insertion sort below the
+    cutoff, one comparison to skip an in-order merge (reference
+    sorters.py:524-552), executed on the GPU."""
+    return _entry(_lib.RS_ALGO_TOP_DOWN, a, cfg, metrics, tags)
+
+
+def bottom_up_mergesort(a, cfg: Optional[SortConfig] = None, metrics: Optional[Metrics] = None,
+                        tags=None) -> Metrics:
+    """Plain bottom-up mergesort: insertion-sorted chunks of min_run_len, merge
+    passes of doubling width with the same skip check (reference
+    sorters.py:555-581), executed on the GPU."""
+    return _entry(_lib.RS_ALGO_BOTTOM_UP, a, cfg, metrics, tags)
+
+
+def alpha_stack_sort(a, cfg: Optional[SortConfig] = None, metrics: Optional[Metrics] = None,
+                     tags=None) -> Metrics:
+    """Merge the topmost two runs until stack lengths grow by factor alpha
+    (reference sorters.py:638-647), executed on the GPU."""
+    return _entry(_lib.RS_ALGO_ALPHA_STACK, a, cfg, metrics, tags)
+
+
+def alpha_merge_sort(a, cfg: Optional[SortConfig] = None, metrics: Optional[Metrics] = None,
+                     tags=None) -> Metrics:
+    """alpha-stack rule plus pre-merging the stack top up to the new run's
+    length before pushing (reference sorters.py:650-660), executed on the GPU."""
+    return _entry(_lib.RS_ALGO_ALPHA_MERGE, a, cfg, metrics, tags)
+
+
 SORTERS = {
     "peeksort": peeksort,
     "powersort": powersort,
+    "top-down": top_down_mergesort,
+    "bottom-up": bottom_up_mergesort,
+    "alpha-stack": alpha_stack_sort,
+    "alpha-merge": alpha_merge_sort,
 }
