@@ -55,6 +55,8 @@ struct DevMetrics {
   unsigned long long instr[8];  // RS_INSTR builds: cycle counters (see rs_merge.cuh)
   unsigned long long depth_wait[kMaxDepth];  // RS_INSTR: producer dependency-wait cycles per depth
   unsigned long long prep_ts[16];            // RS_INSTR: globaltimer at each prep phase boundary
+  unsigned long long prep_arr[16];           // RS_INSTR: latest block arrival at each prep barrier
+  unsigned long long prep_dbg[32];           // RS_INSTR: finer timestamps inside prep phases
   unsigned int last_ctr[8];                  // 'last block done' counters of the prep kernel
   unsigned long long peek[8];                // peeksort replay counters (frontier sizes, records)
 };
@@ -82,10 +84,14 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 
 #ifdef RS_INSTR
 #define RS_TS(met, i) do { if (blockIdx.x == 0 && threadIdx.x == 0) (met)->prep_ts[i] = globaltimer_ns(); } while (0)
+#define RS_DBG(met, i) do { if (threadIdx.x == 0) atomicMax(&(met)->prep_dbg[i], globaltimer_ns()); } while (0)
+#define RS_ARR(met, i) do { __syncthreads(); if (threadIdx.x == 0) atomicMax(&(met)->prep_arr[i], globaltimer_ns()); } while (0)
 #define RS_T0(v) long long v = clock64()
 #define RS_ACC(met, i, v) atomicAdd(&(met)->instr[i], (unsigned long long)(clock64() - (v)))
 #else
 #define RS_TS(met, i)
+#define RS_ARR(met, i)
+#define RS_DBG(met, i)
 #define RS_T0(v)
 #define RS_ACC(met, i, v)
 #endif

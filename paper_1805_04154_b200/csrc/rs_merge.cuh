@@ -189,6 +189,13 @@ struct PTask {
     if ((threadIdx.x & 31) == 0) t = atomicAdd(&met->task_ctr, 1ull);
     st = 1;
   }
+  // static round robin: this producer's next task index (no atomic, so the
+  // whole fetch chain can run ahead of time)
+  __device__ __forceinline__ void claim_static(unsigned long long& snext, unsigned long long stride) {
+    t = snext;
+    snext += stride;
+    st = 1;
+  }
   template <typename Args>
   __device__ __forceinline__ void advance(const Args& E, unsigned long long ntasks) {
     if (st == 1) {
@@ -284,6 +291,7 @@ __global__ void __launch_bounds__(kMergeThreads, RS_MERGE_CTAS) k_merge_exec(Mer
   }
   __syncthreads();
   unsigned long long ntasks = E.met->n_tasks;
+  const unsigned long long t_first = E.met->task_ctr;  // first merge task (after the phase-A tasks)
 
   if (warp < kProducers) {
     // ------------------------------------------------------------- producer
@@ -302,9 +310,19 @@ __global__ void __launch_bounds__(kMergeThreads, RS_MERGE_CTAS) k_merge_exec(Mer
     // held ahead adds to the waits at level transitions (measured: cfg1-3 6-13%
     // faster just in time, cfg4 (7 tiles/task) 2% faster ahead).  A compile-time
     // choice: a runtime flag costs the just-in-time path its gain.
-    constexpr bool ahead = AHEAD;
+#ifndef RS_STATIC
+#define RS_STATIC 0
+#endif
+    // RS_STATIC: task t goes to producer t mod (grid producers); every wait is
+    // still on a smaller task index, so the resident grid cannot deadlock, and
+    // with no claim atomic the next task's fetch chain runs during the search.
+    constexpr bool kStatic = RS_STATIC != 0;
+    constexpr bool ahead = AHEAD || kStatic;
+    const unsigned long long sstride = (unsigned long long)gridDim.x * kProducers;
+    unsigned long long snext = t_first + (unsigned long long)blockIdx.x * kProducers + (unsigned long long)warp;
     PTask cur, nxt;
-    cur.claim(E.met);
+    if (kStatic) cur.claim_static(snext, sstride);
+    else cur.claim(E.met);
     cur.finish(E, ntasks);
     while (cur.valid) {
       RS_T0(tw);
@@ -316,7 +334,10 @@ __global__ void __launch_bounds__(kMergeThreads, RS_MERGE_CTAS) k_merge_exec(Mer
         } while (!cur.ready(E.done));
       }
       if (lane == 0) RS_ACC(E.met, 5, tw);
-      if (ahead) nxt.claim(E.met);
+      if (ahead) {
+        if (kStatic) nxt.claim_static(snext, sstride);
+        else nxt.claim(E.met);
+      }
       const uint32_t j = cur.j, sk = cur.sk;
       const pos_t s = cur.s, e = cur.e, m = cur.m;
       const int d = cur.d;

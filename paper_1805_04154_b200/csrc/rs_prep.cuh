@@ -56,6 +56,7 @@ __global__ void __launch_bounds__(256, 3) k_prep(PrepArgs P) {
   // 1. pair-type bits + candidate tables (sorters.py:462-470, runcore.py:137-159)
   const K* a = reinterpret_cast<const K*>(P.keys);
   d_scan_tables_tma<K>(a, P.n, P.w, P.ascw, P.tables, P.ntiles, met);
+  RS_ARR(met, 1);
   grid.sync();
   RS_TS(met, 1);
 #ifdef RS_INSTR
@@ -69,6 +70,7 @@ __global__ void __launch_bounds__(256, 3) k_prep(PrepArgs P) {
   if (last_block_done(&met->last_ctr[0]))
     d_group_entries(P.gtab, P.ngroups, P.w, P.gbatch, P.gentry, P.goff, const_cast<pos_t*>(P.T.leaf_start), P.n,
                     P.r_max, met);
+  RS_ARR(met, 2);
   grid.sync();
   RS_TS(met, 2);
   // 3. tile entries
@@ -76,6 +78,7 @@ __global__ void __launch_bounds__(256, 3) k_prep(PrepArgs P) {
     d_tile_entries(P.tables, P.ntiles, P.w, P.tbatch, P.gentry, P.goff, P.tentry, P.toff, g);
     __syncthreads();
   }
+  RS_ARR(met, 3);
   grid.sync();
   RS_TS(met, 3);
   // 4. emit leaves, one warp per chain tile
@@ -85,6 +88,7 @@ __global__ void __launch_bounds__(256, 3) k_prep(PrepArgs P) {
       d_emit_tile(P.ascw, P.n, P.w, P.tentry, P.toff, P.r_max, const_cast<pos_t*>(P.T.leaf_start),
                   const_cast<uint32_t*>(P.T.leaf_info), t);
   }
+  RS_ARR(met, 4);
   grid.sync();
   RS_TS(met, 4);
   if (P.leaves_only) return;
@@ -101,14 +105,17 @@ __global__ void __launch_bounds__(256, 3) k_prep(PrepArgs P) {
     d_scan_top(met, P.agg, P.nchunks, 0);
     d_scan_top(met, P.agg, P.nchunks, 1);
   }
+  RS_ARR(met, 5);
   grid.sync();
   RS_TS(met, 5);
   // 6. depths, max stack height (sorters.py:500-502)
   d_scan_down(P.T.P, met, P.agg, P.nchunks, const_cast<uint8_t*>(P.T.la), const_cast<uint8_t*>(P.T.ra));
+  RS_ARR(met, 6);
   grid.sync();
   RS_TS(met, 6);
   // 7. trie ranges, parents, children, spans
   d_tree(P.T, P.F, met);
+  RS_ARR(met, 7);
   grid.sync();
   RS_TS(met, 7);
   // 8. classification + Metrics closed forms; the last block lays out depths
@@ -118,16 +125,20 @@ __global__ void __launch_bounds__(256, 3) k_prep(PrepArgs P) {
     __syncthreads();
     d_order_scan(met, P.chunkdep);
   }
+  RS_ARR(met, 8);
   grid.sync();
   RS_TS(met, 8);
   // 9. task records
   d_task_fill(P.CA, P.chunkdep);
+  RS_ARR(met, 9);
   grid.sync();
   RS_TS(met, 9);
 #ifdef RS_INSTR
   // calibration: the cost of a bare grid barrier
+  RS_ARR(met, 10);
   grid.sync();
   RS_TS(met, 10);
+  RS_ARR(met, 11);
   grid.sync();
   RS_TS(met, 11);
 #endif

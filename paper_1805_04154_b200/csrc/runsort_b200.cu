@@ -464,6 +464,10 @@ int run_powersort(K* keys, void* tags, int64_t n, int w, int classic, unsigned c
   if (int e = prep_grid<K>(sms, sm, &grid_p)) return e;
   void* kargs[] = {&PA};
   RS_CUDA(cudaLaunchCooperativeKernel((void*)k_prep<K>, dim3(grid_p), dim3(256), kargs, sm, st));
+#ifdef RS_INSTR
+  if (getenv("RS_PREP_TWICE"))  // experiment: a second, warm-code prep (idempotent)
+    RS_CUDA(cudaLaunchCooperativeKernel((void*)k_prep<K>, dim3(grid_p), dim3(256), kargs, sm, st));
+#endif
   if (leaves_only) return RS_OK;
   prof_mark(1, st);
   return launch_exec<K, TB>(keys, tags, n, w, classic, msuper, V, L, sms, st);
@@ -928,6 +932,8 @@ int rs_debug_counters(int key_dtype, int tag_bytes, int64_t n, int32_t min_run_l
   for (int d = 0; d < kMaxDepth && k < cap; ++d) out[k++] = hm.depth_wait[d];
   for (int d = 0; d < kMaxDepth && k < cap; ++d) out[k++] = hm.depth_tiles[d];
   for (int d = 0; d < 16 && k < cap; ++d) out[k++] = hm.prep_ts[d];
+  for (int d = 0; d < 16 && k < cap; ++d) out[k++] = hm.prep_arr[d];
+  for (int d = 0; d < 32 && k < cap; ++d) out[k++] = hm.prep_dbg[d];
   return k;
 }
 

@@ -1,0 +1,19 @@
+#!/bin/bash
+# A/B device timing of library variants: tools/ab.sh "cfgs" variant...   (variant "main" = default lib)
+# prints ms/step and per-phase ms of bench.py for each (variant, config); repeats each pair twice.
+cfgs=$1; shift
+mkdir -p gpurun_out/ab
+for rep in 1 2; do
+for v in "$@"; do
+  if [ "$v" = main ]; then lib=$PWD/paper_1805_04154_b200/librunsort_b200.so; else lib=$PWD/paper_1805_04154_b200/librunsort_b200_$v.so; fi
+  for c in $cfgs; do
+    RS_LIB=$lib timeout 300 python bench.py --config $c --steps 20 --warmup 3 --no-cpu-baseline > gpurun_out/ab/${v}_$c.json 2> gpurun_out/ab/${v}_$c.err || { echo "$v cfg$c FAILED"; tail -3 gpurun_out/ab/${v}_$c.err; continue; }
+    python - "$v" "$c" <<'PY'
+import json, sys
+v, c = sys.argv[1], sys.argv[2]
+d = json.load(open(f"gpurun_out/ab/{v}_{c}.json"))
+print(f"{v:10s} cfg{c} {d['ms_per_step']:.4f} ms", {k: round(x, 4) for k, x in d.get("phase_ms", {}).items()}, "sorted" if d.get("sorted_ok") else "UNSORTED", flush=True)
+PY
+  done
+done
+done
