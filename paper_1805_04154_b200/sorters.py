@@ -239,14 +239,22 @@ def _device_sort(algo: int, a, cfg: SortConfig, metrics: Metrics, tags) -> Metri
         cap = n
         bufs = (np.zeros(cap, dtype=np.int64), np.zeros(cap, dtype=np.uint8), np.zeros(cap, dtype=np.uint8))
         tree = _lib.RsTree(cap, 0, bufs[0].ctypes.data, bufs[1].ctypes.data, bufs[2].ctypes.data)
+    # Without a tree export the sort is enqueued without a host sync, the
+    # write-back (D2H for host inputs) is queued behind it on the same stream,
+    # and one synchronizing Metrics fetch ends the call: no bubble between the
+    # last kernel and the copy back.
     rc = L.rs_sort_ex(algo, keys.code, keys.dev_t.data_ptr(), tb,
                       tg.dev_t.data_ptr() if tg is not None else None, n, w, kind, float(cfg.alpha),
-                      ws.data_ptr(), ws_bytes, keys.stream.cuda_stream, ctypes.byref(out),
+                      ws.data_ptr(), ws_bytes, keys.stream.cuda_stream,
+                      ctypes.byref(out) if tree is not None else None,
                       ctypes.byref(tree) if tree is not None else None)
     _lib.check(rc)
     keys.finish()
     if tg is not None:
         tg.finish()
+    if tree is None:
+        _lib.check(L.rs_fetch_metrics(algo, keys.code, tb, n, w, ws.data_ptr(), keys.stream.cuda_stream,
+                                      ctypes.byref(out)))
     if keys.is_torch and keys.obj.device.type == "cpu":
         keys.stream.synchronize()
     metrics.merge_cost += int(out.merge_cost)
