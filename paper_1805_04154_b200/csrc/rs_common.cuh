@@ -30,6 +30,21 @@ __host__ __device__ inline uint32_t task_kind(uint64_t t) { return uint32_t(t >>
 __host__ __device__ inline uint32_t task_tile(uint64_t t) { return uint32_t(t >> 32) & 0x3fffffffu; }
 __host__ __device__ inline uint32_t task_id(uint64_t t) { return uint32_t(t); }
 
+// Merge-task descriptor (48 B, one per merge task, written by the task fill
+// next to its record): everything the merge producer needs after its claim in
+// one round trip -- node span and split, children, their completion counts
+// and buffers -- instead of a chain of dependent lookups.
+struct __align__(16) MDesc {
+  pos_t s, m, e;      // node span [s, e), children split at m
+  uint32_t c0, c1;    // unified child ids
+  uint32_t nd0, nd1;  // children's completion counts (need)
+  uint32_t j;         // node id
+  uint16_t sk;        // task index within the node
+  uint8_t d;          // node depth
+  uint8_t cl;         // bit 0 / 1: child 0 / 1 is a merge node (class 2)
+};
+static_assert(sizeof(MDesc) == 48, "MDesc layout");
+
 // Leaf modes for big (non-fused) leaves.
 enum LeafMode : int { kLeafNone = 0, kLeafSwap = 1, kLeafRevCopy = 2, kLeafCopy = 3 };
 

@@ -107,7 +107,40 @@ struct ClassifyArgs {
   const int32_t* node_b;
   int maxb;      // ExecArgs::maxb
   int fuse_avg;  // fused subtrees: average leaf length below this
+  const uint32_t* child;
+  MDesc* mdesc;  // per merge task, same index as tasks[]
 };
+
+// Merge descriptor of node i (two dependent round trips: the node's fields,
+// then its children's counts and classes).
+__device__ __forceinline__ MDesc load_mdesc(const ClassifyArgs& A, uint32_t i) {
+  MDesc md;
+  md.s = A.node_s[i];
+  md.e = A.node_e[i];
+  md.m = A.leaf_start[i];
+  md.c0 = A.child[2 * i];
+  md.c1 = A.child[2 * i + 1];
+  md.d = A.depth[i];
+  md.nd0 = A.need[md.c0];
+  md.nd1 = A.need[md.c1];
+  uint8_t cl0 = md.c0 < A.leaf_base ? A.cls[md.c0] : 0, cl1 = md.c1 < A.leaf_base ? A.cls[md.c1] : 0;
+  md.cl = (uint8_t)((cl0 == 2 ? 1 : 0) | (cl1 == 2 ? 2 : 0));
+  md.j = i;
+  md.sk = 0;
+  return md;
+}
+
+
+// Task record + descriptor of the k-th task of the node described by md.
+__device__ __forceinline__ void store_merge_task(const ClassifyArgs& A, uint32_t t, MDesc md, uint32_t k) {
+  A.tasks[t] = make_task(kTaskMerge, k, md.j);
+  md.sk = (uint16_t)k;
+  const uint4* src = reinterpret_cast<const uint4*>(&md);
+  uint4* d = reinterpret_cast<uint4*>(A.mdesc + t);
+  d[0] = src[0];
+  d[1] = src[1];
+  d[2] = src[2];
+}
 
 // Node j can run as (part of) one fused phase-A task: its span fits the fused
 // capacity and its internal nodes fit the task's node table (both monotone, so
@@ -157,6 +190,9 @@ __device__ __forceinline__ int classify_node(const ClassifyArgs& A, int64_t j, i
 // ordered by depth (deepest first) and, within a depth, by position, so a
 // node's tasks are claimed after the wave of its children's tasks has passed.
 constexpr int kOrdChunkMin = 256, kOrdChunkMax = 4096;
+// d_task_fill's shared-memory staging: slots, tile counts, depths, then one round of merge descriptors
+constexpr int kFillMdOff = (kOrdChunkMax * 9 + 15) / 16 * 16;
+constexpr int kFillSmem = kFillMdOff + 256 * 48;
 // Chunk of boundaries for the ordered fill: small trees -> many small chunks.
 __host__ __device__ inline int64_t ord_chunk(int64_t r) {
   int64_t c = kOrdChunkMin;
@@ -376,14 +412,23 @@ __device__ void d_task_fill(ClassifyArgs A, const uint32_t* __restrict__ chunk_d
       if (d != 255) s_slot[x] = s_wsum[d * 8 + wid] + pre;
       __syncthreads();
     }
-    // one warp per big node writes its task records
+    // rounds of blockDim nodes: every thread loads one node's merge descriptor
+    // into shared memory (parallel round trips), then one warp per node writes
+    // its task records and per-task descriptors
+    MDesc* s_md = reinterpret_cast<MDesc*>(smem_fill + kFillMdOff);
     int wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (int64_t x = wid; x < cnt_i; x += nw) {
-      if (s_dep[x] == 255) continue;
-      int64_t i = i0 + x;
-      uint32_t tk = s_tk[x];
-      uint32_t slot = s_slot[x];
-      for (uint32_t k = lane; k < tk; k += 32) A.tasks[slot + k] = make_task(kTaskMerge, k, (uint32_t)i);
+    for (int64_t g = 0; g < cnt_i; g += blockDim.x) {
+      int64_t x = g + threadIdx.x;
+      if (x < cnt_i && s_dep[x] != 255) s_md[threadIdx.x] = load_mdesc(A, (uint32_t)(i0 + x));
+      __syncthreads();
+      int64_t ny = cnt_i - g < (int64_t)blockDim.x ? cnt_i - g : (int64_t)blockDim.x;
+      for (int64_t y = wid; y < ny; y += nw) {
+        if (s_dep[g + y] == 255) continue;
+        uint32_t tk = s_tk[g + y], slot = s_slot[g + y];
+        const MDesc md = s_md[y];
+        for (uint32_t k = lane; k < tk; k += 32) store_merge_task(A, slot + k, md, k);
+      }
+      __syncthreads();
     }
   }
 }

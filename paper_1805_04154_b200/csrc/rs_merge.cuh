@@ -25,6 +25,9 @@
 
 namespace rs {
 
+#ifndef RS_MDESC
+#define RS_MDESC 1
+#endif
 constexpr int kSuperMax = 15;          // tiles per merge task: runtime, <= 15 (lane groups of >= 2)
 #ifndef RS_STAGES
 #define RS_STAGES 2
@@ -92,6 +95,7 @@ struct MergeArgs {
   const uint32_t* need;
   uint32_t* done;
   const uint64_t* tasks;
+  const MDesc* mdesc;  // per merge task (RS_MDESC)
   DevMetrics* met;
   const uint8_t* cls;  // unified id -> class (2 = merge node for internal ids)
   uint32_t leaf_base;
@@ -201,9 +205,29 @@ struct PTask {
     if (st == 1) {
       t = __shfl_sync(0xffffffffu, t, 0);
       valid = t < ntasks;
+#if RS_MDESC
+      // one 48-byte descriptor instead of the record -> node -> children chain
+      if (valid) {
+        const MDesc md = E.mdesc[t];
+        j = md.j;
+        sk = md.sk;
+        s = md.s;
+        m = md.m;
+        e = md.e;
+        c0 = md.c0;
+        c1 = md.c1;
+        nd0 = md.nd0;
+        nd1 = md.nd1;
+        d = md.d;
+        cl0 = (md.cl & 1) ? 2 : 0;
+        cl1 = (md.cl & 2) ? 2 : 0;
+      }
+      st = 3;  // next: the children's counters
+#else
       uint64_t rec = valid ? E.tasks[t] : 0ull;
       j = task_id(rec);
       sk = task_tile(rec);
+#endif
     } else if (st == 2) {
       if (valid) {
         c0 = E.child[2 * j];

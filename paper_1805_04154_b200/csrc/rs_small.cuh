@@ -17,12 +17,14 @@ namespace rs {
 
 constexpr int kSmallR = 2048;  // above this the grid-wide phases of k_prep are faster
 
-__host__ __device__ constexpr size_t small_smem_bytes() {
+__host__ __device__ constexpr size_t small_arrays_bytes() {
   return (size_t)(kSmallR + 1) * 8      // Ls: leaf starts
          + (size_t)kSmallR * 8          // Ks: midpoint keys, later node spans
          + (size_t)2 * kSmallR * 4      // par: parents of leaves [0, r) and nodes [r, 2r)
          + (size_t)(kSmallR + 1) * 5;   // Ps, las, ras, dep, ldep
 }
+constexpr size_t kSmallMdOff = (small_arrays_bytes() + 15) / 16 * 16;  // + one round of merge descriptors
+__host__ __device__ constexpr size_t small_smem_bytes() { return kSmallMdOff + 256 * 48; }
 
 // Run by one CTA of NT threads (block 0 of k_prep after its leaf phase);
 // smem_small: small_smem_bytes() of dynamic shared memory.
@@ -293,10 +295,24 @@ __device__ void small_tree(const TreeArrays& T, ClassifyArgs A, int F, unsigned 
   auto drain = [&]() {
     __syncthreads();
     uint32_t nj = s_nj;
-    for (uint32_t e = wid; e < nj; e += nw) {
-      uint32_t slot = jslot[e], id = jid[e], c = jcnt[e];
-      uint32_t kind = c >> 30, cnt = c & 0x3fffffffu;
-      for (uint32_t k = lane; k < cnt; k += 32) A.tasks[slot + k] = make_task(kind, kind == kTaskFuse ? 0 : k, id);
+    MDesc* s_md = reinterpret_cast<MDesc*>(smem_small + kSmallMdOff);
+    for (uint32_t g = 0; g < nj; g += nt) {
+      // merge descriptors of this round's jobs: one thread per job, parallel round trips
+      uint32_t e = g + tid;
+      if (e < nj && (jcnt[e] >> 30) == kTaskMerge) s_md[tid] = load_mdesc(A, jid[e]);
+      __syncthreads();
+      uint32_t ny = nj - g < (uint32_t)nt ? nj - g : (uint32_t)nt;
+      for (uint32_t y = wid; y < ny; y += nw) {
+        uint32_t slot = jslot[g + y], id = jid[g + y], c = jcnt[g + y];
+        uint32_t kind = c >> 30, cnt = c & 0x3fffffffu;
+        if (kind == kTaskMerge) {
+          const MDesc md = s_md[y];
+          for (uint32_t k = lane; k < cnt; k += 32) store_merge_task(A, slot + k, md, k);
+        } else {
+          for (uint32_t k = lane; k < cnt; k += 32) A.tasks[slot + k] = make_task(kind, kind == kTaskFuse ? 0 : k, id);
+        }
+      }
+      __syncthreads();
     }
     __syncthreads();
     if (tid == 0) s_nj = 0;

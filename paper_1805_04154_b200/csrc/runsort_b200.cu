@@ -84,7 +84,7 @@ struct Layout {
   size_t o_key1, o_tag1, o_key2, o_tag2, o_ascw, o_tables, o_gtab, o_gentry, o_goff, o_tentry, o_toff;
   size_t o_leaf_start, o_leaf_info, o_leaf_depth, o_K, o_P, o_la, o_ra, o_depth;
   size_t o_node_a, o_node_b, o_node_s, o_node_e, o_parent, o_child, o_need, o_done;
-  size_t o_agg, o_tasks, o_chunkdep, o_cls, o_met, total;
+  size_t o_agg, o_tasks, o_mdesc, o_chunkdep, o_cls, o_met, total;
   // peeksort replay
   int algo;
   int64_t front_cap, rec_cap, sum_words, wchunks;
@@ -159,6 +159,7 @@ Layout make_layout(int64_t n, int w, int kb, int tb, int algo) {
   L.o_done = take((size_t)(2 * L.r_max + 2) * 4);
   L.o_agg = take((size_t)2 * L.nchunks * sizeof(MC));
   L.o_tasks = take((size_t)L.max_tasks * 8);
+  L.o_mdesc = take((size_t)L.max_tasks * sizeof(MDesc));
   L.o_chunkdep = take((size_t)((L.r_max + kOrdChunkMin - 1) / kOrdChunkMin + 1) * kMaxDepth * 4);
   L.o_cls = take((size_t)(2 * L.r_max + 2));
   if (pk) {
@@ -270,6 +271,7 @@ struct WsView {
   uint32_t *ascw, *gentry, *tentry, *need, *done, *child, *chunkdep;
   uint2 *tables, *gtab;
   uint64_t *goff, *toff, *Kk, *tasks;
+  MDesc* mdesc;
   pos_t *leaf_start, *node_s, *node_e;
   uint32_t* leaf_info;
   uint8_t *leaf_depth, *P, *la, *ra, *depth, *cls;
@@ -310,6 +312,7 @@ WsView view(unsigned char* ws, const Layout& L) {
   V.done = reinterpret_cast<uint32_t*>(at(L.o_done));
   V.agg = reinterpret_cast<MC*>(at(L.o_agg));
   V.tasks = reinterpret_cast<uint64_t*>(at(L.o_tasks));
+  V.mdesc = reinterpret_cast<MDesc*>(at(L.o_mdesc));
   V.chunkdep = reinterpret_cast<uint32_t*>(at(L.o_chunkdep));
   V.cls = reinterpret_cast<uint8_t*>(at(L.o_cls));
   V.key1 = at(L.o_key1);
@@ -338,7 +341,8 @@ ClassifyArgs classify_args(const WsView& V, const Layout& L, int64_t n, int w, i
   return ClassifyArgs{n, w, classic, fcap >= 0 ? fcap : L.fcap, L.tile, MergeCfg<K, TB>::TILE, msuper, peek,
                       runtime_merges, L.leaf_base,
                       V.leaf_start, V.leaf_info, V.leaf_depth, V.depth, V.node_s, V.node_e, V.parent, V.need,
-                      V.cls, V.tasks, V.met, V.node_a, V.node_b, Exec<K, TB>::maxb_for(w), fuse_avg()};
+                      V.cls, V.tasks, V.met, V.node_a, V.node_b, Exec<K, TB>::maxb_for(w), fuse_avg(), V.child,
+                      V.mdesc};
 }
 
 // Phase A (fused subtrees, large leaves) + the merge executor.
@@ -397,6 +401,7 @@ int launch_exec(K* keys, void* tags, int64_t n, int w, int classic, int msuper, 
   M.need = V.need;
   M.done = V.done;
   M.tasks = V.tasks;
+  M.mdesc = V.mdesc;
   M.met = V.met;
   if (msuper > 1) k_merge_exec<K, TB, true><<<grid_m, kMergeThreads, smem_m, st>>>(M);
   else k_merge_exec<K, TB, false><<<grid_m, kMergeThreads, smem_m, st>>>(M);
@@ -424,7 +429,7 @@ int run_powersort(K* keys, void* tags, int64_t n, int w, int classic, unsigned c
   if (gbatch < 1) gbatch = 1;
   int tbatch = gbatch < kChainGroup ? gbatch : kChainGroup;
   size_t sm = 8 * (size_t)chain_warp_bytes(w, sizeof(K));
-  sm = std::max(sm, (size_t)kOrdChunkMax * 9 + 64);
+  sm = std::max(sm, (size_t)kFillSmem + 64);
   sm = std::max(sm, (size_t)batch * W1 * 8 + (size_t)W1 * 8 + 64);
   sm = std::max(sm, (size_t)gbatch * W1 * 8);
   sm = std::max(sm, (size_t)tbatch * W1 * 8);
@@ -665,7 +670,7 @@ int run_baseline(int algo, K* keys, void* tags, int64_t n, int w, int classic, d
   ClassifyArgs CA = classify_args<K, TB>(V, L, n, w, classic, msuper, fixed ? 1 : 0, fixed ? 1 : 0, fixed ? 0 : -1);
   int64_t nch_max = (L.r_max + kOrdChunkMin - 1) / kOrdChunkMin;
   (void)nch_max;
-  size_t sm = (size_t)kOrdChunkMax * 9 + 64;
+  size_t sm = (size_t)kFillSmem + 64;
   static int occ[64] = {0};
   int dev;
   RS_CUDA(cudaGetDevice(&dev));
@@ -720,11 +725,12 @@ int run_peeksort(K* keys, void* tags, int64_t n, int w, int classic, unsigned ch
   PK.chunkdep_words = (nch_max + 1) * kMaxDepth;
   PK.done = V.done;
   PK.done_words = 2 * L.r_max + 2;
-  size_t sm = (size_t)kOrdChunkMax * 9 + 64;
+  size_t sm = (size_t)kFillSmem + 64;
   static int occ[64] = {0};
   int dev;
   RS_CUDA(cudaGetDevice(&dev));
   if (occ[dev] == 0) {
+    RS_CUDA(cudaFuncSetAttribute(k_peek<K, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     int o = 0;
     RS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_peek<K, TB>, 256, sm));
     if (o < 1) return fail(RS_ECUDA, "peeksort kernel does not fit on an SM");
