@@ -162,6 +162,9 @@ __host__ __device__ inline int chain_warp_bytes(int w, int kb) {
   return chain_win_bytes(w, kb) + ((maxw * 8 + maxw * 2 + 127) / 128) * 128;
 }
 
+#ifndef RS_BITS_LPW
+#define RS_BITS_LPW 1
+#endif
 template <typename K>
 __device__ void d_scan_tables_tma(const K* __restrict__ a, pos_t n, int w, uint32_t* __restrict__ ascw,
                                   uint2* __restrict__ tables, int64_t ntiles, DevMetrics* imet = nullptr) {
@@ -208,6 +211,30 @@ __device__ void d_scan_tables_tma(const K* __restrict__ a, pos_t n, int w, uint3
 #endif
     const K* sk = reinterpret_cast<const K*>(kbuf) + koff;  // element 32*q0
     int64_t own0 = t0 >> 5, own1 = (t1 + 31) >> 5;
+#if RS_BITS_LPW
+    // one pair-type word per lane: lane l builds word wb+l from its 33 keys,
+    // visiting them in the rotated order j = (l + k) mod 32 so the 32 lanes
+    // hit 32 different banks; no shuffles, 32 independent compares per lane
+    for (int wb = 0; wb < nwords; wb += 32) {
+      const int wi = wb + lane;
+      if (wi < nwords) {
+        const K* p = sk + 32 * wi;
+        const pos_t p0 = 32 * (q0 + wi);
+        uint32_t w4[4] = {0u, 0u, 0u, 0u};  // independent accumulators: no 32-long OR chain
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          const int j = (lane + k) & 31;
+          w4[k & 3] |= (uint32_t)(p[j] <= p[j + 1]) << j;
+        }
+        uint32_t word = (w4[0] | w4[1]) | (w4[2] | w4[3]);
+        const pos_t rem = (n - 1) - p0;  // pairs p0 + j with j < rem lie before n - 1
+        if (rem < 32) word &= rem <= 0 ? 0u : ((1u << rem) - 1u);
+        asc[wi] = word;
+        const int64_t q = q0 + wi;
+        if (q >= own0 && q < own1) ascw[q] = word;
+      }
+    }
+#else
     constexpr int VEC = 16 / sizeof(K);  // elements per 16B lane load = words per warp load
     constexpr int LPW = 32 / VEC;        // lanes per word
     if (koff % VEC == 0) {
@@ -220,13 +247,15 @@ __device__ void d_scan_tables_tma(const K* __restrict__ a, pos_t n, int w, uint3
         K first = x[0];
         K nxt = __shfl_down_sync(0xffffffffu, first, 1);
         if (lane == 31) nxt = sk[32 * vb + 32 * VEC];
-        pos_t k0 = 32 * (q0 + vb) + (pos_t)lane * VEC;
+        // pairs k0 + i (i < lim) lie before n - 1: one 64-bit clamp instead of VEC compares
+        pos_t rem = (n - 1) - (32 * (q0 + vb) + (pos_t)lane * VEC);
+        int lim = rem <= 0 ? 0 : (rem >= VEC ? VEC : (int)rem);
         uint32_t nib = 0;
 #pragma unroll
         for (int i = 0; i < VEC; ++i) {
           K cur = x[i];
           K nx = i + 1 < VEC ? x[i + 1] : nxt;
-          if (k0 + i < n - 1 && cur <= nx) nib |= 1u << i;
+          nib |= (uint32_t)(i < lim && cur <= nx) << i;
         }
         uint32_t word = nib << ((lane % LPW) * VEC);
 #pragma unroll
@@ -251,6 +280,7 @@ __device__ void d_scan_tables_tma(const K* __restrict__ a, pos_t n, int w, uint3
         if (q >= own0 && q < own1) ascw[q] = word;
       }
     }
+#endif
     __syncwarp();
 #ifdef RS_INSTR
     unsigned long long c2 = clock64();
