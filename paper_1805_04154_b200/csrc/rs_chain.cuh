@@ -185,7 +185,27 @@ __device__ void d_scan_tables_tma(const K* __restrict__ a, pos_t n, int w, uint3
 #ifdef RS_INSTR
   unsigned long long c_wait = 0, c_bits = 0, c_bw = 0, c_walk = 0;
 #endif
-  for (int64_t tile = (int64_t)blockIdx.x * nw + wid; tile < ntiles; tile += (int64_t)gridDim.x * nw) {
+  // The key window is only read by the pair-bit step: the next tile's bulk
+  // copy is issued right after it, overlapping the B-words and the walks.
+  auto issue = [&](int64_t tl) -> int32_t {
+    pos_t u0, u1;
+    int64_t r0, r1;
+    chain_window(tl, n, w, &r0, &r1, &u0, &u1);
+    pos_t e0 = 32 * r0, e1 = 32 * r1 + 1 < n ? 32 * r1 + 1 : n;
+    int32_t ko = 0;
+    if (lane == 0) {
+      uintptr_t a0 = reinterpret_cast<uintptr_t>(a + e0), a1 = reinterpret_cast<uintptr_t>(a + e1);
+      uint32_t bytes = (uint32_t)(((a1 + 15) & ~(uintptr_t)15) - (a0 & ~(uintptr_t)15));
+      fence_proxy_async_smem();
+      mbar_arrive_tx(&kbar[wid], bytes);
+      tma_window(kbuf, a, e0, e1, sizeof(K), &kbar[wid], &ko);
+    }
+    return __shfl_sync(0xffffffffu, ko, 0);
+  };
+  const int64_t tstride = (int64_t)gridDim.x * nw;
+  int32_t koff_next = 0;
+  if ((int64_t)blockIdx.x * nw + wid < ntiles) koff_next = issue((int64_t)blockIdx.x * nw + wid);
+  for (int64_t tile = (int64_t)blockIdx.x * nw + wid; tile < ntiles; tile += tstride) {
 #ifdef RS_INSTR
     unsigned long long c0 = clock64();
 #endif
@@ -193,16 +213,7 @@ __device__ void d_scan_tables_tma(const K* __restrict__ a, pos_t n, int w, uint3
     int64_t q0, q1;
     chain_window(tile, n, w, &q0, &q1, &t0, &t1);
     int nwords = int(q1 - q0);
-    pos_t e0 = 32 * q0, e1 = 32 * q1 + 1 < n ? 32 * q1 + 1 : n;
-    int32_t koff = 0;
-    if (lane == 0) {
-      uintptr_t a0 = reinterpret_cast<uintptr_t>(a + e0), a1 = reinterpret_cast<uintptr_t>(a + e1);
-      uint32_t bytes = (uint32_t)(((a1 + 15) & ~(uintptr_t)15) - (a0 & ~(uintptr_t)15));
-      fence_proxy_async_smem();
-      mbar_arrive_tx(&kbar[wid], bytes);
-      tma_window(kbuf, a, e0, e1, sizeof(K), &kbar[wid], &koff);
-    }
-    koff = __shfl_sync(0xffffffffu, koff, 0);
+    const int32_t koff = koff_next;
     mbar_wait(&kbar[wid], ph);
     ph ^= 1u;
 #ifdef RS_INSTR
@@ -282,6 +293,7 @@ __device__ void d_scan_tables_tma(const K* __restrict__ a, pos_t n, int w, uint3
     }
 #endif
     __syncwarp();
+    if (tile + tstride < ntiles) koff_next = issue(tile + tstride);  // the window has been read
 #ifdef RS_INSTR
     unsigned long long c2 = clock64();
     c_bits += c2 - c1;
