@@ -111,6 +111,14 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 #define RS_ACC(met, i, v)
 #endif
 
+// Out-of-line 64-bit divisions: the inline expansion is ~70 instructions per
+// call site, and the prep's phases run once per sort from a cold instruction
+// cache -- code bytes are latency there.
+__device__ __noinline__ uint64_t udiv64(uint64_t a, uint64_t b) { return a / b; }
+__device__ __forceinline__ int64_t ceil_div64(int64_t a, int64_t b) {
+  return (int64_t)udiv64((uint64_t)(a + b - 1), (uint64_t)b);
+}
+
 __device__ __forceinline__ int bitlen64(uint64_t x) { return x ? 64 - __clzll((long long)x) : 0; }
 
 template <typename T>

@@ -75,9 +75,9 @@ __device__ __forceinline__ int64_t leaf_tiles(pos_t len, int mode, int tile) {
   if (mode == kLeafNone) return 0;
   if (mode == kLeafSwap) {
     int64_t half = tile / 2;
-    return ((len / 2) + half - 1) / half;
+    return ceil_div64(len / 2, half);
   }
-  return (len + tile - 1) / tile;
+  return ceil_div64(len, tile);
 }
 
 // ---------------------------------------------------------------- T4: tasks
@@ -181,8 +181,8 @@ __device__ __forceinline__ int classify_node(const ClassifyArgs& A, int64_t j, i
   *tiles = 0;
   *tasks = 0;
   if (fusable(A, (int32_t)j)) return parent_small(A, A.parent[j]) ? 0 : 1;
-  *tiles = (span + A.mtile - 1) / A.mtile;
-  *tasks = (*tiles + A.msuper - 1) / A.msuper;
+  *tiles = ceil_div64(span, A.mtile);
+  *tasks = ceil_div64(*tiles, A.msuper);
   return 2;
 }
 
@@ -371,7 +371,7 @@ __device__ void d_task_fill(ClassifyArgs A, const uint32_t* __restrict__ chunk_d
         uint32_t dd = A.depth[i], nd = A.need[i];
         if (c == 2) {
           dv = dd;
-          tv = (nd + A.msuper - 1) / A.msuper;
+          tv = (nd + A.msuper - 1) / (uint32_t)A.msuper;
         }
       }
       s_dep[x] = (uint8_t)dv;

@@ -15,6 +15,13 @@
 
 namespace rs {
 
+// Per-item loops stay rolled (per-item state in local memory): the block runs
+// this code once per sort from a cold instruction cache, so code bytes cost
+// more than the extra local-memory traffic.
+#ifndef RS_SMALL_UNROLL_N
+#define RS_SMALL_UNROLL_N 1
+#endif
+constexpr int kSmallUnroll = RS_SMALL_UNROLL_N;
 constexpr int kSmallR = 2048;  // above this the grid-wide phases of k_prep are faster
 
 __host__ __device__ constexpr size_t small_arrays_bytes() {
@@ -118,7 +125,7 @@ __device__ void small_tree(const TreeArrays& T, ClassifyArgs A, int F, unsigned 
   RS_TS(met, 6);
   // ---- trie ranges, parents, children, spans (d_tree)
   pos_t myspan[kSmallPer];
-#pragma unroll
+#pragma unroll kSmallUnroll
   for (int q = 0; q < kSmallPer; ++q) {
     int64_t i = tid + (int64_t)q * nt;
     myspan[q] = 0;
@@ -194,7 +201,7 @@ __device__ void small_tree(const TreeArrays& T, ClassifyArgs A, int F, unsigned 
     }
   }
   __syncthreads();  // Ks dead from here: spans reuse it
-#pragma unroll
+#pragma unroll kSmallUnroll
   for (int q = 0; q < kSmallPer; ++q) {
     int64_t i = tid + (int64_t)q * nt;
     if (i < r) spans[i] = myspan[q];
@@ -213,7 +220,7 @@ __device__ void small_tree(const TreeArrays& T, ClassifyArgs A, int F, unsigned 
   uint32_t tk_of[kSmallPer];   // merge tasks of node i0+q (0 unless big)
   uint32_t a_of[kSmallPer];    // phase-A tasks of item i0+q
   uint8_t lcls[kSmallPer], ncls[kSmallPer];
-#pragma unroll
+#pragma unroll kSmallUnroll
   for (int q = 0; q < kSmallPer; ++q) {
     int64_t i = i0 + q;
     tk_of[q] = 0;
@@ -259,9 +266,9 @@ __device__ void small_tree(const TreeArrays& T, ClassifyArgs A, int F, unsigned 
         A.need[i] = 1;
         a_of[q] += 1;
       } else if (cn == 2) {
-        int64_t tn = (span + A.mtile - 1) / A.mtile;
+        int64_t tn = ceil_div64(span, A.mtile);
         A.need[i] = (uint32_t)tn;
-        tk_of[q] = (uint32_t)((tn + A.msuper - 1) / A.msuper);
+        tk_of[q] = (uint32_t)ceil_div64(tn, A.msuper);
         mbig += span;
         maxd = dep[i] > maxd ? dep[i] : maxd;
       } else A.need[i] = 0;
@@ -322,7 +329,7 @@ __device__ void small_tree(const TreeArrays& T, ClassifyArgs A, int F, unsigned 
   // phase-A tasks (any order; here by position)
   uint32_t totA;
   uint32_t slotA = block_excl_scan_u32(cntA, sscan, &totA);
-#pragma unroll
+#pragma unroll kSmallUnroll
   for (int q = 0; q < kSmallPer; ++q) {
     int64_t i = i0 + q;
     if (q >= per || i >= r) continue;
@@ -341,7 +348,7 @@ __device__ void small_tree(const TreeArrays& T, ClassifyArgs A, int F, unsigned 
   uint64_t base = totA;
   for (int d = dmax; d >= 0; --d) {
     uint32_t mine = 0;
-#pragma unroll
+#pragma unroll kSmallUnroll
     for (int q = 0; q < kSmallPer; ++q)
       if (q < per && i0 + q < r && ncls[q] == 2 && dep[i0 + q] == d) mine += tk_of[q];
     uint32_t tot;
@@ -352,7 +359,7 @@ __device__ void small_tree(const TreeArrays& T, ClassifyArgs A, int F, unsigned 
       met->depth_cursor[d] = base;
     }
     slot += (uint32_t)base;
-#pragma unroll
+#pragma unroll kSmallUnroll
     for (int q = 0; q < kSmallPer; ++q) {
       int64_t i = i0 + q;
       if (q < per && i < r && ncls[q] == 2 && dep[i] == d) {

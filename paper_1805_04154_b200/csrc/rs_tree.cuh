@@ -34,11 +34,14 @@ __device__ __forceinline__ MC shfl_mc_up(MC v, int o) {
 }
 
 // midpoint key of leaf [s0, s1)
-__device__ __forceinline__ uint64_t mid_key(pos_t s0, pos_t s1, pos_t n, int F) {
-  uint64_t l2 = (uint64_t)(s0 + s1);
-  if (F == 32) return (l2 << 32) / (2 * (uint64_t)n);
+__device__ __noinline__ uint64_t mid_key63(uint64_t l2, pos_t n) {  // n > 2^31 only
   unsigned __int128 num = (unsigned __int128)l2 << 63;
   return (uint64_t)(num / (unsigned __int128)(2 * (uint64_t)n));
+}
+__device__ __forceinline__ uint64_t mid_key(pos_t s0, pos_t s1, pos_t n, int F) {
+  uint64_t l2 = (uint64_t)(s0 + s1);
+  if (F == 32) return udiv64(l2 << 32, 2 * (uint64_t)n);
+  return mid_key63(l2, n);
 }
 
 // T1: midpoint keys and boundary powers.
@@ -58,7 +61,10 @@ __device__ void d_keys_powers(const pos_t* __restrict__ leaf_start, pos_t n, int
 }
 
 // ---- T2: (mask, const) scans for left / right ancestor counts ----
-constexpr int kScanItems = 16;  // max items per thread
+#ifndef RS_SCAN_ITEMS
+#define RS_SCAN_ITEMS 2
+#endif
+constexpr int kScanItems = RS_SCAN_ITEMS;  // max items per thread (unrolled: code size)
 constexpr int kScanThreads = 256;
 constexpr int kScanChunk = kScanItems * kScanThreads;
 // Items per thread adapt to r so that small trees still spread over many blocks.
