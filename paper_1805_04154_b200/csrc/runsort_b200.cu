@@ -403,7 +403,9 @@ int launch_exec(K* keys, void* tags, int64_t n, int w, int classic, int msuper, 
   M.tasks = V.tasks;
   M.mdesc = V.mdesc;
   M.met = V.met;
-  if (msuper > 1) k_merge_exec<K, TB, true><<<grid_m, kMergeThreads, smem_m, st>>>(M);
+  bool ahead = msuper > 1;
+  if (const char* ov = getenv("RS_MERGE_AHEAD")) ahead = atoi(ov) != 0;  // tuning override
+  if (ahead) k_merge_exec<K, TB, true><<<grid_m, kMergeThreads, smem_m, st>>>(M);
   else k_merge_exec<K, TB, false><<<grid_m, kMergeThreads, smem_m, st>>>(M);
   if (cudaError_t e_ = cudaGetLastError())
     return fail(RS_ECUDA, std::string("k_merge_exec launch/exec failed: ") + cudaGetErrorString(e_));
