@@ -35,14 +35,15 @@ __host__ __device__ inline uint32_t task_id(uint64_t t) { return uint32_t(t); }
 // one round trip -- node span and split, children, their completion counts
 // and buffers -- instead of a chain of dependent lookups.
 struct __align__(16) MDesc {
-  pos_t s, m, e;      // node span [s, e), children split at m
+  pos_t s_d;          // span start | node depth << 56   (positions < 2^40)
+  pos_t m_cl;         // children split | bit 56 / 57: child 0 / 1 is a merge node (class 2)
+  pos_t e;            // span end
   uint32_t c0, c1;    // unified child ids
   uint32_t nd0, nd1;  // children's completion counts (need)
   uint32_t j;         // node id
-  uint16_t sk;        // task index within the node
-  uint8_t d;          // node depth
-  uint8_t cl;         // bit 0 / 1: child 0 / 1 is a merge node (class 2)
+  uint32_t sk;        // task index within the node
 };
+constexpr pos_t kMdescPosMask = ((pos_t)1 << 56) - 1;
 static_assert(sizeof(MDesc) == 48, "MDesc layout");
 
 // Leaf modes for big (non-fused) leaves.

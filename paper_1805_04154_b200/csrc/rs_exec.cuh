@@ -115,26 +115,27 @@ struct ClassifyArgs {
 // then its children's counts and classes).
 __device__ __forceinline__ MDesc load_mdesc(const ClassifyArgs& A, uint32_t i) {
   MDesc md;
-  md.s = A.node_s[i];
+  pos_t s0 = A.node_s[i];
   md.e = A.node_e[i];
-  md.m = A.leaf_start[i];
+  pos_t m = A.leaf_start[i];
   md.c0 = A.child[2 * i];
   md.c1 = A.child[2 * i + 1];
-  md.d = A.depth[i];
+  pos_t d = A.depth[i];
   md.nd0 = A.need[md.c0];
   md.nd1 = A.need[md.c1];
   uint8_t cl0 = md.c0 < A.leaf_base ? A.cls[md.c0] : 0, cl1 = md.c1 < A.leaf_base ? A.cls[md.c1] : 0;
-  md.cl = (uint8_t)((cl0 == 2 ? 1 : 0) | (cl1 == 2 ? 2 : 0));
+  pos_t cl = (cl0 == 2 ? 1 : 0) | (cl1 == 2 ? 2 : 0);
+  md.s_d = s0 | (d << 56);
+  md.m_cl = m | (cl << 56);
   md.j = i;
   md.sk = 0;
   return md;
 }
 
-
 // Task record + descriptor of the k-th task of the node described by md.
 __device__ __forceinline__ void store_merge_task(const ClassifyArgs& A, uint32_t t, MDesc md, uint32_t k) {
   A.tasks[t] = make_task(kTaskMerge, k, md.j);
-  md.sk = (uint16_t)k;
+  md.sk = k;
   const uint4* src = reinterpret_cast<const uint4*>(&md);
   uint4* d = reinterpret_cast<uint4*>(A.mdesc + t);
   d[0] = src[0];

@@ -211,16 +211,16 @@ struct PTask {
         const MDesc md = E.mdesc[t];
         j = md.j;
         sk = md.sk;
-        s = md.s;
-        m = md.m;
+        s = md.s_d & kMdescPosMask;
+        d = (int)(md.s_d >> 56);
+        m = md.m_cl & kMdescPosMask;
         e = md.e;
         c0 = md.c0;
         c1 = md.c1;
         nd0 = md.nd0;
         nd1 = md.nd1;
-        d = md.d;
-        cl0 = (md.cl & 1) ? 2 : 0;
-        cl1 = (md.cl & 2) ? 2 : 0;
+        cl0 = ((md.m_cl >> 56) & 1) ? 2 : 0;
+        cl1 = ((md.m_cl >> 57) & 1) ? 2 : 0;
       }
       st = 3;  // next: the children's counters
 #else
