@@ -42,7 +42,10 @@ constexpr int kSuperMax = 15;          // tiles per merge task: runtime, <= 15 (
 #define RS_MERGE_CTAS 3
 #endif
 constexpr int kStages = RS_STAGES;     // smem ring depth
-constexpr int kConsumerThreads = 256;  // 8 consumer warps
+#ifndef RS_CONSUMER_WARPS
+#define RS_CONSUMER_WARPS 8
+#endif
+constexpr int kConsumerThreads = 32 * RS_CONSUMER_WARPS;  // consumer warps
 #ifndef RS_PRODUCERS
 #define RS_PRODUCERS 1
 #endif
