@@ -41,6 +41,7 @@ sys.path.insert(0, REPO)
 PEAKS = os.path.join(REPO, "MEASURED_PEAKS.json")
 FALLBACK_HBM_GBS = 6650.0
 KERNELS_PER_SORT = 3  # our launches per powersort (see csrc/runsort_b200.cu run_powersort)
+ALGO_CODES = {"powersort": 0, "peeksort": 1}  # rs_algo (include/runsort_b200.h)
 METRIC = "powersort keys/s at n=1e7 int32 random-runs; % of HBM roofline; 1/2/4/8 GPU"
 
 
@@ -109,22 +110,23 @@ class Clocks:
 
 
 # ------------------------------------------------------------ CPU baseline
-def cpu_oracle_throughput(keys: np.ndarray, tags, seconds: float, threads: int):
-    """Oracle (C restatement of reference powersort) on `threads` host threads,
-    each sorting its own copies of the workload until ~`seconds` elapse."""
+def cpu_oracle_throughput(keys: np.ndarray, tags, seconds: float, threads: int, algo: str = "powersort"):
+    """Oracle (C restatement of reference powersort / peeksort) on `threads` host
+    threads, each sorting its own copies of the workload until ~`seconds` elapse."""
     from oracle import oracle
 
     oracle.lib()
+    sort = getattr(oracle, algo)
     t0 = time.perf_counter()
     a = keys.copy()
-    oracle.powersort(a, 24, "bitonic", None if tags is None else tags.copy())
+    sort(a, 24, "bitonic", None if tags is None else tags.copy())
     single = time.perf_counter() - t0
     reps = max(1, int(seconds / max(single, 1e-3)))
 
     def work(_):
         for _ in range(reps):
             b = keys.copy()
-            oracle.powersort(b, 24, "bitonic", None if tags is None else tags.copy())
+            sort(b, 24, "bitonic", None if tags is None else tags.copy())
         return reps
 
     t0 = time.perf_counter()
@@ -164,14 +166,14 @@ def run_ours(args, rank, world, local_rank):
     work = torch.empty_like(src)
     twork = torch.empty_like(tsrc) if tsrc is not None else None
     key_code = _lib.RS_KEY_I32 if kb == 4 else _lib.RS_KEY_I64
-    ws_bytes = L.rs_workspace_bytes(0, key_code, tb, n, 24)
+    ws_bytes = L.rs_workspace_bytes(ALGO_CODES[args.algo], key_code, tb, n, 24)
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
     import ctypes
 
     def one_sort(profile=False, out=None):
-        return L.rs_sort(0, key_code, work.data_ptr(), tb, twork.data_ptr() if twork is not None else None,
+        return L.rs_sort(ALGO_CODES[args.algo], key_code, work.data_ptr(), tb, twork.data_ptr() if twork is not None else None,
                          n, 24, 0, ws.data_ptr(), ws_bytes, stream.cuda_stream,
                          ctypes.byref(out) if out is not None else None, None)
 
@@ -246,7 +248,7 @@ def run_ours(args, rank, world, local_rank):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        mm = rs.powersort(hk, rs.SortConfig(), None, ht)
+        mm = rs.SORTERS[args.algo](hk, rs.SortConfig(), None, ht)
         e1.record(stream)
         e1.synchronize()
         if it >= args.warmup:
@@ -287,7 +289,7 @@ def run_ours(args, rank, world, local_rank):
             "workload": f"cfg{args.config}: " + ["", "perm 2^20 int32", "random-runs 1e7 int32 mean sqrt(n)",
                                                  "zipf mixed-direction 2^24 int32", "stability 1e8 int32+int32"][args.config],
             "n_per_gpu": n, "key_bytes": kb, "tag_bytes": tb, "min_run_len": 24, "merge_kind": "bitonic",
-            "algo": "powersort", "l2": "flushed (512 MiB write) before every timed step",
+            "algo": args.algo, "l2": "flushed (512 MiB write) before every timed step",
             "parallelism": f"shard{world}" if world > 1 else "single-gpu",
         },
         "sorted_ok": ok,
@@ -310,11 +312,12 @@ def run_cpu_reference(args, as_baseline=False):
     keys, tags = make_input(args.config, args.n)
     threads = host_threads()
     secs = args.cpu_seconds
-    v, info = cpu_oracle_throughput(keys, tags, secs, threads)
+    v, info = cpu_oracle_throughput(keys, tags, secs, threads, args.algo)
     cpu = {"value": v, "unit": "keys/s", "cores": threads, "kind": "port",
            "sample": f"{info['sorts']} full cfg{args.config} sorts (n={len(keys)}), one per thread at a time, "
                      f"{info['wall_s']} s wall; single sort {info['single_sort_s']} s",
-           "impl": "oracle/runsort_oracle.c (C restatement of reference powersort, sorters.py:430-519)"}
+           "impl": "oracle/runsort_oracle.c (C restatement of reference " + args.algo + ", sorters.py:"
+                   + ("430-519" if args.algo == "powersort" else "146-361") + ")"}
     return cpu
 
 
@@ -329,6 +332,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sharded", action="store_true", help="use the multi-GPU sharded path even at N=1")
+    ap.add_argument("--algo", default="powersort", choices=["powersort", "peeksort"])
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -345,13 +349,15 @@ def main():
                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
                "ms_per_step": keys_n / cpu["value"] * 1e3, "higher_is_better": True,
                "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-               "config": {"workload": f"cfg{args.config}", "n_per_gpu": keys_n, "algo": "powersort",
+               "config": {"workload": f"cfg{args.config}", "n_per_gpu": keys_n, "algo": args.algo,
                           "min_run_len": 24, "merge_kind": "bitonic"},
                "cpu_baseline": cpu,
                "e2e": {"value": cpu["value"], "unit": "keys/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(out))
         return 0
 
+    if (world > 1 or args.sharded) and args.algo != "powersort":
+        raise SystemExit("the sharded multi-GPU path runs powersort on each shard (--algo powersort)")
     if world > 1 or args.sharded:
         import torch
         import torch.distributed as dist

@@ -35,8 +35,8 @@ struct PeekArgs {
   pos_t n;
   int w;
   uint32_t* ascw;      // pair bits of the original keys (n/32 + 2 words)
-  uint32_t* no_zero;   // summary: bit q set if ascw[q] == ~0
-  uint32_t* no_one;    // summary: bit q set if ascw[q] == 0
+  uint32_t* no_zero;   // skip summaries (skip_tree_words): level 1 bit q set if ascw[q] == ~0
+  uint32_t* no_one;    // level 1 bit q set if ascw[q] == 0
   PeekItem* front[2];  // frontier ping-pong
   int64_t front_cap;
   pos_t* nodes;        // (l, mid, r, depth) x cap
@@ -66,69 +66,131 @@ __device__ __forceinline__ uint32_t ascword(const uint32_t* asc, int64_t q, int 
   return v ? x : ~x;
 }
 
+// Skip summaries, kSkipLevels deep: level 1 bit q set iff pair word q has no
+// asc == v pair (the word can be skipped); level l bit i set iff level-(l-1)
+// word i is all ones.  A run of length L is crossed in O(levels + L / 32^levels)
+// loads instead of L / 1024 dependent loads (config 3's runs reach n / 4).
+constexpr int kSkipLevels = 4;
+struct SkipTree {
+  const uint32_t* lv[kSkipLevels + 1];  // lv[1..kSkipLevels]
+  int64_t cnt[kSkipLevels + 1];         // words per level
+};
+__host__ __device__ inline int64_t skip_level_words(int64_t words, int l) {
+  int64_t c = words;
+  for (int k = 0; k < l; ++k) c = (c + 31) / 32;
+  return c;
+}
+__host__ __device__ inline int64_t skip_tree_words(int64_t words) {
+  int64_t t = 0;
+  for (int l = 1; l <= kSkipLevels; ++l) t += skip_level_words(words, l);
+  return t + 8;
+}
+__device__ inline SkipTree make_skip_tree(const uint32_t* base, int64_t words) {
+  SkipTree S;
+  int64_t off = 0;
+  S.lv[0] = nullptr;
+  S.cnt[0] = words;
+  for (int l = 1; l <= kSkipLevels; ++l) {
+    S.lv[l] = base + off;
+    S.cnt[l] = skip_level_words(words, l);
+    off += S.cnt[l];
+  }
+  return S;
+}
+
+// Smallest pair word index >= w that is not skippable (kInf if none).
+__device__ int64_t skip_next(const SkipTree& S, int64_t w) {
+  int64_t cur = w;
+  int lev = 1;
+  for (;; ++lev) {
+    int64_t i = cur >> 5;
+    if (i >= S.cnt[lev]) return kInf;
+    uint32_t m = ~__ldcg(S.lv[lev] + i) & (0xffffffffu << (cur & 31));
+    if (m) { cur = (i << 5) + __ffs(m) - 1; break; }
+    cur = i + 1;
+    if (lev == kSkipLevels) {  // top level: linear
+      for (;; ++cur) {
+        if (cur >= S.cnt[lev]) return kInf;
+        uint32_t mt = ~__ldcg(S.lv[lev] + cur);
+        if (mt) { cur = (cur << 5) + __ffs(mt) - 1; break; }
+      }
+      break;
+    }
+  }
+  for (int l = lev - 1; l >= 1; --l) {  // descend: cur is a level-l word with a zero bit
+    if (cur >= S.cnt[l]) return kInf;
+    uint32_t m = ~__ldcg(S.lv[l] + cur);
+    cur = (cur << 5) + __ffs(m) - 1;
+  }
+  return cur;
+}
+
+// Largest pair word index <= w that is not skippable (-1 if none).
+__device__ int64_t skip_prev(const SkipTree& S, int64_t w) {
+  int64_t cur = w;
+  int lev = 1;
+  for (;; ++lev) {
+    if (cur < 0) return -1;
+    int64_t i = cur >> 5;
+    int b = int(cur & 31);
+    uint32_t m = ~__ldcg(S.lv[lev] + i) & (b == 31 ? 0xffffffffu : ((1u << (b + 1)) - 1));
+    if (m) { cur = (i << 5) + 31 - __clz(m); break; }
+    cur = i - 1;
+    if (lev == kSkipLevels) {
+      for (;; --cur) {
+        if (cur < 0) return -1;
+        uint32_t mt = ~__ldcg(S.lv[lev] + cur);
+        if (mt) { cur = (cur << 5) + 31 - __clz(mt); break; }
+      }
+      break;
+    }
+  }
+  for (int l = lev - 1; l >= 1; --l) {
+    uint32_t m = ~__ldcg(S.lv[l] + cur);
+    cur = (cur << 5) + 31 - __clz(m);
+  }
+  return cur;
+}
+
 // Smallest k in [p, q) with asc_k == v, else q.
-__device__ pos_t next_eq(const uint32_t* asc, const uint32_t* skip, pos_t p, pos_t q, int v) {
+__device__ pos_t next_eq(const uint32_t* asc, const SkipTree& S, pos_t p, pos_t q, int v) {
   if (p >= q) return q;
   int64_t wq = p >> 5;
   uint32_t x = ascword(asc, wq, v) & (0xffffffffu << (p & 31));
-  for (;;) {
-    if (x) {
-      pos_t k = (wq << 5) + __ffs(x) - 1;
-      return k < q ? k : q;
-    }
+  if (!x) {
     ++wq;
     if ((wq << 5) >= q) return q;
-    // skip whole words without a v bit via the summary
-    for (;;) {
-      uint32_t sb = ~__ldcg(skip + (wq >> 5)) & (0xffffffffu << (wq & 31));
-      if (sb) {
-        wq = ((wq >> 5) << 5) + __ffs(sb) - 1;
-        break;
-      }
-      wq = ((wq >> 5) + 1) << 5;
-      if ((wq << 5) >= q) return q;
-    }
-    if ((wq << 5) >= q) return q;
+    wq = skip_next(S, wq);
+    if (wq >= kInf || (wq << 5) >= q) return q;
     x = ascword(asc, wq, v);
   }
+  pos_t k = (wq << 5) + __ffs(x) - 1;
+  return k < q ? k : q;
 }
 
 // Largest k in [lo, p) with asc_k == v, else lo - 1.
-__device__ pos_t prev_eq(const uint32_t* asc, const uint32_t* skip, pos_t p, pos_t lo, int v) {
+__device__ pos_t prev_eq(const uint32_t* asc, const SkipTree& S, pos_t p, pos_t lo, int v) {
   if (p <= lo) return lo - 1;
   pos_t last = p - 1;
   int64_t wq = last >> 5;
   int sh = 31 - int(last & 31);
   uint32_t x = ascword(asc, wq, v) & (0xffffffffu >> sh);
-  for (;;) {
-    if (x) {
-      pos_t k = (wq << 5) + 31 - __clz(x);
-      return k >= lo ? k : lo - 1;
-    }
+  if (!x) {
     if ((wq << 5) <= lo) return lo - 1;
-    --wq;
-    for (;;) {
-      int bit = int(wq & 31);
-      uint32_t sb = ~__ldcg(skip + (wq >> 5)) & (bit == 31 ? 0xffffffffu : ((1u << (bit + 1)) - 1));
-      if (sb) {
-        wq = ((wq >> 5) << 5) + 31 - __clz(sb);
-        break;
-      }
-      if ((wq >> 5) == 0) return lo - 1;
-      wq = ((wq >> 5) << 5) - 1;
-      if (((wq + 1) << 5) <= lo) return lo - 1;
-    }
-    if (((wq + 1) << 5) <= lo) return lo - 1;
+    wq = skip_prev(S, wq - 1);
+    if (wq < 0 || ((wq + 1) << 5) <= lo) return lo - 1;
     x = ascword(asc, wq, v);
   }
+  pos_t k = (wq << 5) + 31 - __clz(x);
+  return k >= lo ? k : lo - 1;
 }
 
 template <typename K>
 struct PeekEval {
   const K* a;
   const uint32_t* asc;
-  const uint32_t* no_zero;
-  const uint32_t* no_one;
+  SkipTree no_zero;  // skip words without an asc == 0 pair
+  SkipTree no_one;   // skip words without an asc == 1 pair
   unsigned long long comps;
 
   __device__ bool le(pos_t x, pos_t y) const { return __ldcg(a + x) <= __ldcg(a + y); }
@@ -335,7 +397,55 @@ __device__ void reverse_segments(const PeekArgs& P, const pos_t* revs, int64_t n
   using T = typename TagT<TB>::type;
   K* a = reinterpret_cast<K*>(P.keys);
   T* t = reinterpret_cast<T*>(P.tags);
-  // each block takes whole segments; threads swap pairs
+  constexpr int kRevSeg = 64;  // few (long) segments: element-parallel; many: a block per segment
+  if (nrev <= kRevSeg) {
+    // all blocks share the swaps of every segment (a strictly descending run
+    // can be n / 4 long): prefix of half-lengths in shared memory, grid-stride
+    // over the swaps, binary search for the segment
+    __shared__ pos_t s_pre[kRevSeg + 1];
+    __shared__ pos_t s_i[kRevSeg], s_j[kRevSeg];
+    for (int64_t q = threadIdx.x; q < nrev; q += blockDim.x) {
+      s_i[q] = revs[2 * q];
+      s_j[q] = revs[2 * q + 1];
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {  // warp 0: exclusive scan of the half-lengths, 2 segments per lane
+      const int lane = threadIdx.x;
+      pos_t h0 = 2 * lane < nrev ? (s_j[2 * lane] - s_i[2 * lane] + 1) / 2 : 0;
+      pos_t h1 = 2 * lane + 1 < nrev ? (s_j[2 * lane + 1] - s_i[2 * lane + 1] + 1) / 2 : 0;
+      pos_t inc = h0 + h1;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        pos_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      pos_t ex = inc - h0 - h1;
+      if (2 * lane < nrev) s_pre[2 * lane] = ex;
+      if (2 * lane + 1 < nrev) s_pre[2 * lane + 1] = ex + h0;
+      if (lane == 31) s_pre[nrev] = inc;
+    }
+    __syncthreads();
+    const pos_t total = s_pre[nrev];
+    for (pos_t x = (pos_t)blockIdx.x * blockDim.x + threadIdx.x; x < total; x += (pos_t)gridDim.x * blockDim.x) {
+      int64_t lo = 0, hi = nrev - 1;  // last q with s_pre[q] <= x
+      while (lo < hi) {
+        int64_t md = (lo + hi + 1) >> 1;
+        if (s_pre[md] <= x) lo = md; else hi = md - 1;
+      }
+      pos_t i = s_i[lo], j = s_j[lo], o = x - s_pre[lo];
+      K u = a[i + o], v = a[j - o];
+      a[i + o] = v;
+      a[j - o] = u;
+      if (TB) {
+        T tu = t[i + o], tv = t[j - o];
+        t[i + o] = tv;
+        t[j - o] = tu;
+      }
+    }
+    __syncthreads();
+    return;
+  }
+  // many segments: each block takes whole segments; threads swap pairs
   for (int64_t sidx = blockIdx.x; sidx < nrev; sidx += gridDim.x) {
     pos_t i = revs[2 * sidx], j = revs[2 * sidx + 1];
     pos_t half = (j - i + 1) / 2;
@@ -396,8 +506,28 @@ __global__ void __launch_bounds__(256, 2) k_peek(PeekArgs P) {
       if (lane == 0) { P.no_zero[sw] = z; P.no_one[sw] = o; }
     }
   }
+  // higher skip levels: bit i of level l set iff level-(l-1) word i is all ones
+  {
+    int lane = threadIdx.x & 31;
+    int64_t gw = gtid >> 5, nwarps = gthreads >> 5;
+    int64_t off_prev = 0, off = skip_level_words(P.words, 1);
+    for (int l = 2; l <= kSkipLevels; ++l) {
+      grid.sync();
+      int64_t cprev = skip_level_words(P.words, l - 1), c = skip_level_words(P.words, l);
+      for (int64_t sw = gw; sw < c; sw += nwarps) {
+        int64_t q = 32 * sw + lane;
+        bool zf = q < cprev && P.no_zero[off_prev + q] == 0xffffffffu;
+        bool of = q < cprev && P.no_one[off_prev + q] == 0xffffffffu;
+        uint32_t z = __ballot_sync(0xffffffffu, zf);
+        uint32_t o = __ballot_sync(0xffffffffu, of);
+        if (lane == 0) { P.no_zero[off + sw] = z; P.no_one[off + sw] = o; }
+      }
+      off_prev = off;
+      off += c;
+    }
+  }
   grid.sync();
-  PeekEval<K> V{a, P.ascw, P.no_zero, P.no_one, 0ull};
+  PeekEval<K> V{a, P.ascw, make_skip_tree(P.no_zero, P.words), make_skip_tree(P.no_one, P.words), 0ull};
   PeekOut O;
   O.nodes = P.nodes;
   O.n_nodes = &pc->n_nodes;

@@ -165,7 +165,7 @@ Layout make_layout(int64_t n, int w, int kb, int tb, int algo) {
   if (pk) {
     L.front_cap = n + 1;
     L.rec_cap = n + 1;
-    L.sum_words = (L.words + 31) / 32 + 2;
+    L.sum_words = skip_tree_words(L.words);
     L.wchunks = (L.words + kWordChunk - 1) / kWordChunk + 1;
     L.o_front0 = take((size_t)L.front_cap * sizeof(PeekItem));
     L.o_front1 = take((size_t)L.front_cap * sizeof(PeekItem));
