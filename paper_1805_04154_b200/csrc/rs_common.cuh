@@ -1,6 +1,7 @@
 // rs_common.cuh -- shared types and device helpers for the B200 run-adaptive
 // mergesort (powersort / peeksort of arXiv 1805.04154).
 #pragma once
+#include <cstddef>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -44,7 +45,8 @@ struct __align__(16) MDesc {
   uint32_t sk;        // task index within the node
 };
 constexpr pos_t kMdescPosMask = ((pos_t)1 << 56) - 1;
-static_assert(sizeof(MDesc) == 48, "MDesc layout");
+static_assert(sizeof(MDesc) == 48 && offsetof(MDesc, e) == 16 && offsetof(MDesc, nd0) == 32 &&
+                  offsetof(MDesc, sk) == 44, "MDesc layout (store_merge_task writes it as three uint4)");
 
 // Leaf modes for big (non-fused) leaves.
 enum LeafMode : int { kLeafNone = 0, kLeafSwap = 1, kLeafRevCopy = 2, kLeafCopy = 3 };

@@ -132,15 +132,15 @@ __device__ __forceinline__ MDesc load_mdesc(const ClassifyArgs& A, uint32_t i) {
   return md;
 }
 
-// Task record + descriptor of the k-th task of the node described by md.
-__device__ __forceinline__ void store_merge_task(const ClassifyArgs& A, uint32_t t, MDesc md, uint32_t k) {
+// Task record + descriptor of the k-th task of the node described by md
+// (three 16-byte stores assembled in registers).
+__device__ __forceinline__ void store_merge_task(const ClassifyArgs& A, uint32_t t, const MDesc& md, uint32_t k) {
   A.tasks[t] = make_task(kTaskMerge, k, md.j);
-  md.sk = k;
-  const uint4* src = reinterpret_cast<const uint4*>(&md);
   uint4* d = reinterpret_cast<uint4*>(A.mdesc + t);
-  d[0] = src[0];
-  d[1] = src[1];
-  d[2] = src[2];
+  const uint64_t sd = (uint64_t)md.s_d, mc = (uint64_t)md.m_cl, e = (uint64_t)md.e;
+  d[0] = make_uint4((uint32_t)sd, (uint32_t)(sd >> 32), (uint32_t)mc, (uint32_t)(mc >> 32));
+  d[1] = make_uint4((uint32_t)e, (uint32_t)(e >> 32), md.c0, md.c1);
+  d[2] = make_uint4(md.nd0, md.nd1, md.j, k);
 }
 
 // Node j can run as (part of) one fused phase-A task: its span fits the fused
@@ -354,6 +354,7 @@ __device__ void d_task_fill(ClassifyArgs A, const uint32_t* __restrict__ chunk_d
     if (cn == 1) A.tasks[slot++] = make_task(kTaskFuse, 0, (uint32_t)i);
     __syncthreads();
   }
+  RS_DBG(A.met, 20);
   // merge tasks: slots by (depth, position); chunk boundaries staged in smem,
   // warp 0 assigns ordered slots, all threads write.
   const int64_t oc = ord_chunk(r);
@@ -380,6 +381,7 @@ __device__ void d_task_fill(ClassifyArgs A, const uint32_t* __restrict__ chunk_d
       s_tk[x] = tv;
     }
     __syncthreads();
+    RS_DBG(A.met, 21);
     // ordered slots, 256 nodes per round: every warp ranks its 32 nodes among
     // same-depth peers (shuffle prefix), per-depth warp totals are scanned
     // across warps, and `run` carries each depth's cursor to the next round
@@ -414,22 +416,34 @@ __device__ void d_task_fill(ClassifyArgs A, const uint32_t* __restrict__ chunk_d
       __syncthreads();
     }
     // rounds of blockDim nodes: every thread loads one node's merge descriptor
-    // into shared memory (parallel round trips), then one warp per node writes
-    // its task records and per-task descriptors
+    // into shared memory (parallel round trips), then all threads write the
+    // round's task records and per-task descriptors
+    RS_DBG(A.met, 22);
     MDesc* s_md = reinterpret_cast<MDesc*>(smem_fill + kFillMdOff);
-    int wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    __shared__ uint32_t s_pre[256];  // blockDim == 256
     for (int64_t g = 0; g < cnt_i; g += blockDim.x) {
       int64_t x = g + threadIdx.x;
-      if (x < cnt_i && s_dep[x] != 255) s_md[threadIdx.x] = load_mdesc(A, (uint32_t)(i0 + x));
+      const bool big = x < cnt_i && s_dep[x] != 255;
+      if (big) s_md[threadIdx.x] = load_mdesc(A, (uint32_t)(i0 + x));
+      // flatten the round's tasks over all threads: a node with hundreds of
+      // tiles (the top of the tree) is not written by one warp
+      uint32_t tot;
+      uint32_t pre = block_excl_scan_u32(big ? s_tk[x] : 0u, s_sc, &tot);  // syncs: s_md visible
+      s_pre[threadIdx.x] = pre;
       __syncthreads();
-      int64_t ny = cnt_i - g < (int64_t)blockDim.x ? cnt_i - g : (int64_t)blockDim.x;
-      for (int64_t y = wid; y < ny; y += nw) {
-        if (s_dep[g + y] == 255) continue;
-        uint32_t tk = s_tk[g + y], slot = s_slot[g + y];
-        const MDesc md = s_md[y];
-        for (uint32_t k = lane; k < tk; k += 32) store_merge_task(A, slot + k, md, k);
+      RS_DBG(A.met, 23);
+      const int ny = cnt_i - g < (int64_t)blockDim.x ? (int)(cnt_i - g) : (int)blockDim.x;
+      for (uint32_t q = threadIdx.x; q < tot; q += blockDim.x) {
+        int lo = 0, hi = ny - 1;  // last node y with s_pre[y] <= q
+        while (lo < hi) {
+          int md = (lo + hi + 1) >> 1;
+          if (s_pre[md] <= q) lo = md; else hi = md - 1;
+        }
+        uint32_t k = q - s_pre[lo];
+        store_merge_task(A, s_slot[g + lo] + k, s_md[lo], k);
       }
       __syncthreads();
+      RS_DBG(A.met, 24);
     }
   }
 }
