@@ -54,6 +54,19 @@ def _count_below(keys, rank_i: int, trip: Tuple[int, int, int]) -> int:
     return int(p)
 
 
+def _count_below_many(keys, rank_i: int, trips) -> np.ndarray:
+    """_count_below for many triples with one device search and one copy back."""
+    import torch
+
+    k = torch.tensor([t[0] for t in trips], dtype=torch.int64).to(keys.device).to(keys.dtype)
+    r = np.asarray([t[1] for t in trips], dtype=np.int64)
+    p = np.asarray([t[2] for t in trips], dtype=np.int64)
+    le = torch.searchsorted(keys, k, right=True)
+    lt = torch.searchsorted(keys, k, right=False)
+    both = torch.stack([le, lt]).cpu().numpy().astype(np.int64)
+    return np.where(rank_i < r, both[0], np.where(rank_i > r, both[1], p))
+
+
 def _sample_triples(keys, rank: int, S: int):
     import torch
 
@@ -87,7 +100,7 @@ def compute_splits(keys, group=None, samples: int = SAMPLES) -> np.ndarray:
     n_local = torch.tensor([keys.shape[0]], dtype=torch.int64, device=dev)
     ns = [torch.zeros_like(n_local) for _ in range(W)]
     dist.all_gather(ns, n_local, group=group)
-    ns = [int(x.item()) for x in ns]
+    ns = [int(x) for x in torch.cat(ns).cpu().numpy()]  # one host sync
     T = np.concatenate([[0], np.cumsum(ns)]).astype(np.int64)
 
     # round 1: samples
@@ -128,18 +141,24 @@ def compute_splits(keys, group=None, samples: int = SAMPLES) -> np.ndarray:
     # round 2: exact counts below the bracket ends; round 3: candidates
     G = len(targets)
     a = np.zeros(G, dtype=np.int64)
-    b = np.zeros(G, dtype=np.int64)
-    for gi in range(G):
-        a[gi] = 0 if lo_trip[gi] is None else _count_below(keys, rank, lo_trip[gi])
-        b[gi] = ns[rank] if hi_trip[gi] is None else _count_below(keys, rank, hi_trip[gi])
-        if b[gi] < a[gi]:
-            b[gi] = a[gi]
+    b = np.full(G, ns[rank], dtype=np.int64)
+    # all bracket ends counted in one device search (one host sync, not 2(W-1))
+    ends = [(gi, 0, t) for gi, t in enumerate(lo_trip) if t is not None] + \
+           [(gi, 1, t) for gi, t in enumerate(hi_trip) if t is not None]
+    if ends:
+        counts = _count_below_many(keys, rank, [t for _, _, t in ends])
+        for (gi, side, _), c in zip(ends, counts):
+            if side == 0:
+                a[gi] = c
+            else:
+                b[gi] = c
+    b = np.maximum(a, b)
     meta = torch.tensor(np.stack([a, b], axis=1) if G else np.zeros((0, 2), np.int64), dtype=torch.int64,
                         device=dev)
     metas = [torch.zeros_like(meta) for _ in range(W)]
     if G:
         dist.all_gather(metas, meta, group=group)
-    metas = [x.cpu().numpy() for x in metas]
+    metas = list(torch.stack(metas).cpu().numpy()) if G else [np.zeros((0, 2), np.int64)] * W
     M = max([1] + [int((mt[:, 1] - mt[:, 0]).max()) for mt in metas if len(mt)])
     cand = torch.zeros((G, M), dtype=torch.int64, device=dev)
     for gi in range(G):
@@ -149,7 +168,7 @@ def compute_splits(keys, group=None, samples: int = SAMPLES) -> np.ndarray:
     cands = [torch.zeros_like(cand) for _ in range(W)]
     if G:
         dist.all_gather(cands, cand, group=group)
-    cands = [x.cpu().numpy() for x in cands]
+    cands = list(torch.stack(cands).cpu().numpy()) if G else [np.zeros((0, M), np.int64)] * W
     for gi, t in enumerate(targets):
         base = sum(int(metas[i][gi, 0]) for i in range(W))
         need = t - base
