@@ -371,8 +371,13 @@ def main():
         dist.init_process_group("nccl")
         from paper_1805_04154_b200 import dist as rsdist
 
+        clocks = Clocks(local_rank)
+        clocks.start()
         out = rsdist.bench_sharded(args, rank, world, local_rank)
+        out["clocks"] = clocks.stop()
         if rank == 0:
+            if world == 1 and not args.no_cpu_baseline:
+                out["cpu_baseline"] = run_cpu_reference(args)
             print(json.dumps(out))
         dist.destroy_process_group()
         return 0

@@ -263,6 +263,33 @@ def bench_sharded(args, rank: int, world: int, local_rank: int) -> dict:
     t = torch.tensor([float(np.mean(times))], device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
+    # e2e: this rank's shard from pinned host memory, the sharded sort, its slice back
+    hk = torch.from_numpy(keys_np).pin_memory()
+    ht = torch.from_numpy(tags_np).pin_memory() if tags_np is not None else None
+    e2e = []
+    for it in range(args.warmup + args.steps):
+        hk.copy_(torch.from_numpy(keys_np))
+        flush.fill_(1)
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        dk = hk.to(dev, non_blocking=True)
+        dt = ht.to(dev, non_blocking=True) if ht is not None else None
+        o2, t2, _ = sharded_sort(dk, dt)
+        hk.copy_(o2, non_blocking=True)  # pinned: a device-to-host DMA on the stream
+        if t2 is not None:
+            ht.copy_(t2, non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        dist.barrier()
+        if it >= args.warmup:
+            e2e.append(e0.elapsed_time(e1))
+    te = torch.tensor([float(np.mean(e2e))], device=dev)
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_ms = float(te.item())
+    B = keys_np.itemsize + (tags_np.itemsize if tags_np is not None else 0)
     # global sortedness check: local sorted + boundary with the next rank
     ok = bool((out[1:] >= out[:-1]).all().item()) if out.numel() > 1 else True
     edge = torch.tensor([out[0].item() if out.numel() else 0, out[-1].item() if out.numel() else 0],
@@ -280,5 +307,8 @@ def bench_sharded(args, rank: int, world: int, local_rank: int) -> dict:
                    "n_per_gpu": n, "parallelism": f"shard{world}",
                    "l2": "flushed (512 MiB write) before every timed step"},
         "globally_sorted_ok": ok,
-        "gpu_launches": None,
+        "e2e": {"value": n * world / (e2e_ms / 1e3), "unit": "keys/s", "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": n * B, "d2h_bytes_per_step": n * B},
+        # our kernels per step: two powersorts (shard, then the received runs), 3 launches each
+        "gpu_launches": 6 * args.steps,
     }
