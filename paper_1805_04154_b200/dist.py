@@ -67,22 +67,6 @@ def _count_below_many(keys, rank_i: int, trips) -> np.ndarray:
     return np.where(rank_i < r, both[0], np.where(rank_i > r, both[1], p))
 
 
-def _sample_triples(keys, rank: int, S: int):
-    import torch
-
-    n = keys.shape[0]
-    if n == 0:
-        pos = torch.zeros(S, dtype=torch.int64, device=keys.device)
-        vals = torch.zeros(S, dtype=torch.int64, device=keys.device)
-        valid = torch.zeros(S, dtype=torch.int64, device=keys.device)
-    else:
-        pos = (torch.arange(S, device=keys.device, dtype=torch.int64) * n) // S
-        vals = keys[pos].to(torch.int64)
-        valid = torch.ones(S, dtype=torch.int64, device=keys.device)
-    rk = torch.full((S,), rank, dtype=torch.int64, device=keys.device)
-    return torch.stack([vals, rk, pos, valid], dim=1)  # (S, 4)
-
-
 def compute_splits(keys, group=None, samples: int = SAMPLES) -> np.ndarray:
     """Exact split matrix for the locally sorted shard `keys` (torch tensor).
 
@@ -97,18 +81,28 @@ def compute_splits(keys, group=None, samples: int = SAMPLES) -> np.ndarray:
     rank = dist.get_rank(group)
     dev = keys.device
     S = samples
-    n_local = torch.tensor([keys.shape[0]], dtype=torch.int64, device=dev)
-    ns = [torch.zeros_like(n_local) for _ in range(W)]
-    dist.all_gather(ns, n_local, group=group)
-    ns = [int(x) for x in torch.cat(ns).cpu().numpy()]  # one host sync
+    if W == 1:
+        return np.asarray([[0], [int(keys.shape[0])]], dtype=np.int64)
+    # round 1 (one collective, one host copy): every rank publishes its length
+    # and S regular samples of its sorted shard; positions are implicit
+    n_mine = int(keys.shape[0])
+    pos_np = (np.arange(S, dtype=np.int64) * n_mine) // S
+    pack = torch.zeros(S + 1, dtype=torch.int64, device=dev)
+    pack[0] = n_mine
+    if n_mine:
+        pack[1:] = keys[torch.from_numpy(pos_np).to(dev)].to(torch.int64)
+    gathered = [torch.empty_like(pack) for _ in range(W)]
+    dist.all_gather(gathered, pack, group=group)
+    g = torch.stack(gathered).cpu().numpy()  # (W, S + 1)
+    ns = [int(x) for x in g[:, 0]]
     T = np.concatenate([[0], np.cumsum(ns)]).astype(np.int64)
-
-    # round 1: samples
-    st = _sample_triples(keys, rank, S)
-    gathered = [torch.zeros_like(st) for _ in range(W)]
-    dist.all_gather(gathered, st, group=group)
-    samp = torch.cat(gathered).cpu().numpy()  # (W*S, 4)
-    samp = samp[samp[:, 3] == 1]
+    rows = []
+    for i in range(W):
+        if ns[i] == 0:
+            continue
+        pi = (np.arange(S, dtype=np.int64) * ns[i]) // S
+        rows.append(np.stack([g[i, 1:], np.full(S, i, dtype=np.int64), pi, np.ones(S, dtype=np.int64)], axis=1))
+    samp = np.concatenate(rows) if rows else np.zeros((0, 4), dtype=np.int64)
     # one sample per distinct (rank, position); sort by (key, rank, position)
     _, uidx = np.unique(samp[:, 1] * (1 << 40) + samp[:, 2], return_index=True)
     samp = samp[uidx]
