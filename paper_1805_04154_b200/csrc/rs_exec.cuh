@@ -108,7 +108,8 @@ struct ClassifyArgs {
   int maxb;      // ExecArgs::maxb
   int fuse_avg;  // fused subtrees: average leaf length below this
   const uint32_t* child;
-  MDesc* mdesc;  // per merge task, same index as tasks[]
+  MDesc* mdesc;      // per merge task, index = task slot - first merge slot (met->phaseA)
+  int64_t mdesc_cap;
 };
 
 // Merge descriptor of node i (two dependent round trips: the node's fields,
@@ -134,9 +135,11 @@ __device__ __forceinline__ MDesc load_mdesc(const ClassifyArgs& A, uint32_t i) {
 
 // Task record + descriptor of the k-th task of the node described by md
 // (three 16-byte stores assembled in registers).
-__device__ __forceinline__ void store_merge_task(const ClassifyArgs& A, uint32_t t, const MDesc& md, uint32_t k) {
+__device__ __forceinline__ void store_merge_task(const ClassifyArgs& A, uint32_t t, uint32_t mbase, const MDesc& md,
+                                                 uint32_t k) {
   A.tasks[t] = make_task(kTaskMerge, k, md.j);
-  uint4* d = reinterpret_cast<uint4*>(A.mdesc + t);
+  if ((int64_t)(t - mbase) >= A.mdesc_cap) return;  // beyond the layout bound: the producer walks the node arrays
+  uint4* d = reinterpret_cast<uint4*>(A.mdesc + (t - mbase));
   const uint64_t sd = (uint64_t)md.s_d, mc = (uint64_t)md.m_cl, e = (uint64_t)md.e;
   d[0] = make_uint4((uint32_t)sd, (uint32_t)(sd >> 32), (uint32_t)mc, (uint32_t)(mc >> 32));
   d[1] = make_uint4((uint32_t)e, (uint32_t)(e >> 32), md.c0, md.c1);
@@ -420,6 +423,7 @@ __device__ void d_task_fill(ClassifyArgs A, const uint32_t* __restrict__ chunk_d
     // round's task records and per-task descriptors
     RS_DBG(A.met, 22);
     MDesc* s_md = reinterpret_cast<MDesc*>(smem_fill + kFillMdOff);
+    const uint32_t mbase = (uint32_t)A.met->phaseA;  // first merge-task slot (final after classification)
     __shared__ uint32_t s_pre[256];  // blockDim == 256
     for (int64_t g = 0; g < cnt_i; g += blockDim.x) {
       int64_t x = g + threadIdx.x;
@@ -440,7 +444,7 @@ __device__ void d_task_fill(ClassifyArgs A, const uint32_t* __restrict__ chunk_d
           if (s_pre[md] <= q) lo = md; else hi = md - 1;
         }
         uint32_t k = q - s_pre[lo];
-        store_merge_task(A, s_slot[g + lo] + k, s_md[lo], k);
+        store_merge_task(A, s_slot[g + lo] + k, mbase, s_md[lo], k);
       }
       __syncthreads();
       RS_DBG(A.met, 24);

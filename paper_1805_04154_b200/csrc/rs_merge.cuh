@@ -98,7 +98,8 @@ struct MergeArgs {
   const uint32_t* need;
   uint32_t* done;
   const uint64_t* tasks;
-  const MDesc* mdesc;  // per merge task (RS_MDESC)
+  const MDesc* mdesc;  // per merge task (RS_MDESC), index = task - first merge task
+  long long mdesc_cap;
   DevMetrics* met;
   const uint8_t* cls;  // unified id -> class (2 = merge node for internal ids)
   uint32_t leaf_base;
@@ -190,6 +191,7 @@ struct PTask {
   pos_t s, e, m;
   int d;
   int st;  // stages done: 1 claimed, 2 record, 3 node, 4 need, 5 counters (speculative)
+  unsigned long long tbase;  // first merge task: descriptor index = t - tbase
   bool valid;
   __device__ __forceinline__ void claim(DevMetrics* met) {
     t = 0;
@@ -210,8 +212,16 @@ struct PTask {
       valid = t < ntasks;
 #if RS_MDESC
       // one 48-byte descriptor instead of the record -> node -> children chain
+      // (tasks beyond the descriptor array's bound take the chain below)
+      if (valid && (long long)(t - tbase) >= E.mdesc_cap) {
+        uint64_t rec = E.tasks[t];
+        j = task_id(rec);
+        sk = task_tile(rec);
+        st = 2;
+        return;
+      }
       if (valid) {
-        const MDesc md = E.mdesc[t];
+        const MDesc md = E.mdesc[t - tbase];
         j = md.j;
         sk = md.sk;
         s = md.s_d & kMdescPosMask;
@@ -318,7 +328,8 @@ __global__ void __launch_bounds__(kMergeThreads, RS_MERGE_CTAS) k_merge_exec(Mer
   }
   __syncthreads();
   unsigned long long ntasks = E.met->n_tasks;
-  const unsigned long long t_first = E.met->task_ctr;  // first merge task (after the phase-A tasks)
+  // first merge task (after the phase-A tasks); not task_ctr, which other CTAs may already have advanced
+  const unsigned long long t_first = E.met->phaseA;
 
   if (warp < kProducers) {
     // ------------------------------------------------------------- producer
@@ -348,6 +359,7 @@ __global__ void __launch_bounds__(kMergeThreads, RS_MERGE_CTAS) k_merge_exec(Mer
     const unsigned long long sstride = (unsigned long long)gridDim.x * kProducers;
     unsigned long long snext = t_first + (unsigned long long)blockIdx.x * kProducers + (unsigned long long)warp;
     PTask cur, nxt;
+    cur.tbase = nxt.tbase = t_first;
     if (kStatic) cur.claim_static(snext, sstride);
     else cur.claim(E.met);
     cur.finish(E, ntasks);

@@ -299,6 +299,7 @@ __device__ void small_tree(const TreeArrays& T, ClassifyArgs A, int F, unsigned 
     jid[e] = id;
     jcnt[e] = cnt | (kind << 30);
   };
+  uint32_t s_mbase = 0;  // first merge-task slot (set once the phase-A count is known)
   auto drain = [&]() {
     __syncthreads();
     uint32_t nj = s_nj;
@@ -314,7 +315,7 @@ __device__ void small_tree(const TreeArrays& T, ClassifyArgs A, int F, unsigned 
         uint32_t kind = c >> 30, cnt = c & 0x3fffffffu;
         if (kind == kTaskMerge) {
           const MDesc md = s_md[y];
-          for (uint32_t k = lane; k < cnt; k += 32) store_merge_task(A, slot + k, md, k);
+          for (uint32_t k = lane; k < cnt; k += 32) store_merge_task(A, slot + k, s_mbase, md, k);
         } else {
           for (uint32_t k = lane; k < cnt; k += 32) A.tasks[slot + k] = make_task(kind, kind == kTaskFuse ? 0 : k, id);
         }
@@ -329,6 +330,7 @@ __device__ void small_tree(const TreeArrays& T, ClassifyArgs A, int F, unsigned 
   // phase-A tasks (any order; here by position)
   uint32_t totA;
   uint32_t slotA = block_excl_scan_u32(cntA, sscan, &totA);
+  s_mbase = totA;  // first merge-task slot
 #pragma unroll kSmallUnroll
   for (int q = 0; q < kSmallPer; ++q) {
     int64_t i = i0 + q;

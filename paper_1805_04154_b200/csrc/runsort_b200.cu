@@ -85,6 +85,7 @@ struct Layout {
   size_t o_leaf_start, o_leaf_info, o_leaf_depth, o_K, o_P, o_la, o_ra, o_depth;
   size_t o_node_a, o_node_b, o_node_s, o_node_e, o_parent, o_child, o_need, o_done;
   size_t o_agg, o_tasks, o_mdesc, o_chunkdep, o_cls, o_met, total;
+  int64_t mdesc_cap;  // merge-task descriptors (indexed from the first merge task)
   // peeksort replay
   int algo;
   int64_t front_cap, rec_cap, sum_words, wchunks;
@@ -159,7 +160,12 @@ Layout make_layout(int64_t n, int w, int kb, int tb, int algo) {
   L.o_done = take((size_t)(2 * L.r_max + 2) * 4);
   L.o_agg = take((size_t)2 * L.nchunks * sizeof(MC));
   L.o_tasks = take((size_t)L.max_tasks * 8);
-  L.o_mdesc = take((size_t)L.max_tasks * sizeof(MDesc));
+  // merge tasks <= sum over merge nodes of (span / tile + 1): merge_cost <= n * levels elements
+  // in tiles of >= 1792 (16-byte elements), plus one per merge node (<= r_max; peeksort:
+  // fused subtrees or >= 8-element average leaves).  Overflow is caught on the device.
+  L.mdesc_cap = (int64_t)levels * (n / 1792 + 1) + (algo == RS_ALGO_PEEKSORT ? n / 8 : L.r_max) + 64;
+  if (L.mdesc_cap > L.max_tasks) L.mdesc_cap = L.max_tasks;
+  L.o_mdesc = take((size_t)L.mdesc_cap * sizeof(MDesc));
   L.o_chunkdep = take((size_t)((L.r_max + kOrdChunkMin - 1) / kOrdChunkMin + 1) * kMaxDepth * 4);
   L.o_cls = take((size_t)(2 * L.r_max + 2));
   if (pk) {
@@ -342,7 +348,7 @@ ClassifyArgs classify_args(const WsView& V, const Layout& L, int64_t n, int w, i
                       runtime_merges, L.leaf_base,
                       V.leaf_start, V.leaf_info, V.leaf_depth, V.depth, V.node_s, V.node_e, V.parent, V.need,
                       V.cls, V.tasks, V.met, V.node_a, V.node_b, Exec<K, TB>::maxb_for(w), fuse_avg(), V.child,
-                      V.mdesc};
+                      V.mdesc, L.mdesc_cap};
 }
 
 // Phase A (fused subtrees, large leaves) + the merge executor.
@@ -402,6 +408,7 @@ int launch_exec(K* keys, void* tags, int64_t n, int w, int classic, int msuper, 
   M.done = V.done;
   M.tasks = V.tasks;
   M.mdesc = V.mdesc;
+  M.mdesc_cap = L.mdesc_cap;
   M.met = V.met;
   bool ahead = msuper > 1;
   if (const char* ov = getenv("RS_MERGE_AHEAD")) ahead = atoi(ov) != 0;  // tuning override
