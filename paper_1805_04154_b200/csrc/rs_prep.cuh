@@ -98,13 +98,9 @@ __global__ void __launch_bounds__(256, 3) k_prep(PrepArgs P) {
     if (blockIdx.x == 0) small_tree<256>(P.T, P.CA, P.F, smem_prep);
     return;
   }
-  // 5. node powers + ancestor-count scan (chunk aggregates); last block scans them
+  // 5. node powers + ancestor-count scan (chunk aggregates); each direction's last chunk scans them
   d_scan_reduce(P.T.leaf_start, P.n, P.F, const_cast<uint64_t*>(P.T.K), const_cast<uint8_t*>(P.T.P), met, P.agg,
-                P.nchunks);
-  if (last_block_done(&met->last_ctr[1])) {
-    d_scan_top(met, P.agg, P.nchunks, 0);
-    d_scan_top(met, P.agg, P.nchunks, 1);
-  }
+                P.nchunks, &met->last_ctr[3]);
   RS_ARR(met, 5);
   grid.sync();
   RS_TS(met, 5);

@@ -124,12 +124,19 @@ __device__ inline MC block_excl_scan_mc(MC v, MC* sm, MC* total) {
   return r;
 }
 
+__device__ void d_scan_top(const DevMetrics* __restrict__ met, MC* __restrict__ agg, int64_t nchunks_max, int dir);
+
 // Also computes the node powers (dir 0 writes K and P): P_j from leaf starts
-// s_{j-1}, s_j, s_{j+1} (sorters.py:414-423).
+// s_{j-1}, s_j, s_{j+1} (sorters.py:414-423).  The block that completes a
+// direction's last chunk aggregate scans that direction's aggregates
+// (d_scan_top), so the two directions' top scans run concurrently.
+// dir_ctr: two zeroed counters.
 __device__ void d_scan_reduce(const pos_t* __restrict__ leaf_start, pos_t n, int F, uint64_t* __restrict__ Kk,
                               uint8_t* __restrict__ P, const DevMetrics* __restrict__ met,
-                              MC* __restrict__ agg /* [2][nchunks_max] */, int64_t nchunks_max) {
+                              MC* __restrict__ agg /* [2][nchunks_max] */, int64_t nchunks_max,
+                              unsigned int* __restrict__ dir_ctr) {
   __shared__ MC sm[33];
+  __shared__ bool s_top;
   int64_t r = (int64_t)met->n_leaves;
   int64_t m = r - 1;
   if (m <= 0) {
@@ -172,7 +179,14 @@ __device__ void d_scan_reduce(const pos_t* __restrict__ leaf_start, pos_t n, int
       }
     }
     MC t = block_reduce_mc(v, sm);
-    if (threadIdx.x == 0) agg[dir * nchunks_max + ch] = t;
+    if (threadIdx.x == 0) {
+      agg[dir * nchunks_max + ch] = t;
+      __threadfence();
+      s_top = atomicAdd(&dir_ctr[dir], 1u) == (unsigned)(nch - 1);
+      if (s_top) __threadfence();
+    }
+    __syncthreads();
+    if (s_top) d_scan_top(met, agg, nchunks_max, dir);
     __syncthreads();
   }
 }
