@@ -88,3 +88,35 @@ def test_peeksort_config2_full():
     work, _, m = _run(a, 24, "bitonic")
     assert np.array_equal(work, ref_a)
     assert _mt(m) == ref.metrics_tuple()
+
+
+def _runs_array(rng, lens, key_dtype):
+    """Consecutive runs alternately ascending and strictly descending."""
+    parts = []
+    for i, L in enumerate(lens):
+        v = np.sort(rng.choice(1 << 30, size=int(L), replace=False))
+        parts.append(v if i % 2 == 0 else v[::-1])
+    return np.concatenate(parts).astype(key_dtype)
+
+
+@pytest.mark.parametrize("key_dtype", [np.int32, np.int64])
+def test_peeksort_long_descending_runs_vs_oracle(key_dtype):
+    """Few very long strictly descending runs (reversed by all blocks at once)
+    and many short ones (one block per segment); both pass through the
+    multi-level run-scan summaries."""
+    rng = np.random.default_rng(11)
+    cases = [
+        [1 << 18, 3, 1 << 19, 5, (1 << 18) + 7],          # 5 long runs, 2^20 elements
+        [int(x) for x in rng.integers(2, 3000, size=600)],  # > 64 descending runs per level
+        [1 << 20, 1 << 20],                                  # one ascending + one descending run
+    ]
+    for lens in cases:
+        a = _runs_array(rng, lens, key_dtype)
+        n = len(a)
+        tags = np.arange(n, dtype=np.int64)
+        for w in (1, 24):
+            ref_a, ref_t = a.copy(), tags.copy()
+            ref = oracle.peeksort(ref_a, w, "bitonic", ref_t)
+            work, tw, m = _run(a, w, "bitonic", tags)
+            assert np.array_equal(work, ref_a) and np.array_equal(tw, ref_t), (len(lens), w)
+            assert _mt(m) == ref.metrics_tuple(), (len(lens), w)
