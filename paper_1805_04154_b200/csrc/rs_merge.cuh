@@ -416,6 +416,11 @@ __global__ void __launch_bounds__(kMergeThreads, RS_MERGE_CTAS) k_merge_exec(Mer
       else if (diag == tot) split = na;
       if (lane == 0) RS_ACC(E.met, 1, tsrch);
       RS_T0(tiss);
+#ifndef RS_CLAIM_EARLY
+#define RS_CLAIM_EARLY 0  // 1: measured 1-2 us slower (a task claimed during the issue is held)
+#endif
+      // just in time, but the claim's atomic round trip overlaps this task's issue
+      if (!ahead && RS_CLAIM_EARLY) nxt.claim(E.met);
       bool merged = true;  // the reference performs this merge (Metrics)
       if (E.skipchk && kbeg == 0) {
         // sorters.py:545-550 / 575-578: one comparison; an in-order pair is not
@@ -520,7 +525,7 @@ __global__ void __launch_bounds__(kMergeThreads, RS_MERGE_CTAS) k_merge_exec(Mer
       }
       if (lane == 0) RS_ACC(E.met, 7, tiss);
       if (!ahead) {  // just in time: no task held ahead
-        nxt.claim(E.met);
+        if (!RS_CLAIM_EARLY) nxt.claim(E.met);
         nxt.finish(E, ntasks);
       }
       cur = nxt;
