@@ -122,6 +122,13 @@ __device__ __forceinline__ int64_t ceil_div64(int64_t a, int64_t b) {
   return (int64_t)udiv64((uint64_t)(a + b - 1), (uint64_t)b);
 }
 
+// Programmatic dependent launch: a kernel launched with the programmatic
+// stream-serialization attribute may start while its predecessor finishes;
+// pdl_wait() blocks until the predecessor grid has completed and its memory
+// is visible, pdl_trigger() lets this grid's dependent start launching.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ int bitlen64(uint64_t x) { return x ? 64 - __clzll((long long)x) : 0; }
 
 template <typename T>

@@ -927,6 +927,7 @@ __global__ void __launch_bounds__(kExecThreads, 3) k_phaseA(ExecArgs E) {
   __shared__ uint64_t s_rec;       // record of the task to run next (kind 3: none)
   __shared__ int32_t s_off[2];     // its span's offsets in buffer s_ib, if issued
   __shared__ int s_ib, s_issued;
+  pdl_wait();  // the prep's outputs are complete and visible
   const unsigned long long ntasks = E.met->phaseA;
   constexpr uint64_t kNone = ~0ull;
   // thread 0's view of the next task
@@ -965,7 +966,10 @@ __global__ void __launch_bounds__(kExecThreads, 3) k_phaseA(ExecArgs E) {
     uint64_t rec = s_rec;
     int ib = s_ib;
     int issued = s_issued;
-    if (rec == kNone) break;
+    if (rec == kNone) {
+      pdl_trigger();  // no more tasks for this CTA: k_merge_exec may start launching
+      break;
+    }
     uint32_t kind = task_kind(rec), id = task_id(rec), tile = task_tile(rec);
     __syncthreads();  // everyone has read the shared slots
     if (threadIdx.x == 0) {

@@ -327,6 +327,7 @@ __global__ void __launch_bounds__(kMergeThreads, RS_MERGE_CTAS) k_merge_exec(Mer
     mbar_fence_init();
   }
   __syncthreads();
+  pdl_wait();  // phase A (and the prep before it) complete and visible
   unsigned long long ntasks = E.met->n_tasks;
   // first merge task (after the phase-A tasks); not task_ctr, which other CTAs may already have advanced
   const unsigned long long t_first = E.met->phaseA;

@@ -95,6 +95,7 @@ __global__ void __launch_bounds__(256, 3) k_prep(PrepArgs P) {
   // small trees: phases 5-9 in block 0 alone, out of shared memory (rs_small.cuh)
   if ((int64_t)met->n_leaves <= kSmallR) {
     extern __shared__ __align__(16) unsigned char smem_prep[];
+    pdl_trigger();
     if (blockIdx.x == 0) small_tree<256>(P.T, P.CA, P.F, smem_prep);
     return;
   }
@@ -124,7 +125,8 @@ __global__ void __launch_bounds__(256, 3) k_prep(PrepArgs P) {
   RS_ARR(met, 8);
   grid.sync();
   RS_TS(met, 8);
-  // 9. task records
+  // 9. task records (k_phaseA may start launching: it waits for this grid to complete)
+  pdl_trigger();
   d_task_fill(P.CA, P.chunkdep);
   RS_ARR(met, 9);
   grid.sync();

@@ -240,6 +240,25 @@ int exec_grid(int sms, int w, int* grid_a, size_t* smem_a, int* grid_m, size_t* 
   return RS_OK;
 }
 
+// Launch with programmatic stream serialization: the kernel may start while
+// the previous kernel on the stream finishes (it calls pdl_wait() before
+// touching that kernel's outputs).  RS_NO_PDL=1 launches normally.
+template <typename Kern, typename Arg>
+cudaError_t pdl_launch(Kern kern, int grid, int block, size_t smem, cudaStream_t st, const Arg& arg) {
+  static const bool off = getenv("RS_NO_PDL") != nullptr;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = off ? 0 : 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, arg);
+}
+
 template <typename K>
 int prep_grid(int sms, size_t smem, int* grid) {
   static size_t cached_smem[64] = {0};
@@ -383,7 +402,8 @@ int launch_exec(K* keys, void* tags, int64_t n, int w, int classic, int msuper, 
   E.tasks = V.tasks;
   E.met = V.met;
   E.maxb = Exec<K, TB>::maxb_for(w);
-  k_phaseA<K, TB><<<grid_a, kExecThreads, smem_a, st>>>(E);
+  if (cudaError_t e_ = pdl_launch(k_phaseA<K, TB>, grid_a, kExecThreads, smem_a, st, E))
+    return fail(RS_ECUDA, std::string("k_phaseA launch failed: ") + cudaGetErrorString(e_));
   if (cudaError_t e_ = cudaGetLastError())
     return fail(RS_ECUDA, std::string("k_phaseA launch/exec failed: ") + cudaGetErrorString(e_));
   prof_mark(2, st);
@@ -412,8 +432,9 @@ int launch_exec(K* keys, void* tags, int64_t n, int w, int classic, int msuper, 
   M.met = V.met;
   bool ahead = msuper > 1;
   if (const char* ov = getenv("RS_MERGE_AHEAD")) ahead = atoi(ov) != 0;  // tuning override
-  if (ahead) k_merge_exec<K, TB, true><<<grid_m, kMergeThreads, smem_m, st>>>(M);
-  else k_merge_exec<K, TB, false><<<grid_m, kMergeThreads, smem_m, st>>>(M);
+  cudaError_t le = ahead ? pdl_launch(k_merge_exec<K, TB, true>, grid_m, kMergeThreads, smem_m, st, M)
+                         : pdl_launch(k_merge_exec<K, TB, false>, grid_m, kMergeThreads, smem_m, st, M);
+  if (le != cudaSuccess) return fail(RS_ECUDA, std::string("k_merge_exec launch failed: ") + cudaGetErrorString(le));
   if (cudaError_t e_ = cudaGetLastError())
     return fail(RS_ECUDA, std::string("k_merge_exec launch/exec failed: ") + cudaGetErrorString(e_));
   prof_mark(3, st);
