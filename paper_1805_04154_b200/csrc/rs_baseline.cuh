@@ -34,6 +34,7 @@ __global__ void __launch_bounds__(256) k_tree_tasks(ClassifyArgs CA, uint32_t* c
     d_order_scan(CA.met, chunkdep);
   }
   grid.sync();
+  pdl_trigger();  // k_phaseA may start launching (it waits for this grid)
   d_task_fill(CA, chunkdep);
 }
 

@@ -680,6 +680,7 @@ __global__ void __launch_bounds__(256, 2) k_peek(PeekArgs P) {
     d_order_scan(met, P.chunkdep);
   }
   grid.sync();
+  pdl_trigger();  // k_phaseA may start launching (it waits for this grid)
   d_task_fill(P.CA, P.chunkdep);
 }
 
