@@ -316,9 +316,20 @@ struct PeekOut {
   DevMetrics* met;
 };
 
+// Slot allocation on a shared counter, one atomic per group of converged lanes
+// (a wide level has thousands of items hitting the same four counters).
+__device__ __forceinline__ unsigned long long agg_inc(unsigned long long* ctr) {
+  const unsigned mask = __activemask();
+  const int lane = threadIdx.x & 31, leader = __ffs(mask) - 1;
+  unsigned long long base = 0;
+  if (lane == leader) base = atomicAdd(ctr, (unsigned long long)__popc(mask));
+  base = __shfl_sync(mask, base, leader);
+  return base + (unsigned long long)__popc(mask & ((1u << lane) - 1u));
+}
+
 __device__ __forceinline__ void peek_push(const PeekOut& O, pos_t l, pos_t r, pos_t e, pos_t s, bool ed, bool sd,
                                           uint32_t d) {
-  unsigned long long k = atomicAdd(O.next_cnt, 1ull);
+  unsigned long long k = agg_inc(O.next_cnt);
   if ((int64_t)k >= O.front_cap) { O.met->error = 2; return; }
   PeekItem it;
   it.l = l; it.r = r; it.e = e; it.s = s;
@@ -327,18 +338,18 @@ __device__ __forceinline__ void peek_push(const PeekOut& O, pos_t l, pos_t r, po
   O.next[k] = it;
 }
 __device__ __forceinline__ void peek_leaf(const PeekOut& O, pos_t l, pos_t r, pos_t npre, uint32_t d) {
-  unsigned long long k = atomicAdd(O.n_leaves, 1ull);
+  unsigned long long k = agg_inc(O.n_leaves);
   if ((int64_t)k >= O.rec_cap) { O.met->error = 2; return; }
   O.leaves[4 * k] = l; O.leaves[4 * k + 1] = r; O.leaves[4 * k + 2] = npre; O.leaves[4 * k + 3] = d;
 }
 __device__ __forceinline__ void peek_node(const PeekOut& O, pos_t l, pos_t mid, pos_t r, uint32_t d) {
-  unsigned long long k = atomicAdd(O.n_nodes, 1ull);
+  unsigned long long k = agg_inc(O.n_nodes);
   if ((int64_t)k >= O.rec_cap) { O.met->error = 2; return; }
   O.nodes[4 * k] = l; O.nodes[4 * k + 1] = mid; O.nodes[4 * k + 2] = r; O.nodes[4 * k + 3] = d;
 }
 __device__ __forceinline__ void peek_rev(const PeekOut& O, pos_t i, pos_t j) {
   if (j <= i) return;
-  unsigned long long k = atomicAdd(O.n_revs, 1ull);
+  unsigned long long k = agg_inc(O.n_revs);
   if ((int64_t)k >= O.rec_cap) { O.met->error = 2; return; }
   O.revs[2 * k] = i; O.revs[2 * k + 1] = j;
 }
