@@ -473,7 +473,7 @@ __device__ void reverse_segments(const PeekArgs& P, const pos_t* revs, int64_t n
   }
 }
 
-constexpr int kWordChunk = 4096;  // bitmap words per scan chunk
+constexpr int kWordChunk = 1024;  // bitmap words per scan chunk (a block scans its chunk in blockDim rounds)
 
 template <typename K, int TB>
 __global__ void __launch_bounds__(256, 2) k_peek(PeekArgs P) {
@@ -549,6 +549,7 @@ __global__ void __launch_bounds__(256, 2) k_peek(PeekArgs P) {
   O.front_cap = P.front_cap;
   O.rec_cap = P.rec_cap;
   O.met = met;
+  if (blockIdx.x == 0) RS_DBG(met, 1);
   // 1. first run (sorters.py:177) and the root call (:351-357)
   if (gtid == 0) {
     O.next = P.front[0];
@@ -563,6 +564,7 @@ __global__ void __launch_bounds__(256, 2) k_peek(PeekArgs P) {
     else peek_push(O, 0, n - 1, e0, n - 1, !desc, false, 0);
   }
   grid.sync();
+  if (blockIdx.x == 0) RS_DBG(met, 2);
   // 2. level-synchronous replay
   int cur = 0;
   unsigned long long rev_done = 0;
@@ -581,6 +583,7 @@ __global__ void __launch_bounds__(256, 2) k_peek(PeekArgs P) {
     cur ^= 1;
   }
   grid.sync();
+  if (blockIdx.x == 0) RS_DBG(met, 3);
   // 3. leaf-start bitmap and its word prefix popcount
   unsigned long long R = pc->n_leaves;
   unsigned long long NN = pc->n_nodes;
@@ -599,12 +602,16 @@ __global__ void __launch_bounds__(256, 2) k_peek(PeekArgs P) {
     __syncthreads();
   }
   grid.sync();
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    uint32_t run = 0;
-    for (int64_t c = 0; c < nchunks; ++c) {
-      uint32_t v = P.chunk[c];
-      P.chunk[c] = run;
-      run += v;
+  if (blockIdx.x == 0) {  // exclusive scan of the chunk sums: block scans of blockDim chunks
+    __shared__ uint32_t s_cs[40];
+    uint32_t carry = 0;
+    for (int64_t c0 = 0; c0 < nchunks; c0 += blockDim.x) {
+      int64_t c = c0 + threadIdx.x;
+      uint32_t v = c < nchunks ? P.chunk[c] : 0u;
+      uint32_t tot;
+      uint32_t ex = block_excl_scan_u32(v, s_cs, &tot);
+      if (c < nchunks) P.chunk[c] = carry + ex;
+      carry += tot;
     }
   }
   grid.sync();
@@ -623,6 +630,7 @@ __global__ void __launch_bounds__(256, 2) k_peek(PeekArgs P) {
     }
   }
   grid.sync();
+  if (blockIdx.x == 0) RS_DBG(met, 4);
   // 4. leaves and nodes onto leaf / boundary indices
   TreeArrays& T = P.T;
   pos_t* leaf_start = const_cast<pos_t*>(T.leaf_start);
@@ -653,6 +661,7 @@ __global__ void __launch_bounds__(256, 2) k_peek(PeekArgs P) {
   comps = block_sum(comps + V.comps, sred);
   if (threadIdx.x == 0 && comps) atomicAdd(&met->comparisons, comps);
   grid.sync();
+  if (blockIdx.x == 0) RS_DBG(met, 5);
   // 5. parents and children from depths (a child's parent is the deeper of the
   //    boundaries at its span's two ends)
   for (int64_t i = gtid; i < (int64_t)R; i += gthreads) {
@@ -682,6 +691,7 @@ __global__ void __launch_bounds__(256, 2) k_peek(PeekArgs P) {
     }
   }
   grid.sync();
+  if (blockIdx.x == 0) RS_DBG(met, 6);
   // 6. classification (no detection term: peeksort counted its scans above),
   //    ordered task list -- shared with powersort.
   d_classify(P.CA, P.chunkdep);

@@ -956,7 +956,8 @@ int rs_debug_counters(int key_dtype, int tag_bytes, int64_t n, int32_t min_run_l
                       int cap) {
   if (n <= 1 || !workspace || !out) return 0;
   int kb = key_dtype == RS_KEY_I64 ? 8 : 4;
-  Layout L = make_layout(n, min_run_len, kb, tag_bytes, RS_ALGO_POWERSORT);
+  const char* da = getenv("RS_DEBUG_ALGO");  // instrumentation: the layout of another algorithm's workspace
+  Layout L = make_layout(n, min_run_len, kb, tag_bytes, da ? atoi(da) : RS_ALGO_POWERSORT);
   DevMetrics hm;
   RS_CUDA(cudaDeviceSynchronize());
   RS_CUDA(cudaMemcpy(&hm, reinterpret_cast<unsigned char*>(workspace) + L.o_met, sizeof(DevMetrics),

@@ -9,6 +9,7 @@ ap.add_argument('--config', type=int, default=2)
 ap.add_argument('--n', type=int, default=None)
 ap.add_argument('--reps', type=int, default=3)
 ap.add_argument('--w', type=int, default=24)
+ap.add_argument('--algo', type=int, default=0)
 a = ap.parse_args()
 keys, tags = workloads.generate(a.config, a.n)
 L = _lib.lib()
@@ -19,14 +20,14 @@ twork = torch.empty_like(tsrc) if tsrc is not None else None
 kc = _lib.RS_KEY_I32 if keys.itemsize == 4 else _lib.RS_KEY_I64
 tb = tags.itemsize if tags is not None else 0
 n = len(keys)
-wsb = L.rs_workspace_bytes(0, kc, tb, n, a.w)
+wsb = L.rs_workspace_bytes(a.algo, kc, tb, n, a.w)
 ws = torch.empty(wsb, dtype=torch.uint8, device=dev)
 st = torch.cuda.current_stream()
 for i in range(a.reps):
     work.copy_(src)
     if twork is not None: twork.copy_(tsrc)
     m = _lib.RsMetrics()
-    _lib.check(L.rs_sort(0, kc, work.data_ptr(), tb, twork.data_ptr() if twork is not None else None, n, a.w, 0,
+    _lib.check(L.rs_sort(a.algo, kc, work.data_ptr(), tb, twork.data_ptr() if twork is not None else None, n, a.w, 0,
                          ws.data_ptr(), wsb, st.cuda_stream, ctypes.byref(m), None))
 torch.cuda.synchronize()
 print('ok', m.merge_cost, m.runs_detected)
@@ -35,7 +36,7 @@ if __import__('os').environ.get('RS_LIB'):
     k = L.rs_debug_counters(kc, tb, n, a.w, ws.data_ptr(), buf, 202)
     ts = list(buf[138:154]); print('prep phase us', [round((ts[i] - ts[i-1]) / 1e3, 1) for i in range(1, 12) if ts[i] and ts[i-1]])
     arr = list(buf[154:170]); print('phase work (latest arrival - prev exit) / barrier (exit - latest arrival) us', [(i, round((arr[i] - ts[i-1]) / 1e3, 1), round((ts[i] - arr[i]) / 1e3, 1)) for i in range(1, 10) if arr[i] and ts[i] and ts[i-1]])
-    dbg = list(buf[170:202]); t4 = ts[8]; print('dbg us after ts8', [(i, round((dbg[i] - t4) / 1e3, 1)) for i in range(32) if dbg[i]])
+    dbg = list(buf[170:202]); t4 = min([x for x in dbg if x] or [0]); print('dbg us after first dbg', [(i, round((dbg[i] - t4) / 1e3, 1)) for i in range(32) if dbg[i]])
     print('ts us after ts4', [(i, round((ts[i] - t4) / 1e3, 1)) for i in range(4, 12) if ts[i]])
     print('phase-1 max-warp cycles wait/bits/bwords/walk', ts[12:16])
     dw = list(buf[10:74]); dt = list(buf[74:138])
