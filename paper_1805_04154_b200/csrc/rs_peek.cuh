@@ -57,9 +57,10 @@ struct PeekArgs {
 
 // Extra per-call counters live in the metrics struct's spare fields.
 struct PeekCounters {
-  unsigned long long front_n[2];
+  unsigned long long front_n[3];
   unsigned long long n_nodes, n_leaves, n_revs;
 };
+static_assert(sizeof(PeekCounters) <= sizeof(((DevMetrics*)nullptr)->peek), "PeekCounters live in DevMetrics::peek");
 
 __device__ __forceinline__ uint32_t ascword(const uint32_t* asc, int64_t q, int v) {
   uint32_t x = __ldcg(asc + q);
@@ -566,21 +567,28 @@ __global__ void __launch_bounds__(256, 2) k_peek(PeekArgs P) {
   grid.sync();
   if (blockIdx.x == 0) RS_DBG(met, 2);
   // 2. level-synchronous replay
-  int cur = 0;
+  // Level L evaluates front[L & 1] (count front_n[L % 3]) and pushes into
+  // front[(L+1) & 1] / front_n[(L+1) % 3]; front_n[(L+2) % 3] was last read at
+  // level L-1, so thread 0 clears it now and one barrier per level suffices
+  // (plus one after a level's reversals, whose keys the next evaluations read).
+  int lev = 0;
   unsigned long long rev_done = 0;
   for (;;) {
     unsigned long long nrev = *(volatile unsigned long long*)&pc->n_revs;
-    if (nrev > rev_done) reverse_segments<K, TB>(P, P.revs + 2 * rev_done, (int64_t)(nrev - rev_done));
-    rev_done = nrev;
-    unsigned long long cnt = *(volatile unsigned long long*)&pc->front_n[cur];
+    if (nrev > rev_done) {
+      reverse_segments<K, TB>(P, P.revs + 2 * rev_done, (int64_t)(nrev - rev_done));
+      rev_done = nrev;
+      grid.sync();
+    }
+    unsigned long long cnt = *(volatile unsigned long long*)&pc->front_n[lev % 3];
     if (cnt == 0) break;
-    if (gtid == 0) pc->front_n[cur ^ 1] = 0;
+    if (gtid == 0) pc->front_n[(lev + 2) % 3] = 0;
+    O.next = P.front[(lev + 1) & 1];
+    O.next_cnt = &pc->front_n[(lev + 1) % 3];
+    const PeekItem* items = P.front[lev & 1];
+    for (int64_t x = gtid; x < (int64_t)cnt; x += gthreads) peek_item<K>(V, items[x], P.w, O);
     grid.sync();
-    O.next = P.front[cur ^ 1];
-    O.next_cnt = &pc->front_n[cur ^ 1];
-    for (int64_t x = gtid; x < (int64_t)cnt; x += gthreads) peek_item<K>(V, P.front[cur][x], P.w, O);
-    grid.sync();
-    cur ^= 1;
+    ++lev;
   }
   grid.sync();
   if (blockIdx.x == 0) RS_DBG(met, 3);
