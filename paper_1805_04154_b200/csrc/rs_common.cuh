@@ -13,9 +13,15 @@ constexpr int kWarp = 32;
 constexpr pos_t kInf = INT64_MAX / 4;
 
 // ---- chain (min-run) phase ----
-constexpr int kChainT = 2048;      // positions per chain tile
+#ifndef RS_CHAIN_T
+#define RS_CHAIN_T 2048
+#endif
+constexpr int kChainT = RS_CHAIN_T;  // positions per chain tile
 constexpr int kChainThreads = 256;
-constexpr int kChainGroup = 64;    // tiles per composition group
+#ifndef RS_CHAIN_GROUP
+#define RS_CHAIN_GROUP 64
+#endif
+constexpr int kChainGroup = RS_CHAIN_GROUP;  // tiles per composition group
 constexpr int kTableBatch = 32;    // tables staged into smem per batch
 
 // ---- executor ----
