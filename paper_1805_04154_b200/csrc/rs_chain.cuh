@@ -72,16 +72,16 @@ __device__ __forceinline__ pos_t chain_next(pos_t p, pos_t ne, int w, pos_t n) {
 
 // Window of words [q0, q1) for chain tile `tile`.
 __device__ __forceinline__ void chain_window(int64_t tile, pos_t n, int w, int64_t* q0, int64_t* q1,
-                                             pos_t* t0, pos_t* t1) {
-  *t0 = tile * (pos_t)kChainT;
-  *t1 = (*t0 + kChainT < n) ? *t0 + kChainT : n;
+                                             pos_t* t0, pos_t* t1, int ct = kChainT) {
+  *t0 = tile * (pos_t)ct;
+  *t1 = (*t0 + ct < n) ? *t0 + ct : n;
   int64_t total_words = (n + 31) >> 5;
   *q0 = *t0 == 0 ? 0 : ((*t0 - 1) >> 5);
   int64_t e = ((*t1 + w + 64) >> 5) + 1;
   *q1 = e < total_words ? e : total_words;
 }
 
-__host__ __device__ constexpr int kMaxWinWords(int w) { return (kChainT + w + 96) / 32 + 4; }
+__host__ __device__ constexpr int kMaxWinWords(int w, int ct = kChainT) { return (ct + w + 96) / 32 + 4; }
 
 // K1+K2a: pair-type bits for this tile (written to ascw) and the tile's
 // candidate table.  One CTA per chain tile.
@@ -154,26 +154,26 @@ __device__ void d_scan_table_tile(const K* __restrict__ a, pos_t n, int w, uint3
 // a warp-private shared-memory slice with one 1D bulk copy (mbarrier
 // completion), derives the pair-type bits and B-words there, and its lanes
 // walk the w+1 candidates.  16+ tiles are in flight per SM.
-__host__ __device__ inline int chain_win_bytes(int w, int kb) {
-  return ((kChainT + w + 192) * kb + 16 + 127) / 128 * 128;
+__host__ __device__ inline int chain_win_bytes(int w, int kb, int ct = kChainT) {
+  return ((ct + w + 192) * kb + 16 + 127) / 128 * 128;
 }
-__host__ __device__ inline int chain_warp_bytes(int w, int kb) {
-  int maxw = kMaxWinWords(w);
-  return chain_win_bytes(w, kb) + ((maxw * 8 + maxw * 2 + 127) / 128) * 128;
+__host__ __device__ inline int chain_warp_bytes(int w, int kb, int ct = kChainT) {
+  int maxw = kMaxWinWords(w, ct);
+  return chain_win_bytes(w, kb, ct) + ((maxw * 8 + maxw * 2 + 127) / 128) * 128;
 }
 
 #ifndef RS_BITS_LPW
 #define RS_BITS_LPW 1
 #endif
 template <typename K>
-__device__ void d_scan_tables_tma(const K* __restrict__ a, pos_t n, int w, uint32_t* __restrict__ ascw,
-                                  uint2* __restrict__ tables, int64_t ntiles, DevMetrics* imet = nullptr) {
+__device__ __forceinline__ void d_scan_tables_tma(const K* __restrict__ a, pos_t n, int w, uint32_t* __restrict__ ascw,
+                                  uint2* __restrict__ tables, int64_t ntiles, int ct, DevMetrics* imet = nullptr) {
   extern __shared__ __align__(128) unsigned char smem_tab[];
   __shared__ __align__(8) uint64_t kbar[32];
   int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  int maxw = kMaxWinWords(w);
-  unsigned char* kbuf = smem_tab + (size_t)wid * chain_warp_bytes(w, sizeof(K));
-  uint32_t* asc = reinterpret_cast<uint32_t*>(kbuf + chain_win_bytes(w, sizeof(K)));
+  int maxw = kMaxWinWords(w, ct);
+  unsigned char* kbuf = smem_tab + (size_t)wid * chain_warp_bytes(w, sizeof(K), ct);
+  uint32_t* asc = reinterpret_cast<uint32_t*>(kbuf + chain_win_bytes(w, sizeof(K), ct));
   uint32_t* bw = asc + maxw;
   uint16_t* nz = reinterpret_cast<uint16_t*>(bw + maxw);
   if (lane == 0) {
@@ -190,7 +190,7 @@ __device__ void d_scan_tables_tma(const K* __restrict__ a, pos_t n, int w, uint3
   auto issue = [&](int64_t tl) -> int32_t {
     pos_t u0, u1;
     int64_t r0, r1;
-    chain_window(tl, n, w, &r0, &r1, &u0, &u1);
+    chain_window(tl, n, w, &r0, &r1, &u0, &u1, ct);
     pos_t e0 = 32 * r0, e1 = 32 * r1 + 1 < n ? 32 * r1 + 1 : n;
     int32_t ko = 0;
     if (lane == 0) {
@@ -211,7 +211,7 @@ __device__ void d_scan_tables_tma(const K* __restrict__ a, pos_t n, int w, uint3
 #endif
     pos_t t0, t1;
     int64_t q0, q1;
-    chain_window(tile, n, w, &q0, &q1, &t0, &t1);
+    chain_window(tile, n, w, &q0, &q1, &t0, &t1, ct);
     int nwords = int(q1 - q0);
     const int32_t koff = koff_next;
     mbar_wait(&kbar[wid], ph);
@@ -443,18 +443,18 @@ __device__ void d_tile_entries(const uint2* __restrict__ tables, int64_t ntiles,
 
 // K2e: one warp per tile re-walks the chain from the tile's true entry and emits
 // leaves: start position and info = min(natural run length, w) | desc << 31.
-__device__ void d_emit_tile(const uint32_t* __restrict__ ascw, pos_t n, int w, const uint32_t* __restrict__ tentry,
+__device__ __forceinline__ void d_emit_tile(const uint32_t* __restrict__ ascw, pos_t n, int w, const uint32_t* __restrict__ tentry,
                             const uint64_t* __restrict__ toff, int64_t r_max, pos_t* __restrict__ leaf_start,
-                            uint32_t* __restrict__ leaf_info, int64_t tile) {
+                            uint32_t* __restrict__ leaf_info, int64_t tile, int ct) {
   extern __shared__ uint32_t smem_u32[];
   int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  int maxw = kMaxWinWords(w);
+  int maxw = kMaxWinWords(w, ct);
   uint32_t* asc = smem_u32 + (size_t)wid * (maxw * 2 + (maxw + 1) / 2 + 1);
   uint32_t* bw = asc + maxw;
   uint16_t* nz = reinterpret_cast<uint16_t*>(bw + maxw);
   pos_t t0, t1;
   int64_t q0, q1;
-  chain_window(tile, n, w, &q0, &q1, &t0, &t1);
+  chain_window(tile, n, w, &q0, &q1, &t0, &t1, ct);
   int nwords = int(q1 - q0);
   {
     uint32_t v[4];

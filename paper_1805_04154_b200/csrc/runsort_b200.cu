@@ -72,10 +72,19 @@ int fail(int code, const std::string& msg) {
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+// Positions per chain tile: 2048 (measured best for cfg2 / cfg4); below ~7M
+// keys that leaves most prep warps without a tile, and 1024 is faster
+// (cfg1, n = 2^20: -9%).  A function of n only, so every layout agrees.
+inline int chain_tile_for(int64_t n) {  // k_prep is instantiated for 1024 and 2048
+  if (const char* ov = getenv("RS_CHAIN_TILE")) return atoi(ov) >= 2048 ? 2048 : 1024;  // tuning override
+  return n < (int64_t)2048 * 3552 ? 1024 : 2048;
+}
+
 struct Layout {
   // inputs
   int64_t n;
   int w, kb, tb;
+  int chain_t;  // positions per chain tile
   int tile, fcap;
   // derived sizes
   int64_t words, ntiles, ngroups, r_max, nchunks, max_tasks;
@@ -112,7 +121,8 @@ Layout make_layout(int64_t n, int w, int kb, int tb, int algo) {
   L.fcap = exec_fcap(kb, tb);
   if (const char* ov = getenv("RS_FCAP")) L.fcap = std::max(2, std::min(L.fcap, atoi(ov)));  // tuning override
   L.words = (n + 31) / 32 + 2;
-  L.ntiles = (n + kChainT - 1) / kChainT;
+  L.chain_t = chain_tile_for(n);
+  L.ntiles = (n + L.chain_t - 1) / L.chain_t;
   L.ngroups = (L.ntiles + kChainGroup - 1) / kChainGroup;
   int64_t minleaf = w > 2 ? w : 2;
   if (algo == RS_ALGO_TOP_DOWN) minleaf = (w + 1) / 2;  // halves of ranges > w
@@ -259,16 +269,16 @@ cudaError_t pdl_launch(Kern kern, int grid, int block, size_t smem, cudaStream_t
   return cudaLaunchKernelEx(&cfg, kern, arg);
 }
 
-template <typename K>
+template <typename K, int CT>
 int prep_grid(int sms, size_t smem, int* grid) {
   static size_t cached_smem[64] = {0};
   static int cached_occ[64] = {0};
   int dev;
   RS_CUDA(cudaGetDevice(&dev));
   if (cached_smem[dev] != smem) {
-    RS_CUDA(cudaFuncSetAttribute(k_prep<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    RS_CUDA(cudaFuncSetAttribute(k_prep<K, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int o = 0;
-    RS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_prep<K>, 256, smem));
+    RS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_prep<K, CT>, 256, smem));
     if (o < 1) return fail(RS_ECUDA, "prep kernel does not fit on an SM");
     cached_occ[dev] = o;
     cached_smem[dev] = smem;
@@ -451,14 +461,15 @@ int run_powersort(K* keys, void* tags, int64_t n, int w, int classic, unsigned c
   prof_set_met(V.met);
   // everything before the executors in one cooperative kernel
   int W1 = w + 1;
-  int maxw = kMaxWinWords(w);
+  const int ct = L.chain_t;
+  int maxw = kMaxWinWords(w, ct);
   int batch = (int)((40 * 1024 - (size_t)W1 * 8) / ((size_t)W1 * 8));
   if (batch < 1) batch = 1;
   if (batch > kTableBatch) batch = kTableBatch;
   int gbatch = (int)(40 * 1024 / ((size_t)W1 * 8));
   if (gbatch < 1) gbatch = 1;
   int tbatch = gbatch < kChainGroup ? gbatch : kChainGroup;
-  size_t sm = 8 * (size_t)chain_warp_bytes(w, sizeof(K));
+  size_t sm = 8 * (size_t)chain_warp_bytes(w, sizeof(K), ct);
   sm = std::max(sm, (size_t)kFillSmem + 64);
   sm = std::max(sm, (size_t)batch * W1 * 8 + (size_t)W1 * 8 + 64);
   sm = std::max(sm, (size_t)gbatch * W1 * 8);
@@ -496,12 +507,13 @@ int run_powersort(K* keys, void* tags, int64_t n, int w, int classic, unsigned c
   int msuper = merge_super<K, TB>(n, sms);
   PA.CA = classify_args<K, TB>(V, L, n, w, classic, msuper, 0);
   int grid_p;
-  if (int e = prep_grid<K>(sms, sm, &grid_p)) return e;
+  void* kprep = ct == 1024 ? (void*)k_prep<K, 1024> : (void*)k_prep<K, 2048>;
+  if (int e = (ct == 1024 ? prep_grid<K, 1024>(sms, sm, &grid_p) : prep_grid<K, 2048>(sms, sm, &grid_p))) return e;
   void* kargs[] = {&PA};
-  RS_CUDA(cudaLaunchCooperativeKernel((void*)k_prep<K>, dim3(grid_p), dim3(256), kargs, sm, st));
+  RS_CUDA(cudaLaunchCooperativeKernel(kprep, dim3(grid_p), dim3(256), kargs, sm, st));
 #ifdef RS_INSTR
   if (getenv("RS_PREP_TWICE"))  // experiment: a second, warm-code prep (idempotent)
-    RS_CUDA(cudaLaunchCooperativeKernel((void*)k_prep<K>, dim3(grid_p), dim3(256), kargs, sm, st));
+    RS_CUDA(cudaLaunchCooperativeKernel(kprep, dim3(grid_p), dim3(256), kargs, sm, st));
 #endif
   if (leaves_only) return RS_OK;
   prof_mark(1, st);
