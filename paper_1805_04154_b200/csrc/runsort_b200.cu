@@ -72,12 +72,17 @@ int fail(int code, const std::string& msg) {
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-// Positions per chain tile: 2048 (measured best for cfg2 / cfg4); below ~7M
-// keys that leaves most prep warps without a tile, and 1024 is faster
-// (cfg1, n = 2^20: -9%).  A function of n only, so every layout agrees.
-inline int chain_tile_for(int64_t n) {  // k_prep is instantiated for 1024 and 2048
-  if (const char* ov = getenv("RS_CHAIN_TILE")) return atoi(ov) >= 2048 ? 2048 : 1024;  // tuning override
-  return n < (int64_t)2048 * 3552 ? 1024 : 2048;
+// Positions per chain tile (k_prep is instantiated for 1024, 2048 and 2560):
+// below ~7M keys 2048-position tiles leave most prep warps without a tile and
+// 1024 is faster (cfg1, n = 2^20: -9%); from ~12M keys 2560 balances the
+// warps' tile counts better.  A function of n only, so every layout agrees.
+inline int chain_tile_for(int64_t n) {
+  if (const char* ov = getenv("RS_CHAIN_TILE")) {  // tuning override
+    int v = atoi(ov);
+    return v >= 2560 ? 2560 : (v >= 2048 ? 2048 : 1024);
+  }
+  if (n < (int64_t)2048 * 3552) return 1024;
+  return n < (int64_t)12000000 ? 2048 : 2560;  // 2560 from ~12M keys: cfg3 -4 us, cfg4 -30 us (cfg2 even)
 }
 
 struct Layout {
@@ -507,8 +512,11 @@ int run_powersort(K* keys, void* tags, int64_t n, int w, int classic, unsigned c
   int msuper = merge_super<K, TB>(n, sms);
   PA.CA = classify_args<K, TB>(V, L, n, w, classic, msuper, 0);
   int grid_p;
-  void* kprep = ct == 1024 ? (void*)k_prep<K, 1024> : (void*)k_prep<K, 2048>;
-  if (int e = (ct == 1024 ? prep_grid<K, 1024>(sms, sm, &grid_p) : prep_grid<K, 2048>(sms, sm, &grid_p))) return e;
+  void* kprep = ct == 1024 ? (void*)k_prep<K, 1024> : ct == 2560 ? (void*)k_prep<K, 2560> : (void*)k_prep<K, 2048>;
+  if (int e = (ct == 1024   ? prep_grid<K, 1024>(sms, sm, &grid_p)
+               : ct == 2560 ? prep_grid<K, 2560>(sms, sm, &grid_p)
+                            : prep_grid<K, 2048>(sms, sm, &grid_p)))
+    return e;
   void* kargs[] = {&PA};
   RS_CUDA(cudaLaunchCooperativeKernel(kprep, dim3(grid_p), dim3(256), kargs, sm, st));
 #ifdef RS_INSTR
