@@ -101,6 +101,14 @@ int rs_sort_ex(int algo, int key_dtype, void* keys, int tag_bytes, void* tags, i
 int rs_fetch_metrics(int algo, int key_dtype, int tag_bytes, int64_t n, int32_t min_run_len,
                      void* workspace, void* stream, rs_metrics* out);
 
+/* Merge-tree export of the last rs_sort that used `workspace` (same algo, n,
+ * dtypes, min_run_len), for SortConfig.record_tree when the caller sizes the
+ * host arrays by the leaf count r instead of n: call once with
+ * tree->capacity == 0 to read r into tree->n_leaves, then again with
+ * capacity >= r.  Synchronizes `stream`.  Powersort and peeksort only. */
+int rs_export_tree(int algo, int key_dtype, int tag_bytes, int64_t n, int32_t min_run_len, void* workspace,
+                   void* stream, rs_tree* tree);
+
 /* Host-buffer convenience entry (what a plain ctypes binding of the reference
  * would call with numpy arrays): allocates device memory, copies in, sorts,
  * copies back, frees.  Synchronous. */
@@ -122,7 +130,9 @@ int rs_profile_read(double* ms, int cap);
 int rs_debug_counters(int key_dtype, int tag_bytes, int64_t n, int32_t min_run_len, void* workspace,
                       uint64_t* out, int cap);
 
-/* Largest min_run_len the device path accepts for this element type. */
+/* Largest min_run_len the device path accepts for this element type (the
+ * fused-subtree capacity, lowered for 8-byte keys so that the run-detection
+ * kernel's per-warp windows fit in shared memory at every n). */
 int32_t rs_max_min_run_len(int key_dtype, int tag_bytes);
 
 /* Input format of the reference's generators (gen.py:210-236 save_array /

@@ -12,6 +12,7 @@
 //   7. k_execute       persistent dataflow executor (leaves + merges)
 #include <algorithm>
 #include <functional>
+#include <map>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -72,17 +73,73 @@ int fail(int code, const std::string& msg) {
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+// Tuning overrides (environment), read once per process: the product path
+// never calls getenv per sort (thread-safe static initialisation).
+struct Tunables {
+  int chain_tile = 0;    // RS_CHAIN_TILE: force 1024 / 2048 / 2560-position chain tiles
+  int fcap = 0;          // RS_FCAP: cap the fused-subtree size
+  int merge_super = 0;   // RS_MERGE_SUPER: tiles per merge task
+  int fuse_avg = 256;    // RS_FUSE_AVG: fuse subtrees when n < fuse_avg * r
+  int merge_ahead = -1;  // RS_MERGE_AHEAD: claim-ahead merge producer (-1 = from msuper)
+  bool no_pdl = false;   // RS_NO_PDL: plain launches instead of programmatic dependent launch
+  bool prep_twice = false;  // RS_PREP_TWICE (RS_INSTR builds): a second, warm-code prep
+  int debug_algo = -1;   // RS_DEBUG_ALGO: rs_debug_counters reads another algorithm's layout
+};
+const Tunables& tun() {
+  static const Tunables t = [] {
+    Tunables v;
+    auto geti = [](const char* k, int d) {
+      const char* e = getenv(k);
+      return e ? atoi(e) : d;
+    };
+    v.chain_tile = geti("RS_CHAIN_TILE", 0);
+    v.fcap = geti("RS_FCAP", 0);
+    v.merge_super = geti("RS_MERGE_SUPER", 0);
+    v.fuse_avg = geti("RS_FUSE_AVG", 256);
+    v.merge_ahead = geti("RS_MERGE_AHEAD", -1);
+    v.no_pdl = getenv("RS_NO_PDL") != nullptr;
+    v.prep_twice = getenv("RS_PREP_TWICE") != nullptr;
+    v.debug_algo = geti("RS_DEBUG_ALGO", -1);
+    return v;
+  }();
+  return t;
+}
+
+constexpr size_t kMaxSmemPerBlock = 227 * 1024;
+
+// Dynamic shared memory of k_prep for (w, key bytes, chain tile).
+size_t prep_smem_bytes(int w, int kb, int ct) {
+  int W1 = w + 1;
+  int maxw = kMaxWinWords(w, ct);
+  int batch = (int)((40 * 1024 - (size_t)W1 * 8) / ((size_t)W1 * 8));
+  if (batch < 1) batch = 1;
+  if (batch > kTableBatch) batch = kTableBatch;
+  int gbatch = (int)(40 * 1024 / ((size_t)W1 * 8));
+  if (gbatch < 1) gbatch = 1;
+  int tbatch = gbatch < kChainGroup ? gbatch : kChainGroup;
+  size_t sm = 8 * (size_t)chain_warp_bytes(w, kb, ct);
+  sm = std::max(sm, (size_t)kFillSmem + 64);
+  sm = std::max(sm, (size_t)batch * W1 * 8 + (size_t)W1 * 8 + 64);
+  sm = std::max(sm, (size_t)gbatch * W1 * 8);
+  sm = std::max(sm, (size_t)tbatch * W1 * 8);
+  sm = std::max(sm, (size_t)8 * (maxw * 2 + (maxw + 1) / 2 + 1) * 4);
+  sm = std::max(sm, small_smem_bytes());
+  return sm;
+}
+
 // Positions per chain tile (k_prep is instantiated for 1024, 2048 and 2560):
 // below ~7M keys 2048-position tiles leave most prep warps without a tile and
 // 1024 is faster (cfg1, n = 2^20: -9%); from ~12M keys 2560 balances the
 // warps' tile counts better.  A function of n only, so every layout agrees.
-inline int chain_tile_for(int64_t n) {
-  if (const char* ov = getenv("RS_CHAIN_TILE")) {  // tuning override
-    int v = atoi(ov);
-    return v >= 2560 ? 2560 : (v >= 2048 ? 2048 : 1024);
-  }
-  if (n < (int64_t)2048 * 3552) return 1024;
-  return n < (int64_t)12000000 ? 2048 : 2560;  // 2560 from ~12M keys: cfg3 -4 us, cfg4 -30 us (cfg2 even)
+// Large min_run_len values step the tile down until the prep's per-warp
+// windows fit in shared memory (a function of (n, w, key bytes) only).
+inline int chain_tile_for(int64_t n, int w, int kb) {
+  int ct;
+  if (int v = tun().chain_tile) ct = v >= 2560 ? 2560 : (v >= 2048 ? 2048 : 1024);  // tuning override
+  else if (n < (int64_t)2048 * 3552) ct = 1024;
+  else ct = n < (int64_t)12000000 ? 2048 : 2560;  // 2560 from ~12M keys: cfg3 -4 us, cfg4 -30 us (cfg2 even)
+  while (ct > 1024 && prep_smem_bytes(w, kb, ct) > kMaxSmemPerBlock) ct = ct == 2560 ? 2048 : 1024;
+  return ct;
 }
 
 struct Layout {
@@ -124,9 +181,9 @@ Layout make_layout(int64_t n, int w, int kb, int tb, int algo) {
   L.tb = tb;
   L.tile = exec_tile(kb, tb);
   L.fcap = exec_fcap(kb, tb);
-  if (const char* ov = getenv("RS_FCAP")) L.fcap = std::max(2, std::min(L.fcap, atoi(ov)));  // tuning override
+  if (int v = tun().fcap) L.fcap = std::max(2, std::min(L.fcap, v));  // tuning override
   L.words = (n + 31) / 32 + 2;
-  L.chain_t = chain_tile_for(n);
+  L.chain_t = chain_tile_for(n, w, kb);
   L.ntiles = (n + L.chain_t - 1) / L.chain_t;
   L.ngroups = (L.ntiles + kChainGroup - 1) / kChainGroup;
   int64_t minleaf = w > 2 ? w : 2;
@@ -223,35 +280,58 @@ int device_sms(int* sms) {
   return RS_OK;
 }
 
-template <typename K, int TB>
-int exec_grid(int sms, int w, int* grid_a, size_t* smem_a, int* grid_m, size_t* smem_m) {
-  static int occ_a[64] = {0}, occ_m[64] = {0};
-  static size_t occ_a_smem[64] = {0};
+// Per-device launch geometry, computed once under g_mu.  The shared-memory
+// attribute of a kernel only ever grows (concurrent sorts with different
+// min_run_len on other threads never see it shrink under their launch), and
+// occupancies are cached per (device, shared-memory size).
+struct OccKey {
+  const void* fn;
+  int dev;
+  size_t smem;
+  bool operator<(const OccKey& o) const {
+    return fn != o.fn ? fn < o.fn : (dev != o.dev ? dev < o.dev : smem < o.smem);
+  }
+};
+std::map<OccKey, int> g_occ;                         // guarded by g_mu
+std::map<std::pair<const void*, int>, size_t> g_attr;  // guarded by g_mu
+
+int occupancy(const void* fn, int threads, size_t smem, size_t attr_smem, int* occ, const char* what) {
   int dev;
   RS_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_mu);
+  size_t& cur = g_attr[{fn, dev}];
+  size_t want = std::max(smem, attr_smem);
+  if (want > cur) {
+    RS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)want));
+    cur = want;
+  }
+  auto it = g_occ.find(OccKey{fn, dev, smem});
+  if (it == g_occ.end()) {
+    int o = 0;
+    RS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, threads, smem));
+    if (o < 1) return fail(RS_ECUDA, std::string(what) + " does not fit on an SM");
+    it = g_occ.emplace(OccKey{fn, dev, smem}, o).first;
+  }
+  *occ = it->second;
+  return RS_OK;
+}
+
+template <typename K, int TB>
+int exec_grid(int sms, int w, int* grid_a, size_t* smem_a, int* grid_m, size_t* smem_m) {
   *smem_a = Exec<K, TB>::smem_bytes(w);
   *smem_m = MergeCfg<K, TB>::SMEM;
-  if (occ_m[dev] == 0) {
-    RS_CUDA(cudaFuncSetAttribute(k_phaseA<K, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)Exec<K, TB>::smem_bytes(1)));
-    RS_CUDA(cudaFuncSetAttribute(k_merge_exec<K, TB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)*smem_m));
-    RS_CUDA(cudaFuncSetAttribute(k_merge_exec<K, TB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)*smem_m));
-    int o = 0;
-    RS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_merge_exec<K, TB, false>, kMergeThreads, *smem_m));
-    if (o < 1) return fail(RS_ECUDA, "merge executor does not fit on an SM");
-    occ_m[dev] = o;
-  }
-  if (occ_a_smem[dev] != *smem_a) {
-    int o = 0;
-    RS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_phaseA<K, TB>, kExecThreads, *smem_a));
-    if (o < 1) return fail(RS_ECUDA, "phase-A kernel does not fit on an SM");
-    occ_a[dev] = o;
-    occ_a_smem[dev] = *smem_a;
-  }
-  *grid_a = sms * occ_a[dev];
-  *grid_m = sms * occ_m[dev];
+  int oa, om, om2;
+  if (int e = occupancy((const void*)k_phaseA<K, TB>, kExecThreads, *smem_a, Exec<K, TB>::smem_bytes(1), &oa,
+                        "phase-A kernel"))
+    return e;
+  if (int e = occupancy((const void*)k_merge_exec<K, TB, false>, kMergeThreads, *smem_m, *smem_m, &om,
+                        "merge executor"))
+    return e;
+  if (int e = occupancy((const void*)k_merge_exec<K, TB, true>, kMergeThreads, *smem_m, *smem_m, &om2,
+                        "merge executor"))
+    return e;
+  *grid_a = sms * oa;
+  *grid_m = sms * std::min(om, om2);
   return RS_OK;
 }
 
@@ -260,7 +340,7 @@ int exec_grid(int sms, int w, int* grid_a, size_t* smem_a, int* grid_m, size_t* 
 // touching that kernel's outputs).  RS_NO_PDL=1 launches normally.
 template <typename Kern, typename Arg>
 cudaError_t pdl_launch(Kern kern, int grid, int block, size_t smem, cudaStream_t st, const Arg& arg) {
-  static const bool off = getenv("RS_NO_PDL") != nullptr;
+  const bool off = tun().no_pdl;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(block);
@@ -276,19 +356,9 @@ cudaError_t pdl_launch(Kern kern, int grid, int block, size_t smem, cudaStream_t
 
 template <typename K, int CT>
 int prep_grid(int sms, size_t smem, int* grid) {
-  static size_t cached_smem[64] = {0};
-  static int cached_occ[64] = {0};
-  int dev;
-  RS_CUDA(cudaGetDevice(&dev));
-  if (cached_smem[dev] != smem) {
-    RS_CUDA(cudaFuncSetAttribute(k_prep<K, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int o = 0;
-    RS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_prep<K, CT>, 256, smem));
-    if (o < 1) return fail(RS_ECUDA, "prep kernel does not fit on an SM");
-    cached_occ[dev] = o;
-    cached_smem[dev] = smem;
-  }
-  *grid = sms * cached_occ[dev];
+  int o;
+  if (int e = occupancy((const void*)k_prep<K, CT>, 256, smem, smem, &o, "prep kernel")) return e;
+  *grid = sms * o;
   return RS_OK;
 }
 
@@ -300,7 +370,7 @@ int merge_super(int64_t n, int sms) {
   int64_t ctas = (int64_t)sms * 3;
   int64_t per_level_tiles = n / MergeCfg<K, TB>::TILE;
   int64_t s = per_level_tiles / (8 * ctas);
-  if (const char* ov = getenv("RS_MERGE_SUPER")) s = atoi(ov);  // tuning override
+  if (int v = tun().merge_super) s = v;  // tuning override
   if (s < 1) s = 1;
   if (s > 7) s = 7;
   return (int)s;
@@ -370,10 +440,7 @@ TreeArrays tree_arrays(const WsView& V, const Layout& L) {
 // Fused phase-A subtrees only for short leaves on average (measured on B200:
 // cfg1's 24-element leaves gain 2x from fusing, cfg2/cfg4's ~1-3K-element runs
 // merge faster in the executor).
-int fuse_avg() {
-  if (const char* ov = getenv("RS_FUSE_AVG")) return atoi(ov);  // tuning override
-  return 256;
-}
+int fuse_avg() { return tun().fuse_avg; }
 
 template <typename K, int TB>
 ClassifyArgs classify_args(const WsView& V, const Layout& L, int64_t n, int w, int classic, int msuper, int peek,
@@ -446,7 +513,7 @@ int launch_exec(K* keys, void* tags, int64_t n, int w, int classic, int msuper, 
   M.mdesc_cap = L.mdesc_cap;
   M.met = V.met;
   bool ahead = msuper > 1;
-  if (const char* ov = getenv("RS_MERGE_AHEAD")) ahead = atoi(ov) != 0;  // tuning override
+  if (tun().merge_ahead >= 0) ahead = tun().merge_ahead != 0;  // tuning override
   cudaError_t le = ahead ? pdl_launch(k_merge_exec<K, TB, true>, grid_m, kMergeThreads, smem_m, st, M)
                          : pdl_launch(k_merge_exec<K, TB, false>, grid_m, kMergeThreads, smem_m, st, M);
   if (le != cudaSuccess) return fail(RS_ECUDA, std::string("k_merge_exec launch failed: ") + cudaGetErrorString(le));
@@ -465,22 +532,16 @@ int run_powersort(K* keys, void* tags, int64_t n, int w, int classic, unsigned c
   prof_mark(0, st);
   prof_set_met(V.met);
   // everything before the executors in one cooperative kernel
-  int W1 = w + 1;
   const int ct = L.chain_t;
-  int maxw = kMaxWinWords(w, ct);
+  int W1 = w + 1;
   int batch = (int)((40 * 1024 - (size_t)W1 * 8) / ((size_t)W1 * 8));
   if (batch < 1) batch = 1;
   if (batch > kTableBatch) batch = kTableBatch;
   int gbatch = (int)(40 * 1024 / ((size_t)W1 * 8));
   if (gbatch < 1) gbatch = 1;
   int tbatch = gbatch < kChainGroup ? gbatch : kChainGroup;
-  size_t sm = 8 * (size_t)chain_warp_bytes(w, sizeof(K), ct);
-  sm = std::max(sm, (size_t)kFillSmem + 64);
-  sm = std::max(sm, (size_t)batch * W1 * 8 + (size_t)W1 * 8 + 64);
-  sm = std::max(sm, (size_t)gbatch * W1 * 8);
-  sm = std::max(sm, (size_t)tbatch * W1 * 8);
-  sm = std::max(sm, (size_t)8 * (maxw * 2 + (maxw + 1) / 2 + 1) * 4);
-  sm = std::max(sm, small_smem_bytes());
+  size_t sm = prep_smem_bytes(w, (int)sizeof(K), ct);
+  if (sm > kMaxSmemPerBlock) return fail(RS_EUNSUPPORTED, "min_run_len too large for the prep kernel's shared memory");
   int F = n <= ((int64_t)1 << 31) ? 32 : 63;
   int64_t nch_max = (L.r_max + kOrdChunkMin - 1) / kOrdChunkMin;
   PrepArgs PA;
@@ -520,7 +581,7 @@ int run_powersort(K* keys, void* tags, int64_t n, int w, int classic, unsigned c
   void* kargs[] = {&PA};
   RS_CUDA(cudaLaunchCooperativeKernel(kprep, dim3(grid_p), dim3(256), kargs, sm, st));
 #ifdef RS_INSTR
-  if (getenv("RS_PREP_TWICE"))  // experiment: a second, warm-code prep (idempotent)
+  if (tun().prep_twice)  // experiment: a second, warm-code prep (idempotent)
     RS_CUDA(cudaLaunchCooperativeKernel(kprep, dim3(grid_p), dim3(256), kargs, sm, st));
 #endif
   if (leaves_only) return RS_OK;
@@ -721,19 +782,11 @@ int run_baseline(int algo, K* keys, void* tags, int64_t n, int w, int classic, d
   int64_t nch_max = (L.r_max + kOrdChunkMin - 1) / kOrdChunkMin;
   (void)nch_max;
   size_t sm = (size_t)kFillSmem + 64;
-  static int occ[64] = {0};
-  int dev;
-  RS_CUDA(cudaGetDevice(&dev));
-  if (occ[dev] == 0) {
-    RS_CUDA(cudaFuncSetAttribute(k_tree_tasks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    int o = 0;
-    RS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_tree_tasks, 256, sm));
-    if (o < 1) return fail(RS_ECUDA, "task-list kernel does not fit on an SM");
-    occ[dev] = o;
-  }
+  int occ;
+  if (int e = occupancy((const void*)k_tree_tasks, 256, sm, sm, &occ, "task-list kernel")) return e;
   uint32_t* cd = V.chunkdep;
   void* kargs[] = {&CA, &cd};
-  RS_CUDA(cudaLaunchCooperativeKernel((void*)k_tree_tasks, dim3(sms * occ[dev]), dim3(256), kargs, sm, st));
+  RS_CUDA(cudaLaunchCooperativeKernel((void*)k_tree_tasks, dim3(sms * occ), dim3(256), kargs, sm, st));
   prof_mark(1, st);
   return launch_exec<K, TB>(keys, tags, n, w, classic, msuper, V, L, sms, st, fixed ? 1 : 0);
 }
@@ -776,18 +829,10 @@ int run_peeksort(K* keys, void* tags, int64_t n, int w, int classic, unsigned ch
   PK.done = V.done;
   PK.done_words = 2 * L.r_max + 2;
   size_t sm = (size_t)kFillSmem + 64;
-  static int occ[64] = {0};
-  int dev;
-  RS_CUDA(cudaGetDevice(&dev));
-  if (occ[dev] == 0) {
-    RS_CUDA(cudaFuncSetAttribute(k_peek<K, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    int o = 0;
-    RS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_peek<K, TB>, 256, sm));
-    if (o < 1) return fail(RS_ECUDA, "peeksort kernel does not fit on an SM");
-    occ[dev] = o;
-  }
+  int occ;
+  if (int e = occupancy((const void*)k_peek<K, TB>, 256, sm, sm, &occ, "peeksort kernel")) return e;
   void* kargs[] = {&PK};
-  RS_CUDA(cudaLaunchCooperativeKernel((void*)k_peek<K, TB>, dim3(sms * occ[dev]), dim3(256), kargs, sm, st));
+  RS_CUDA(cudaLaunchCooperativeKernel((void*)k_peek<K, TB>, dim3(sms * occ), dim3(256), kargs, sm, st));
   prof_mark(1, st);
   return launch_exec<K, TB>(keys, tags, n, w, classic, msuper, V, L, sms, st);
 }
@@ -805,6 +850,9 @@ int validate(int algo, int key_dtype, int tag_bytes, int64_t n, int32_t w, int32
   if (w > exec_fcap(*kb, tag_bytes))
     return fail(RS_EUNSUPPORTED, "min_run_len exceeds the device path's fused-subtree capacity");
   if (n >= ((int64_t)1 << 40)) return fail(RS_EUNSUPPORTED, "n >= 2^40 is not supported");
+  if (algo != RS_ALGO_PEEKSORT && algo != RS_ALGO_TOP_DOWN && algo != RS_ALGO_BOTTOM_UP && n > 1 &&
+      prep_smem_bytes(w, *kb, chain_tile_for(n, w, *kb)) > kMaxSmemPerBlock)
+    return fail(RS_EUNSUPPORTED, "min_run_len exceeds the run-detection kernel's shared-memory capacity");
   return RS_OK;
 }
 
@@ -931,6 +979,30 @@ int rs_fetch_metrics(int algo, int key_dtype, int tag_bytes, int64_t n, int32_t 
   return read_metrics(L, reinterpret_cast<unsigned char*>(workspace), reinterpret_cast<cudaStream_t>(stream), out);
 }
 
+int rs_export_tree(int algo, int key_dtype, int tag_bytes, int64_t n, int32_t min_run_len, void* workspace,
+                   void* stream, rs_tree* tree) {
+  if (!tree) return fail(RS_EINVAL, "null tree");
+  if (algo != RS_ALGO_POWERSORT && algo != RS_ALGO_PEEKSORT)
+    return fail(RS_EUNSUPPORTED, "the baseline sorters record no merge tree");
+  if (n <= 1) {
+    tree->n_leaves = n;
+    if (n == 1 && tree->capacity >= 1 && tree->leaf_len) tree->leaf_len[0] = 1;
+    return RS_OK;
+  }
+  int kb = key_dtype == RS_KEY_I64 ? 8 : 4;
+  Layout L = make_layout(n, min_run_len, kb, tag_bytes, algo);
+  unsigned char* ws = reinterpret_cast<unsigned char*>(workspace);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (tree->capacity == 0) {  // size query: n_leaves only
+    DevMetrics hm;
+    RS_CUDA(cudaMemcpyAsync(&hm, ws + L.o_met, sizeof(DevMetrics), cudaMemcpyDeviceToHost, st));
+    RS_CUDA(cudaStreamSynchronize(st));
+    tree->n_leaves = (int64_t)hm.n_leaves;
+    return RS_OK;
+  }
+  return export_tree(L, ws, st, tree);
+}
+
 int rs_sort_host(int algo, int key_dtype, void* keys, int tag_bytes, void* tags, int64_t n, int32_t min_run_len,
                  int32_t merge_kind, rs_metrics* out, rs_tree* tree) {
   int kb;
@@ -976,8 +1048,8 @@ int rs_debug_counters(int key_dtype, int tag_bytes, int64_t n, int32_t min_run_l
                       int cap) {
   if (n <= 1 || !workspace || !out) return 0;
   int kb = key_dtype == RS_KEY_I64 ? 8 : 4;
-  const char* da = getenv("RS_DEBUG_ALGO");  // instrumentation: the layout of another algorithm's workspace
-  Layout L = make_layout(n, min_run_len, kb, tag_bytes, da ? atoi(da) : RS_ALGO_POWERSORT);
+  int da = tun().debug_algo;  // instrumentation: the layout of another algorithm's workspace
+  Layout L = make_layout(n, min_run_len, kb, tag_bytes, da >= 0 ? da : RS_ALGO_POWERSORT);
   DevMetrics hm;
   RS_CUDA(cudaDeviceSynchronize());
   RS_CUDA(cudaMemcpy(&hm, reinterpret_cast<unsigned char*>(workspace) + L.o_met, sizeof(DevMetrics),
@@ -995,7 +1067,10 @@ int rs_debug_counters(int key_dtype, int tag_bytes, int64_t n, int32_t min_run_l
 }
 
 int32_t rs_max_min_run_len(int key_dtype, int tag_bytes) {
-  return exec_fcap(key_dtype == RS_KEY_I64 ? 8 : 4, tag_bytes);
+  int kb = key_dtype == RS_KEY_I64 ? 8 : 4;
+  int w = exec_fcap(kb, tag_bytes);
+  while (w > 1 && prep_smem_bytes(w, kb, 1024) > kMaxSmemPerBlock) --w;  // smallest chain tile
+  return w;
 }
 
 int rs_profile(int enable) {

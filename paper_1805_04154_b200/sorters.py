@@ -114,19 +114,21 @@ _SIGNED = {np.dtype(np.int32): _lib.RS_KEY_I32, np.dtype(np.int64): _lib.RS_KEY_
 
 
 class _Staged:
-    """A contiguous CUDA int32/int64 view of the caller's keys or tags, plus
-    the write-back needed to land the result in the caller's object."""
+    """A contiguous CUDA int32/int64 view of the caller's keys or tags on
+    device `dev`, plus the write-back that lands the result in the caller's
+    object (numpy array, CPU tensor, or a CUDA tensor that could not be
+    sorted in place)."""
 
-    def __init__(self, obj, is_keys: bool):
+    def __init__(self, obj, is_keys: bool, dev, stream):
         torch = _torch()
         self.obj = obj
-        self.dev_t = None
-        self.writeback = None
         self.flip = None
+        self.host_out = None
         if isinstance(obj, torch.Tensor):
             self.is_torch = True
-            t = obj
-            npdt = np.dtype(str(t.dtype).replace("torch.", "")) if t.dtype not in (torch.bool,) else np.dtype(bool)
+            if obj.dim() != 1:
+                raise ValueError("expected a one-dimensional tensor")
+            npdt = np.dtype(str(obj.dtype).replace("torch.", "")) if obj.dtype != torch.bool else np.dtype(bool)
         else:
             self.is_torch = False
             arr = np.asarray(obj)
@@ -140,13 +142,9 @@ class _Staged:
             if npdt.itemsize not in (4, 8):
                 raise NotImplementedError("tags must have a 4- or 8-byte dtype")
             self.kind, self.code = "raw", npdt.itemsize
-        dev = torch.device("cuda", torch.cuda.current_device())
-        stream = torch.cuda.current_stream(dev)
+        self.on_host = not (self.is_torch and obj.device.type == "cuda")
         if self.is_torch:
             t = obj
-            if t.dim() != 1:
-                raise ValueError("expected a one-dimensional tensor")
-            base = t
             if t.device.type != "cuda":
                 d = t.to(dev, non_blocking=t.is_pinned())
             elif not t.is_contiguous():
@@ -156,10 +154,7 @@ class _Staged:
         else:
             arr = np.ascontiguousarray(np.asarray(obj))
             d = torch.from_numpy(arr).to(dev)
-            base = None
-        d = self._to_work(d)
-        self.dev_t = d
-        self.base = base
+        self.dev_t = self._to_work(d)
         self.stream = stream
 
     def _key_plan(self, npdt):
@@ -194,7 +189,7 @@ class _Staged:
             return d.view(torch.int64) ^ torch.tensor(-(1 << 63), dtype=torch.int64, device=d.device)
         raise AssertionError(self.kind)
 
-    def finish(self):
+    def _result(self):
         torch = _torch()
         d = self.dev_t
         if self.kind == "widen":
@@ -203,60 +198,114 @@ class _Staged:
             d = (d ^ torch.tensor(-(1 << 31), dtype=torch.int32, device=d.device)).view(torch.uint32)
         elif self.kind == "flip64":
             d = (d ^ torch.tensor(-(1 << 63), dtype=torch.int64, device=d.device)).view(torch.uint64)
+        return d
+
+    def finish_device(self):
+        """Device-side write-back (CUDA tensors the sort could not run in place on)."""
+        if self.on_host:
+            return
+        d = self._result()
+        t = self.obj
+        if d.data_ptr() != t.data_ptr() or d.dtype != t.dtype:
+            if d.dtype != t.dtype:
+                d = d.view(t.dtype) if d.element_size() == t.element_size() else d.to(t.dtype)
+            t.copy_(d)
+
+    def queue_host_copy(self):
+        """Queue the device-to-host copy of the result into a staging buffer the
+        caller does not see (numpy inputs); nothing for other inputs."""
+        if not self.on_host or self.is_torch:
+            return
+        torch = _torch()
+        d = self._result()
+        self.host_out = torch.empty(d.shape, dtype=d.dtype, pin_memory=True)
+        self.host_out.copy_(d, non_blocking=True)
+
+    def finish_host(self):
+        """Host write-back, called once the device reported no error: numpy
+        arrays get the staged result, CPU tensors a copy straight into them."""
+        if not self.on_host:
+            return
         if self.is_torch:
+            d = self._result()
             t = self.obj
-            if d.data_ptr() != t.data_ptr() or d.dtype != t.dtype:
-                if d.dtype != t.dtype:
-                    d = d.view(t.dtype) if d.element_size() == t.element_size() else d.to(t.dtype)
-                t.copy_(d, non_blocking=t.device.type == "cpu" and t.is_pinned())
-        else:
-            host = d.cpu().numpy()
-            arr = self.obj
-            if host.dtype != arr.dtype:
-                host = host.view(arr.dtype) if host.itemsize == arr.dtype.itemsize else host.astype(arr.dtype)
-            arr[...] = host
+            if d.dtype != t.dtype:
+                d = d.view(t.dtype) if d.element_size() == t.element_size() else d.to(t.dtype)
+            t.copy_(d, non_blocking=t.is_pinned())
+            return
+        host = self.host_out.numpy()
+        arr = self.obj
+        if host.dtype != arr.dtype:
+            host = host.view(arr.dtype) if host.itemsize == arr.dtype.itemsize else host.astype(arr.dtype)
+        arr[...] = host
+
+
+def _target_device(a, tags):
+    """The device the sort runs on: the keys' CUDA device, else the current one.
+    CUDA tags must live on that same device."""
+    torch = _torch()
+    if isinstance(a, torch.Tensor) and a.device.type == "cuda":
+        dev = a.device
+    else:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    if isinstance(tags, torch.Tensor) and tags.device.type == "cuda" and tags.device != dev:
+        raise ValueError(f"tags are on {tags.device} but the keys sort on {dev}")
+    return dev
 
 
 def _device_sort(algo: int, a, cfg: SortConfig, metrics: Metrics, tags) -> Metrics:
+    torch = _torch()
+    dev = _target_device(a, tags)
+    with torch.cuda.device(dev):
+        return _device_sort_on(algo, a, cfg, metrics, tags, dev)
+
+
+def _device_sort_on(algo: int, a, cfg: SortConfig, metrics: Metrics, tags, dev) -> Metrics:
     L = _lib.lib()
     torch = _torch()
-    keys = _Staged(a, True)
+    stream = torch.cuda.current_stream(dev)
+    keys = _Staged(a, True, dev, stream)
     n = keys.n
     tg = None
     if tags is not None:
-        tg = _Staged(tags, False)
+        tg = _Staged(tags, False, dev, stream)
         if tg.n != n:
             raise ValueError("tags must have the same length as the keys")
     w = int(cfg.min_run_len)
     kind = _lib.RS_MERGE_CLASSIC if cfg.merge_kind == "classic" else _lib.RS_MERGE_BITONIC
     tb = tg.code if tg is not None else 0
     ws_bytes = L.rs_workspace_bytes(algo, keys.code, tb, n, w)
-    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=keys.dev_t.device)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
     out = _lib.RsMetrics()
-    tree = None
-    bufs = None
-    if cfg.record_tree and n > 1 and algo in (_lib.RS_ALGO_POWERSORT, _lib.RS_ALGO_PEEKSORT):
-        cap = n
-        bufs = (np.zeros(cap, dtype=np.int64), np.zeros(cap, dtype=np.uint8), np.zeros(cap, dtype=np.uint8))
-        tree = _lib.RsTree(cap, 0, bufs[0].ctypes.data, bufs[1].ctypes.data, bufs[2].ctypes.data)
-    # Without a tree export the sort is enqueued without a host sync, the
-    # write-back (D2H for host inputs) is queued behind it on the same stream,
-    # and one synchronizing Metrics fetch ends the call: no bubble between the
-    # last kernel and the copy back.
+    # The sort is enqueued without a host sync; numpy results are copied back
+    # into a staging buffer queued behind it, and one synchronizing Metrics
+    # fetch follows.  Only when the device reported no invariant failure is
+    # the caller's host object overwritten (CUDA tensors are sorted in place).
     rc = L.rs_sort_ex(algo, keys.code, keys.dev_t.data_ptr(), tb,
                       tg.dev_t.data_ptr() if tg is not None else None, n, w, kind, float(cfg.alpha),
-                      ws.data_ptr(), ws_bytes, keys.stream.cuda_stream,
-                      ctypes.byref(out) if tree is not None else None,
-                      ctypes.byref(tree) if tree is not None else None)
+                      ws.data_ptr(), ws_bytes, stream.cuda_stream, None, None)
     _lib.check(rc)
-    keys.finish()
-    if tg is not None:
-        tg.finish()
-    if tree is None:
-        _lib.check(L.rs_fetch_metrics(algo, keys.code, tb, n, w, ws.data_ptr(), keys.stream.cuda_stream,
-                                      ctypes.byref(out)))
-    if keys.is_torch and keys.obj.device.type == "cpu":
-        keys.stream.synchronize()
+    staged = [keys] + ([tg] if tg is not None else [])
+    for s_ in staged:
+        s_.finish_device()
+        s_.queue_host_copy()
+    _lib.check(L.rs_fetch_metrics(algo, keys.code, tb, n, w, ws.data_ptr(), stream.cuda_stream,
+                                  ctypes.byref(out)))
+    tree = None
+    if cfg.record_tree and algo in (_lib.RS_ALGO_POWERSORT, _lib.RS_ALGO_PEEKSORT):
+        # host arrays sized by the leaf count r (not n): query r, then export
+        probe = _lib.RsTree(0, 0, None, None, None)
+        _lib.check(L.rs_export_tree(algo, keys.code, tb, n, w, ws.data_ptr(), stream.cuda_stream,
+                                    ctypes.byref(probe)))
+        r = int(probe.n_leaves)
+        bufs = (np.zeros(r, dtype=np.int64), np.zeros(r, dtype=np.uint8), np.zeros(r, dtype=np.uint8))
+        tree = _lib.RsTree(r, 0, bufs[0].ctypes.data, bufs[1].ctypes.data, bufs[2].ctypes.data)
+        _lib.check(L.rs_export_tree(algo, keys.code, tb, n, w, ws.data_ptr(), stream.cuda_stream,
+                                    ctypes.byref(tree)))
+    for s_ in staged:
+        s_.finish_host()
+    if any(s_.on_host for s_ in staged):
+        stream.synchronize()  # non-blocking copies into pinned CPU tensors have landed
     metrics.merge_cost += int(out.merge_cost)
     metrics.comparisons += int(out.comparisons)
     if algo == _lib.RS_ALGO_PEEKSORT:

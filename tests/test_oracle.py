@@ -97,3 +97,48 @@ def test_node_powers_match_reference(golden):
     for s1, e1, s2, e2, n, p in meta["node_powers"]:
         assert oracle.node_power_def(s1, e1, s2, e2, n) == p
         assert oracle.node_power0(s1 - 1, e1 - 1, s2 - 1, e2 - 1, n) == p
+
+
+# --------------------------------------------------------------- analytic
+def test_analytic_node_powers_match_reference(golden):
+    """oracle/analytic.py's node_power_def / node_power0 vs the reference's own
+    node_power_def outputs (including n = 2^31, where powersort uses the loop)."""
+    from oracle import analytic
+
+    meta, _ = golden
+    big = 0
+    for s1, e1, s2, e2, n, p in meta["node_powers"]:
+        assert analytic.node_power_def(s1, e1, s2, e2, n) == p
+        assert analytic.node_power0(s1 - 1, e1 - 1, s2 - 1, e2 - 1, n) == p
+        big += n >= 1 << 31
+    assert big > 0
+
+
+def test_analytic_metrics_match_oracle():
+    """Metrics from the run structure alone == the element-by-element oracle,
+    on inputs with duplicates, strictly descending runs and short runs."""
+    from oracle import analytic
+
+    rng = np.random.default_rng(11)
+    for it in range(300):
+        n = int(rng.integers(2, 3000))
+        kind = it % 4
+        if kind == 0:
+            a = rng.integers(0, 5, n)
+        elif kind == 1:
+            a = rng.integers(0, 1 << 40, n)
+            b = np.sort(rng.choice(n, size=min(n - 1, int(rng.integers(1, 40))), replace=False))
+            for s, e in zip(np.r_[0, b], np.r_[b, n]):
+                a[s:e] = np.sort(a[s:e])[:: (1 if rng.random() < 0.5 else -1)]
+        elif kind == 2:
+            a = np.arange(n)[:: -1].copy()
+        else:
+            a = np.repeat(rng.integers(0, 100, n // 7 + 1), 7)[:n]
+        a = a.astype(np.int64)
+        w = int(rng.choice([1, 2, 3, 7, 24, 100]))
+        got = analytic.powersort_metrics_numpy(a, w)
+        res = oracle.powersort(a.copy(), w, "bitonic", want_tree=True)
+        assert (got["merge_cost"], got["comparisons"], got["runs_detected"], got["max_stack_height"]) == \
+            res.metrics_tuple(), (it, n, w)
+        assert np.array_equal(got["leaf_starts"], res.leaf_starts)
+        assert np.array_equal(got["powers"], res.powers)
