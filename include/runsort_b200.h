@@ -144,6 +144,43 @@ int32_t rs_max_min_run_len(int key_dtype, int tag_bytes);
  * RS_EIO: the file cannot be opened. */
 int rs_load_bin(const char* path, int64_t* n_out, void* dst, int64_t capacity, void* stream);
 
+/* ---- Arrays that span GPUs ----
+ * W <= 8 sorted shards, each given by a device pointer that may be local or a
+ * peer GPU's buffer mapped over NVLink (rs_ipc_open), and a range [lo, hi).
+ * The global order is (key, shard index, position): the stable order of the
+ * shards' concatenation in index order, as the reference's left-wins merges
+ * define it (runcore.py:262-263). */
+typedef struct {
+  const void* keys;
+  const void* tags; /* NULL when tag_bytes == 0 */
+  int64_t lo, hi;
+} rs_shard;
+
+/* Exact co-rank: for each global rank targets[b] in [0, sum(hi - lo)], the
+ * split out[b * w + i] = absolute position in shard i such that shard i's
+ * elements [lo_i, out[b*w+i]) are exactly the first targets[b] elements of the
+ * global order.  Workspace: device memory of >= ntargets * 8 * (1 + w) + 512
+ * bytes.  Synchronizes `stream`. */
+int rs_corank(int key_dtype, const rs_shard* shards, int w, const int64_t* targets, int ntargets,
+              int64_t* out, void* workspace, size_t ws_bytes, void* stream);
+
+/* Stable w-way merge of the shard ranges into out_keys (+ out_tags), length
+ * sum(hi - lo), ties to the lower shard index.  Reads the shards through their
+ * pointers (peer memory included) and writes the output once.  Asynchronous on
+ * `stream`. */
+size_t rs_kway_workspace_bytes(int key_dtype, int tag_bytes, const rs_shard* shards, int w);
+int rs_kway_merge(int key_dtype, int tag_bytes, const rs_shard* shards, int w, void* out_keys, void* out_tags,
+                  void* workspace, size_t ws_bytes, void* stream);
+
+/* CUDA IPC for the peer-mapped shards: rs_ipc_alloc allocates `bytes` of device
+ * memory and writes its 64-byte IPC handle; another process on the node maps it
+ * with rs_ipc_open (peer access enabled lazily) and unmaps with rs_ipc_close;
+ * the owner frees with rs_ipc_free. */
+int rs_ipc_alloc(size_t bytes, void** ptr, void* handle);
+int rs_ipc_open(const void* handle, void** ptr);
+int rs_ipc_close(void* ptr);
+int rs_ipc_free(void* ptr);
+
 /* Thread-local message for the last non-RS_OK return. */
 const char* rs_last_error(void);
 

@@ -20,7 +20,8 @@ RS_EIO = 6
 
 # every symbol include/runsort_b200.h declares
 EXPORTS = ("rs_workspace_bytes", "rs_sort", "rs_sort_ex", "rs_fetch_metrics", "rs_sort_host", "rs_export_tree", "rs_profile",
-           "rs_profile_read", "rs_debug_counters", "rs_max_min_run_len", "rs_load_bin", "rs_last_error",
+           "rs_profile_read", "rs_debug_counters", "rs_max_min_run_len", "rs_load_bin", "rs_corank", "rs_kway_workspace_bytes", "rs_kway_merge",
+           "rs_ipc_alloc", "rs_ipc_open", "rs_ipc_close", "rs_ipc_free", "rs_last_error",
            "rs_version")
 
 
@@ -33,6 +34,11 @@ class RsTree(ctypes.Structure):
     _fields_ = [("capacity", ctypes.c_int64), ("n_leaves", ctypes.c_int64),
                 ("leaf_len", ctypes.c_void_p), ("node_power", ctypes.c_void_p),
                 ("node_depth", ctypes.c_void_p)]
+
+
+class RsShard(ctypes.Structure):
+    _fields_ = [("keys", ctypes.c_void_p), ("tags", ctypes.c_void_p), ("lo", ctypes.c_int64),
+                ("hi", ctypes.c_int64)]
 
 
 _lib = None
@@ -78,6 +84,23 @@ def lib():
         L.rs_load_bin.restype = ctypes.c_int
         L.rs_load_bin.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_int64), ctypes.c_void_p, ctypes.c_int64,
                                   ctypes.c_void_p]
+        L.rs_corank.restype = ctypes.c_int
+        L.rs_corank.argtypes = [ctypes.c_int, ctypes.POINTER(RsShard), ctypes.c_int, ctypes.POINTER(ctypes.c_int64),
+                                ctypes.c_int, ctypes.POINTER(ctypes.c_int64), ctypes.c_void_p, ctypes.c_size_t,
+                                ctypes.c_void_p]
+        L.rs_kway_workspace_bytes.restype = ctypes.c_size_t
+        L.rs_kway_workspace_bytes.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.POINTER(RsShard), ctypes.c_int]
+        L.rs_kway_merge.restype = ctypes.c_int
+        L.rs_kway_merge.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.POINTER(RsShard), ctypes.c_int, ctypes.c_void_p,
+                                    ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]
+        L.rs_ipc_alloc.restype = ctypes.c_int
+        L.rs_ipc_alloc.argtypes = [ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p), ctypes.c_void_p]
+        L.rs_ipc_open.restype = ctypes.c_int
+        L.rs_ipc_open.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p)]
+        L.rs_ipc_close.restype = ctypes.c_int
+        L.rs_ipc_close.argtypes = [ctypes.c_void_p]
+        L.rs_ipc_free.restype = ctypes.c_int
+        L.rs_ipc_free.argtypes = [ctypes.c_void_p]
         L.rs_last_error.restype = ctypes.c_char_p
         L.rs_last_error.argtypes = []
         L.rs_version.restype = ctypes.c_int

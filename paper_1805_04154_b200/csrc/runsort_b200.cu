@@ -25,6 +25,7 @@
 #include "rs_chain.cuh"
 #include "rs_common.cuh"
 #include "rs_exec.cuh"
+#include "rs_kway.cuh"
 #include "rs_merge.cuh"
 #include "rs_prep.cuh"
 #include "rs_peek.cuh"
@@ -912,9 +913,183 @@ int dispatch_tags(int algo, K* keys, int tb, void* tags, int64_t n, int w, int c
   return run_powersort<K, 8>(keys, tags, n, w, classic, ws, L, st);
 }
 
+// ------------------------------------------------ cross-GPU merge (rs_kway.cuh)
+int load_shards(const rs_shard* shards, int w, int tag_bytes, KwayShards* S) {
+  if (w < 1 || w > kKwayMaxW) return fail(RS_EINVAL, "between 1 and 8 shards");
+  if (!shards) return fail(RS_EINVAL, "null shard list");
+  memset(S, 0, sizeof(*S));
+  S->w = w;
+  for (int i = 0; i < w; ++i) {
+    if (shards[i].hi < shards[i].lo || shards[i].lo < 0) return fail(RS_EINVAL, "shard range must satisfy 0 <= lo <= hi");
+    if (shards[i].hi > shards[i].lo && !shards[i].keys) return fail(RS_EINVAL, "null shard keys");
+    if (tag_bytes && shards[i].hi > shards[i].lo && !shards[i].tags) return fail(RS_EINVAL, "null shard tags");
+    S->keys[i] = shards[i].keys;
+    S->tags[i] = shards[i].tags;
+    S->lo[i] = shards[i].lo;
+    S->hi[i] = shards[i].hi;
+  }
+  return RS_OK;
+}
+
+struct KwayLayout {
+  int64_t spacing, npiv;
+  KwayPiv piv;
+  size_t o_bounds, o_claim, total;
+};
+
+template <typename K, int TB>
+KwayLayout kway_layout(const KwayShards& S, int sms) {
+  KwayLayout KL{};
+  int64_t M = 0;
+  for (int i = 0; i < S.w; ++i) M += S.hi[i] - S.lo[i];
+  int64_t sp = M / (8 * (int64_t)sms);  // ~8 work items per SM
+  if (sp > ((int64_t)1 << 17)) sp = (int64_t)1 << 17;
+  if (sp < KwayCfg<K, TB>::KS) sp = KwayCfg<K, TB>::KS;
+  KL.spacing = sp;
+  KL.piv.off[0] = 0;
+  for (int i = 0; i < S.w; ++i) KL.piv.off[i + 1] = KL.piv.off[i] + (S.hi[i] - S.lo[i] + sp - 1) / sp;
+  KL.npiv = KL.piv.off[S.w];
+  size_t off = 0;
+  KL.o_bounds = off;
+  off = align_up(off + (size_t)(KL.npiv + 2) * S.w * 8, 256);
+  KL.o_claim = off;
+  off = align_up(off + 8, 256);
+  KL.total = off + 256;
+  return KL;
+}
+
+template <typename K, int TB>
+int run_kway(const KwayShards& S, void* out_keys, void* out_tags, unsigned char* ws, size_t ws_bytes, cudaStream_t st) {
+  int sms;
+  if (int e = device_sms(&sms)) return e;
+  KwayLayout KL = kway_layout<K, TB>(S, sms);
+  if (ws_bytes < KL.total) return fail(RS_ENOMEM, "k-way merge workspace too small");
+  int64_t* bounds = reinterpret_cast<int64_t*>(ws + KL.o_bounds);
+  unsigned long long* claim = reinterpret_cast<unsigned long long*>(ws + KL.o_claim);
+  RS_CUDA(cudaMemsetAsync(claim, 0, 8, st));
+  int64_t pw = KL.npiv * 32;
+  int pgrid = (int)std::min<int64_t>((pw + 255) / 256, (int64_t)sms * 8);
+  if (pgrid < 1) pgrid = 1;
+  k_kway_pivots<K><<<pgrid, 256, 0, st>>>(S, KL.spacing, KL.piv, KL.npiv, bounds);
+  RS_CUDA(cudaGetLastError());
+  int wp = 1;
+  while (wp < S.w) wp <<= 1;
+  size_t sm = KwayCfg<K, TB>::smem(wp);
+  int occ;
+  if (int e = occupancy((const void*)k_kway_merge<K, TB>, KwayCfg<K, TB>::THREADS, sm,
+                        KwayCfg<K, TB>::smem(kKwayMaxW), &occ, "k-way merge kernel"))
+    return e;
+  KwayMergeArgs A;
+  A.S = S;
+  A.bounds = bounds;
+  A.nitems = KL.npiv + 1;
+  A.out_keys = out_keys;
+  A.out_tags = out_tags;
+  A.claim = claim;
+  int grid = (int)std::min<int64_t>((int64_t)sms * occ, A.nitems);
+  k_kway_merge<K, TB><<<grid, KwayCfg<K, TB>::THREADS, sm, st>>>(A);
+  RS_CUDA(cudaGetLastError());
+  return RS_OK;
+}
+
 }  // namespace
 
 extern "C" {
+
+int rs_corank(int key_dtype, const rs_shard* shards, int w, const int64_t* targets, int ntargets, int64_t* out,
+              void* workspace, size_t ws_bytes, void* stream) {
+  KwayShards S;
+  if (int e = load_shards(shards, w, 0, &S)) return e;
+  if (ntargets < 0 || (ntargets > 0 && (!targets || !out))) return fail(RS_EINVAL, "null targets / out");
+  if (ntargets == 0) return RS_OK;
+  size_t need = (size_t)ntargets * 8 * (1 + w) + 512;
+  if (!workspace || ws_bytes < need) return fail(RS_ENOMEM, "co-rank workspace too small");
+  int64_t total = 0;
+  for (int i = 0; i < w; ++i) total += S.hi[i] - S.lo[i];
+  for (int b = 0; b < ntargets; ++b)
+    if (targets[b] < 0 || targets[b] > total) return fail(RS_EINVAL, "co-rank target outside [0, total]");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  int64_t* dt = reinterpret_cast<int64_t*>(workspace);
+  int64_t* dout = reinterpret_cast<int64_t*>(reinterpret_cast<unsigned char*>(workspace) +
+                                             align_up((size_t)ntargets * 8, 256));
+  RS_CUDA(cudaMemcpyAsync(dt, targets, (size_t)ntargets * 8, cudaMemcpyHostToDevice, st));
+  if (key_dtype == RS_KEY_I64) k_corank<int64_t><<<ntargets, kCorankThreads, 0, st>>>(S, dt, dout);
+  else k_corank<int32_t><<<ntargets, kCorankThreads, 0, st>>>(S, dt, dout);
+  RS_CUDA(cudaGetLastError());
+  RS_CUDA(cudaMemcpyAsync(out, dout, (size_t)ntargets * w * 8, cudaMemcpyDeviceToHost, st));
+  RS_CUDA(cudaStreamSynchronize(st));
+  return RS_OK;
+}
+
+size_t rs_kway_workspace_bytes(int key_dtype, int tag_bytes, const rs_shard* shards, int w) {
+  KwayShards S;
+  if (load_shards(shards, w, 0, &S)) return 0;
+  int sms;
+  if (device_sms(&sms)) sms = 148;
+  if (key_dtype == RS_KEY_I64) {
+    return tag_bytes == 0 ? kway_layout<int64_t, 0>(S, sms).total
+                          : (tag_bytes == 4 ? kway_layout<int64_t, 4>(S, sms).total : kway_layout<int64_t, 8>(S, sms).total);
+  }
+  return tag_bytes == 0 ? kway_layout<int32_t, 0>(S, sms).total
+                        : (tag_bytes == 4 ? kway_layout<int32_t, 4>(S, sms).total : kway_layout<int32_t, 8>(S, sms).total);
+}
+
+int rs_kway_merge(int key_dtype, int tag_bytes, const rs_shard* shards, int w, void* out_keys, void* out_tags,
+                  void* workspace, size_t ws_bytes, void* stream) {
+  KwayShards S;
+  if (key_dtype != RS_KEY_I32 && key_dtype != RS_KEY_I64) return fail(RS_EUNSUPPORTED, "keys must be int32 or int64");
+  if (tag_bytes != 0 && tag_bytes != 4 && tag_bytes != 8) return fail(RS_EUNSUPPORTED, "tags must be 4 or 8 bytes wide");
+  if (int e = load_shards(shards, w, tag_bytes, &S)) return e;
+  int64_t M = 0;
+  for (int i = 0; i < w; ++i) M += S.hi[i] - S.lo[i];
+  if (M == 0) return RS_OK;
+  if (!out_keys || (tag_bytes && !out_tags) || !workspace) return fail(RS_EINVAL, "null output or workspace");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  unsigned char* ws = reinterpret_cast<unsigned char*>(workspace);
+  if (key_dtype == RS_KEY_I64) {
+    if (tag_bytes == 0) return run_kway<int64_t, 0>(S, out_keys, out_tags, ws, ws_bytes, st);
+    if (tag_bytes == 4) return run_kway<int64_t, 4>(S, out_keys, out_tags, ws, ws_bytes, st);
+    return run_kway<int64_t, 8>(S, out_keys, out_tags, ws, ws_bytes, st);
+  }
+  if (tag_bytes == 0) return run_kway<int32_t, 0>(S, out_keys, out_tags, ws, ws_bytes, st);
+  if (tag_bytes == 4) return run_kway<int32_t, 4>(S, out_keys, out_tags, ws, ws_bytes, st);
+  return run_kway<int32_t, 8>(S, out_keys, out_tags, ws, ws_bytes, st);
+}
+
+int rs_ipc_alloc(size_t bytes, void** ptr, void* handle) {
+  if (!ptr || !handle) return fail(RS_EINVAL, "null ptr / handle");
+  *ptr = nullptr;
+  if (cudaMalloc(ptr, bytes ? bytes : 256) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(RS_ENOMEM, "cudaMalloc of an IPC-shareable shard buffer failed");
+  }
+  cudaIpcMemHandle_t h;
+  if (cudaError_t e = cudaIpcGetMemHandle(&h, *ptr)) {
+    cudaFree(*ptr);
+    *ptr = nullptr;
+    return fail(RS_ECUDA, std::string("cudaIpcGetMemHandle failed: ") + cudaGetErrorString(e));
+  }
+  memcpy(handle, &h, sizeof(h));
+  return RS_OK;
+}
+
+int rs_ipc_open(const void* handle, void** ptr) {
+  if (!ptr || !handle) return fail(RS_EINVAL, "null ptr / handle");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  RS_CUDA(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return RS_OK;
+}
+
+int rs_ipc_close(void* ptr) {
+  RS_CUDA(cudaIpcCloseMemHandle(ptr));
+  return RS_OK;
+}
+
+int rs_ipc_free(void* ptr) {
+  RS_CUDA(cudaFree(ptr));
+  return RS_OK;
+}
 
 size_t rs_workspace_bytes(int algo, int key_dtype, int tag_bytes, int64_t n, int32_t min_run_len) {
   (void)algo;

@@ -1,27 +1,29 @@
 """Arrays that span GPUs: per-GPU powersort on contiguous shards, then an exact
-splitter-partitioned exchange and a stable merge.
+co-rank split and one stable W-way merge.
 
 Global order = the reference's stable order of the concatenated array, i.e.
-(key, shard rank, position in shard).  Each rank ends with the same number of
-elements it started with, holding the next contiguous slice of the globally
-sorted array.
+(key, shard rank, position in shard): the reference's merges send ties to the
+left run (runcore.py:262-263).  Rank g ends with output positions
+[t_g, t_{g+1}) of that order, t_g = n_0 + ... + n_{g-1}: the same number of
+elements it started with, the next contiguous slice of the sorted array.
 
-Splitters (exact, two all-gathers, independent of key duplicates):
-  1. every rank publishes S regular samples of its sorted shard as
-     (key, rank, position) triples;
-  2. for every target boundary t_g every rank derives, from the samples alone,
-     a bracket [lo_g, hi_g) of triples that must contain the t_g-th element,
-     counts exactly how many of its elements precede lo_g / hi_g, and
-     publishes its elements inside the bracket (<= 2*ceil(n_i/S)+2 of them);
-  3. every rank merges the published candidates and derives the same split
-     matrix c[g][i] (elements of shard i among the first t_g).
-Exchange: one all-to-all-v of keys (and tags); the received W sorted runs are
-concatenated in rank order and stably merged by the same powersort path
-(its leaves are the received runs, ties go to the lower rank).
+Two data planes, one merge kernel (csrc/rs_kway.cuh):
 
-The local sorter is a parameter so the host logic can be exercised with the
-gloo backend on CPU (tests/test_dist_gloo.py); the product path passes the
-CUDA powersort.
+* **P2P (NVLink, the default on one node).**  Every rank's shard lives in a
+  CUDA-IPC buffer (``P2PShardSpace``) that every other rank maps.  After the
+  local sorts and one host barrier, rank g finds its split vectors with the
+  device co-rank kernel reading all W shards in place (``rs_corank``: exact
+  multi-sequence selection over peer memory, no host round of samples), and
+  the W-way merge kernel streams its slice straight out of the peers' buffers
+  (``rs_kway_merge``).  The exchange is the merge's input stream: each element
+  crosses NVLink once and is written once.
+* **NCCL (fallback, e.g. across nodes).**  Splitters from regular samples and
+  two all-gathers (``compute_splits``), ``all_to_all_single`` of the segments,
+  then the same W-way merge over the W received runs in local HBM.
+
+The local sorter and the NCCL-plane merge are parameters so the host logic can
+be exercised with the gloo backend on CPU (tests/test_dist_gloo.py); the product
+path passes the CUDA powersort and the CUDA k-way merge.
 """
 from __future__ import annotations
 
@@ -208,101 +210,139 @@ def _default_local_sort(keys, tags):
     return powersort(keys, SortConfig(), None, tags)
 
 
+def _device_merge(out, tout, recv):
+    """Stable W-way merge of the received runs (rank order) on the device."""
+    import torch
+
+    from . import kway
+
+    shards, off = [], 0
+    for c in recv:
+        shards.append(kway.Shard(out.data_ptr(), tout.data_ptr() if tout is not None else None, off, off + c))
+        off += c
+    mk = torch.empty_like(out)
+    mt = torch.empty_like(tout) if tout is not None else None
+    kway.kway_merge(shards, mk, mt)
+    return mk, mt
+
+
 def sharded_sort(keys, tags=None, group=None, local_sort: Optional[Callable] = None,
-                 samples: int = SAMPLES):
-    """Globally stable sort of an array sharded contiguously over the ranks.
+                 samples: int = SAMPLES, merge: Optional[Callable] = None):
+    """Globally stable sort of an array sharded contiguously over the ranks,
+    NCCL data plane (see sharded_sort_p2p for the NVLink path).
 
     `keys` (and `tags`) are this rank's contiguous shard (torch tensors).  Returns
     (sorted_slice, tags_slice, info): this rank's slice of the global sorted
     order, same length as its input shard.
     """
     local_sort = local_sort or _default_local_sort
+    merge = merge or _device_merge
     m_local = local_sort(keys, tags)
     splits = compute_splits(keys, group, samples)
     out, tout, recv = exchange(keys, splits, tags, group)
-    m_merge = local_sort(out, tout)
-    return out, tout, {"local": m_local, "merge": m_merge, "splits": splits, "recv": recv}
+    out, tout = merge(out, tout, recv)
+    return out, tout, {"local": m_local, "splits": splits, "recv": recv}
 
 
-# ------------------------------------------------------------------ bench --
-def bench_sharded(args, rank: int, world: int, local_rank: int) -> dict:
-    """bench.py --gpus N (torchrun): weak scaling, n keys per rank."""
+class P2PShardSpace:
+    """Shard buffers every rank of `group` maps (CUDA IPC over NVLink).
+
+    ``keys`` / ``tags`` are this rank's shard (torch views of its IPC buffers,
+    capacity elements); ``peer_keys[i]`` / ``peer_tags[i]`` are the device
+    addresses of rank i's buffers in this process.  Collective: every rank
+    constructs it with the same capacity and dtypes.
+    """
+
+    def __init__(self, capacity: int, key_dtype, tag_dtype=None, group=None):
+        import torch
+
+        from . import kway
+
+        dist = _dist()
+        self.group = group
+        self.W = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        if self.W > kway.MAX_SHARDS:
+            raise ValueError(f"the P2P merge takes at most {kway.MAX_SHARDS} ranks")
+        self.capacity = int(capacity)
+        self.device = torch.device("cuda", torch.cuda.current_device())
+        kb = torch.empty(0, dtype=key_dtype).element_size()
+        self._kbuf = kway.IpcBuffer(max(1, self.capacity) * kb)
+        self._tbuf = None
+        if tag_dtype is not None:
+            tb = torch.empty(0, dtype=tag_dtype).element_size()
+            self._tbuf = kway.IpcBuffer(max(1, self.capacity) * tb)
+        self.keys = kway.tensor_at(self._kbuf.address, self.capacity, key_dtype, self.device)
+        self.tags = (kway.tensor_at(self._tbuf.address, self.capacity, tag_dtype, self.device)
+                     if self._tbuf is not None else None)
+        mine = (self._kbuf.handle_bytes(), self._tbuf.handle_bytes() if self._tbuf is not None else None)
+        allh = [None] * self.W
+        dist.all_gather_object(allh, mine, group=group)
+        self._opened = []
+        self.peer_keys, self.peer_tags = [], []
+        for i, (hk, ht) in enumerate(allh):
+            if i == self.rank:
+                self.peer_keys.append(self._kbuf.address)
+                self.peer_tags.append(self._tbuf.address if self._tbuf is not None else None)
+                continue
+            pk = kway.ipc_open(hk)
+            self._opened.append(pk)
+            self.peer_keys.append(pk)
+            if ht is not None:
+                pt = kway.ipc_open(ht)
+                self._opened.append(pt)
+                self.peer_tags.append(pt)
+            else:
+                self.peer_tags.append(None)
+
+    def close(self):
+        from . import kway
+
+        _dist().barrier(group=self.group)
+        for p in self._opened:
+            kway.ipc_close(p)
+        self._opened = []
+        _dist().barrier(group=self.group)
+        self._kbuf.free()
+        if self._tbuf is not None:
+            self._tbuf.free()
+
+
+def sharded_sort_p2p(space: P2PShardSpace, n_local: int, local_sort: Optional[Callable] = None,
+                     out_keys=None, out_tags=None):
+    """Globally stable sort of the shards in `space` (this rank: the first
+    n_local elements of space.keys / space.tags), NVLink data plane.
+
+    Returns (sorted_slice, tags_slice, info) like sharded_sort.  The shard
+    buffers hold each rank's locally sorted shard afterwards.
+    """
     import torch
-    import torch.distributed as dist
 
-    from . import workloads
+    from . import kway
 
-    dev = torch.device("cuda", local_rank)
-    keys_np, tags_np = workloads.generate(args.config, args.n, seed=1 + rank)
-    n = len(keys_np)
-    src = torch.from_numpy(keys_np).to(dev)
-    tsrc = torch.from_numpy(tags_np).to(dev) if tags_np is not None else None
-    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
-    times = []
-    for it in range(args.warmup + args.steps):
-        work = src.clone()
-        tw = tsrc.clone() if tsrc is not None else None
-        flush.fill_(1)
-        dist.barrier()
-        torch.cuda.synchronize()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record()
-        out, tout, info = sharded_sort(work, tw)
-        e1.record()
-        torch.cuda.synchronize()
-        dist.barrier()
-        if it >= args.warmup:
-            times.append(e0.elapsed_time(e1))
-    t = torch.tensor([float(np.mean(times))], device=dev)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
-    # e2e: this rank's shard from pinned host memory, the sharded sort, its slice back
-    hk = torch.from_numpy(keys_np).pin_memory()
-    ht = torch.from_numpy(tags_np).pin_memory() if tags_np is not None else None
-    e2e = []
-    for it in range(args.warmup + args.steps):
-        hk.copy_(torch.from_numpy(keys_np))
-        flush.fill_(1)
-        dist.barrier()
-        torch.cuda.synchronize()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record()
-        dk = hk.to(dev, non_blocking=True)
-        dt = ht.to(dev, non_blocking=True) if ht is not None else None
-        o2, t2, _ = sharded_sort(dk, dt)
-        hk.copy_(o2, non_blocking=True)  # pinned: a device-to-host DMA on the stream
-        if t2 is not None:
-            ht.copy_(t2, non_blocking=True)
-        e1.record()
-        torch.cuda.synchronize()
-        dist.barrier()
-        if it >= args.warmup:
-            e2e.append(e0.elapsed_time(e1))
-    te = torch.tensor([float(np.mean(e2e))], device=dev)
-    dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_ms = float(te.item())
-    B = keys_np.itemsize + (tags_np.itemsize if tags_np is not None else 0)
-    # global sortedness check: local sorted + boundary with the next rank
-    ok = bool((out[1:] >= out[:-1]).all().item()) if out.numel() > 1 else True
-    edge = torch.tensor([out[0].item() if out.numel() else 0, out[-1].item() if out.numel() else 0],
-                        dtype=torch.int64, device=dev)
-    edges = [torch.zeros_like(edge) for _ in range(world)]
-    dist.all_gather(edges, edge)
-    for i in range(world - 1):
-        ok &= bool(edges[i][1].item() <= edges[i + 1][0].item())
-    return {
-        "metric": "powersort keys/s at n=1e7 int32 random-runs; % of HBM roofline; 1/2/4/8 GPU",
-        "value": n * world / (ms / 1e3), "unit": "keys/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": str(keys_np.dtype), "data": "synthetic (seeded PCG64, shard i uses seed 1+i)",
-        "config": {"workload": f"cfg{args.config} per rank, one global array sharded contiguously",
-                   "n_per_gpu": n, "parallelism": f"shard{world}",
-                   "l2": "flushed (512 MiB write) before every timed step"},
-        "globally_sorted_ok": ok,
-        "e2e": {"value": n * world / (e2e_ms / 1e3), "unit": "keys/s", "ms_per_step": e2e_ms,
-                "h2d_bytes_per_step": n * B, "d2h_bytes_per_step": n * B},
-        # our kernels per step: two powersorts (shard, then the received runs), 3 launches each
-        "gpu_launches": 6 * args.steps,
-    }
+    dist = _dist()
+    group = space.group
+    W, g = space.W, space.rank
+    local_sort = local_sort or _default_local_sort
+    keys = space.keys[:n_local]
+    tags = space.tags[:n_local] if space.tags is not None else None
+    m_local = local_sort(keys, tags) if n_local > 1 else None
+    # every shard sorted and visible before any peer reads it
+    torch.cuda.current_stream().synchronize()
+    ns = [None] * W
+    dist.all_gather_object(ns, int(n_local), group=group)  # doubles as the barrier
+    T = np.concatenate([[0], np.cumsum(ns)]).astype(np.int64)
+    shards = [kway.Shard(space.peer_keys[i], space.peer_tags[i], 0, ns[i]) for i in range(W)]
+    c = kway.corank(shards, [int(T[g]), int(T[g + 1])], space.keys.dtype, space.device)
+    mine = [shards[i].with_range(int(c[0][i]), int(c[1][i])) for i in range(W)]
+    if out_keys is None:
+        out_keys = torch.empty(n_local, dtype=space.keys.dtype, device=space.device)
+    if tags is not None and out_tags is None:
+        out_tags = torch.empty(n_local, dtype=space.tags.dtype, device=space.device)
+    kway.kway_merge(mine, out_keys[:n_local], out_tags[:n_local] if tags is not None else None)
+    # peers may still be reading this rank's shard: nobody rewrites a shard
+    # buffer before every merge has finished
+    torch.cuda.current_stream().synchronize()
+    dist.barrier(group=group)
+    return out_keys[:n_local], (out_tags[:n_local] if tags is not None else None), \
+        {"local": m_local, "splits": c, "lens": ns}

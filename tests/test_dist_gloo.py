@@ -26,6 +26,13 @@ def _free_port():
     return p
 
 
+def _cpu_merge(out, tout, recv):
+    """CPU stand-in for the CUDA W-way merge: the received runs in rank order,
+    stably merged (a stable sort of their concatenation is that merge)."""
+    order = torch.from_numpy(np.argsort(out.numpy(), kind="stable"))
+    return out[order], (tout[order] if tout is not None else None)
+
+
 def _cpu_stable_sort(keys, tags):
     order = torch.from_numpy(np.argsort(keys.numpy(), kind="stable"))
     keys.copy_(keys[order])
@@ -66,7 +73,8 @@ def _worker(rank, W, port, seed, q):
                 k, t = _shards(case, W, seed)[rank]
                 keys = torch.from_numpy(k.copy())
                 tags = torch.from_numpy(t.copy())
-                out, tout, info = rsd.sharded_sort(keys, tags, local_sort=_cpu_stable_sort, samples=samples)
+                out, tout, info = rsd.sharded_sort(keys, tags, local_sort=_cpu_stable_sort, samples=samples,
+                                                merge=_cpu_merge)
                 q.put((case, samples, rank, out.numpy().copy(), tout.numpy().copy()))
     finally:
         dist.destroy_process_group()
