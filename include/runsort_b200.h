@@ -109,11 +109,17 @@ int rs_fetch_metrics(int algo, int key_dtype, int tag_bytes, int64_t n, int32_t 
 int rs_export_tree(int algo, int key_dtype, int tag_bytes, int64_t n, int32_t min_run_len, void* workspace,
                    void* stream, rs_tree* tree);
 
-/* Host-buffer convenience entry (what a plain ctypes binding of the reference
- * would call with numpy arrays): allocates device memory, copies in, sorts,
- * copies back, frees.  Synchronous. */
+/* Host-buffer entry (what a plain ctypes binding of the reference calls with
+ * numpy arrays): device memory from the stream-ordered pool, the arrays copied
+ * in and out in 4 MiB chunks through pinned slots by a pool of host threads
+ * (host copies overlapped with the DMAs), the sort in between.  Synchronous;
+ * the caller's buffers are written only after the device reported success. */
 int rs_sort_host(int algo, int key_dtype, void* keys, int tag_bytes, void* tags, int64_t n,
                  int32_t min_run_len, int32_t merge_kind, rs_metrics* out, rs_tree* tree);
+
+/* rs_sort_host with the alpha-stack / alpha-merge growth ratio. */
+int rs_sort_host_ex(int algo, int key_dtype, void* keys, int tag_bytes, void* tags, int64_t n,
+                    int32_t min_run_len, int32_t merge_kind, double alpha, rs_metrics* out, rs_tree* tree);
 
 /* Per-phase CUDA-event timing of subsequent rs_sort calls on this thread
  * (events recorded on the sort's own stream).  rs_profile_read waits for the

@@ -19,7 +19,7 @@ RS_MERGE_BITONIC, RS_MERGE_CLASSIC = 0, 1
 RS_EIO = 6
 
 # every symbol include/runsort_b200.h declares
-EXPORTS = ("rs_workspace_bytes", "rs_sort", "rs_sort_ex", "rs_fetch_metrics", "rs_sort_host", "rs_export_tree", "rs_profile",
+EXPORTS = ("rs_workspace_bytes", "rs_sort", "rs_sort_ex", "rs_fetch_metrics", "rs_sort_host", "rs_sort_host_ex", "rs_export_tree", "rs_profile",
            "rs_profile_read", "rs_debug_counters", "rs_max_min_run_len", "rs_load_bin", "rs_corank", "rs_kway_workspace_bytes", "rs_kway_merge",
            "rs_ipc_alloc", "rs_ipc_open", "rs_ipc_close", "rs_ipc_free", "rs_last_error",
            "rs_version")
@@ -69,6 +69,10 @@ def lib():
         L.rs_sort_host.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p,
                                    ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(RsMetrics),
                                    ctypes.POINTER(RsTree)]
+        L.rs_sort_host_ex.restype = ctypes.c_int
+        L.rs_sort_host_ex.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p,
+                                      ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_double,
+                                      ctypes.POINTER(RsMetrics), ctypes.POINTER(RsTree)]
         L.rs_export_tree.restype = ctypes.c_int
         L.rs_export_tree.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_int32,
                                      ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(RsTree)]

@@ -25,6 +25,7 @@
 #include "rs_chain.cuh"
 #include "rs_common.cuh"
 #include "rs_exec.cuh"
+#include "rs_host.h"
 #include "rs_kway.cuh"
 #include "rs_merge.cuh"
 #include "rs_prep.cuh"
@@ -1180,37 +1181,63 @@ int rs_export_tree(int algo, int key_dtype, int tag_bytes, int64_t n, int32_t mi
 
 int rs_sort_host(int algo, int key_dtype, void* keys, int tag_bytes, void* tags, int64_t n, int32_t min_run_len,
                  int32_t merge_kind, rs_metrics* out, rs_tree* tree) {
+  return rs_sort_host_ex(algo, key_dtype, keys, tag_bytes, tags, n, min_run_len, merge_kind, 2.0, out, tree);
+}
+
+int rs_sort_host_ex(int algo, int key_dtype, void* keys, int tag_bytes, void* tags, int64_t n, int32_t min_run_len,
+                    int32_t merge_kind, double alpha, rs_metrics* out, rs_tree* tree) {
   int kb;
   if (int e = validate(algo, key_dtype, tag_bytes, n, min_run_len, merge_kind, &kb)) return e;
+  if (!(alpha > 1.0)) return fail(RS_EINVAL, "alpha must be > 1");
   if (tags == nullptr) tag_bytes = 0;
-  if (n <= 1) return rs_sort(algo, key_dtype, keys, tag_bytes, tags, n, min_run_len, merge_kind, nullptr, 0,
-                             nullptr, out, tree);
-  size_t ws = rs_workspace_bytes(algo, key_dtype, tag_bytes, n, min_run_len);
+  if (n <= 1) return rs_sort_ex(algo, key_dtype, keys, tag_bytes, tags, n, min_run_len, merge_kind, alpha, nullptr, 0,
+                                nullptr, out, tree);
+  if (!keys) return fail(RS_EINVAL, "null keys");
+  int dev;
+  RS_CUDA(cudaGetDevice(&dev));
+  Layout L = make_layout(n, min_run_len, kb, tag_bytes, algo);
+  size_t ws = L.total;
   void *dk = nullptr, *dt = nullptr, *dws = nullptr;
   cudaStream_t st;
   RS_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
   int rc = RS_OK;
-  do {
-    if (cudaMallocAsync(&dk, (size_t)n * kb + 64, st) != cudaSuccess ||
-        (tag_bytes && cudaMallocAsync(&dt, (size_t)n * tag_bytes + 64, st) != cudaSuccess) ||
-        cudaMallocAsync(&dws, ws, st) != cudaSuccess) {
-      rc = fail(RS_ENOMEM, "device allocation failed");
-      break;
-    }
-    if (cudaMemcpyAsync(dk, keys, (size_t)n * kb, cudaMemcpyHostToDevice, st) != cudaSuccess ||
-        (tag_bytes && cudaMemcpyAsync(dt, tags, (size_t)n * tag_bytes, cudaMemcpyHostToDevice, st) != cudaSuccess)) {
-      rc = fail(RS_ECUDA, "host-to-device copy failed");
-      break;
-    }
-    rc = rs_sort(algo, key_dtype, dk, tag_bytes, dt, n, min_run_len, merge_kind, dws, ws, st, out, tree);
-    if (rc) break;
-    if (cudaMemcpyAsync(keys, dk, (size_t)n * kb, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
-        (tag_bytes && cudaMemcpyAsync(tags, dt, (size_t)n * tag_bytes, cudaMemcpyDeviceToHost, st) != cudaSuccess) ||
-        cudaStreamSynchronize(st) != cudaSuccess) {
-      rc = fail(RS_ECUDA, "device-to-host copy failed");
-      break;
-    }
-  } while (0);
+  {
+    host::Session S(dev);
+    std::vector<host::Span> spans;
+    do {
+      if (cudaMallocAsync(&dk, (size_t)n * kb + 64, st) != cudaSuccess ||
+          (tag_bytes && cudaMallocAsync(&dt, (size_t)n * tag_bytes + 64, st) != cudaSuccess) ||
+          cudaMallocAsync(&dws, ws, st) != cudaSuccess) {
+        cudaGetLastError();
+        rc = fail(RS_ENOMEM, "device allocation failed");
+        break;
+      }
+      spans.push_back({reinterpret_cast<unsigned char*>(keys), reinterpret_cast<unsigned char*>(dk), (size_t)n * kb});
+      if (tag_bytes)
+        spans.push_back({reinterpret_cast<unsigned char*>(tags), reinterpret_cast<unsigned char*>(dt),
+                         (size_t)n * tag_bytes});
+      if (!S.init((size_t)n * (kb + tag_bytes))) {
+        rc = fail(RS_ENOMEM, "pinned staging allocation failed");
+        break;
+      }
+      if (!S.h2d(spans, st)) {
+        rc = fail(RS_ECUDA, "host-to-device copy failed");
+        break;
+      }
+      rc = rs_sort_ex(algo, key_dtype, dk, tag_bytes, dt, n, min_run_len, merge_kind, alpha, dws, ws, st, nullptr,
+                      nullptr);
+      if (rc) break;
+      unsigned char* wsp = reinterpret_cast<unsigned char*>(dws);
+      int d = S.d2h(spans, st, [&]() -> int {
+        int e = read_metrics(L, wsp, st, out);  // synchronizes: the sort is complete
+        if (!e && tree) e = export_tree(L, wsp, st, tree);
+        return e;
+      });
+      if (d > 0) rc = d;  // the device's verdict (nothing was written back)
+      else if (d < 0) rc = fail(RS_ECUDA, "device-to-host copy failed");
+    } while (0);
+    cudaStreamSynchronize(st);
+  }  // staging session: pinned slots back to the pool
   if (dk) cudaFreeAsync(dk, st);
   if (dt) cudaFreeAsync(dt, st);
   if (dws) cudaFreeAsync(dws, st);

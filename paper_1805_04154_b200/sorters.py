@@ -253,10 +253,48 @@ def _target_device(a, tags):
     return dev
 
 
+def _host_native(a, tags) -> bool:
+    """numpy keys/tags the host staging engine (rs_sort_host_ex) takes as they are."""
+    if not isinstance(a, np.ndarray) or a.dtype not in _SIGNED or a.ndim != 1 or not a.flags.c_contiguous \
+            or not a.flags.writeable:
+        return False
+    if tags is None:
+        return True
+    return isinstance(tags, np.ndarray) and tags.ndim == 1 and tags.flags.c_contiguous and \
+        tags.flags.writeable and tags.dtype.itemsize in (4, 8) and len(tags) == len(a)
+
+
+def _accumulate(algo: int, metrics: Metrics, out) -> None:
+    metrics.merge_cost += int(out.merge_cost)
+    metrics.comparisons += int(out.comparisons)
+    if algo == _lib.RS_ALGO_PEEKSORT:
+        metrics.runs_detected = int(out.runs_detected)  # sorters.py:358 assigns
+    else:
+        metrics.runs_detected += int(out.runs_detected)  # sorters.py:464 accumulates
+        if int(out.max_stack_height) > metrics.max_stack_height:
+            metrics.max_stack_height = int(out.max_stack_height)
+
+
+def _host_sort(algo: int, a: np.ndarray, cfg: SortConfig, metrics: Metrics, tags) -> Metrics:
+    """numpy in, numpy out through the library's host staging engine: chunked,
+    multi-threaded copies through pinned slots overlapped with the DMAs, and the
+    caller's arrays written only after the device reported success."""
+    L = _lib.lib()
+    out = _lib.RsMetrics()
+    kind = _lib.RS_MERGE_CLASSIC if cfg.merge_kind == "classic" else _lib.RS_MERGE_BITONIC
+    _lib.check(L.rs_sort_host_ex(algo, _SIGNED[a.dtype], a.ctypes.data, tags.dtype.itemsize if tags is not None else 0,
+                                 tags.ctypes.data if tags is not None else None, len(a), int(cfg.min_run_len), kind,
+                                 float(cfg.alpha), ctypes.byref(out), None))
+    _accumulate(algo, metrics, out)
+    return metrics
+
+
 def _device_sort(algo: int, a, cfg: SortConfig, metrics: Metrics, tags) -> Metrics:
     torch = _torch()
     dev = _target_device(a, tags)
     with torch.cuda.device(dev):
+        if not cfg.record_tree and _host_native(a, tags):
+            return _host_sort(algo, a, cfg, metrics, tags)
         return _device_sort_on(algo, a, cfg, metrics, tags, dev)
 
 
@@ -306,14 +344,7 @@ def _device_sort_on(algo: int, a, cfg: SortConfig, metrics: Metrics, tags, dev) 
         s_.finish_host()
     if any(s_.on_host for s_ in staged):
         stream.synchronize()  # non-blocking copies into pinned CPU tensors have landed
-    metrics.merge_cost += int(out.merge_cost)
-    metrics.comparisons += int(out.comparisons)
-    if algo == _lib.RS_ALGO_PEEKSORT:
-        metrics.runs_detected = int(out.runs_detected)  # sorters.py:358 assigns
-    else:
-        metrics.runs_detected += int(out.runs_detected)  # sorters.py:464 accumulates
-        if int(out.max_stack_height) > metrics.max_stack_height:
-            metrics.max_stack_height = int(out.max_stack_height)
+    _accumulate(algo, metrics, out)
     if tree is not None:
         r = int(tree.n_leaves)
         lens = bufs[0][:r]

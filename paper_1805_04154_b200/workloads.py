@@ -124,38 +124,71 @@ def config5_bounds(n: int = CONFIG5_N, seed: int = 1, mean: float = float(1 << 1
     return _geometric_bounds(_rng(seed), n, mean)
 
 
-def config5_device(n: int = CONFIG5_N, seed: int = 1, device="cuda", out=None,
-                   mean: float = float(1 << 16)):
-    """Config 5 on the device: uniform int64 in [0, 2^63), geometric segments
-    of mean 2^16, each sorted ascending.  Keys come from per-chunk PCG64-seeded
-    torch generators over fixed 2^24-element chunks, so the array does not
-    depend on how it is later sharded."""
+def _config5_raw(lo: int, hi: int, n: int, seed: int, device, out):
+    """Raw (unsorted) values of positions [lo, hi): per-chunk PCG64-seeded torch
+    generators over fixed 2^24-element chunks, so any range of the array is the
+    same bytes whatever range or GPU count it is generated for."""
     import torch
 
-    b = config5_bounds(n, seed, mean)
-    if out is None:
-        out = torch.empty(n, dtype=torch.int64, device=device)
     g = torch.Generator(device=device)
-    for c0 in range(0, n, CONFIG5_CHUNK):
-        c1 = min(n, c0 + CONFIG5_CHUNK)
-        g.manual_seed(int(_rng(seed * 1_000_003 + c0 // CONFIG5_CHUNK).integers(0, 1 << 62)))
-        out[c0:c1] = torch.randint(0, (1 << 63) - 1, (c1 - c0,), generator=g, device=device,
-                                   dtype=torch.int64)
-    # sort every segment: group segments into ~chunk-sized windows
+    c = (lo // CONFIG5_CHUNK) * CONFIG5_CHUNK
+    while c < hi:
+        c1 = min(n, c + CONFIG5_CHUNK)
+        g.manual_seed(int(_rng(seed * 1_000_003 + c // CONFIG5_CHUNK).integers(0, 1 << 62)))
+        vals = torch.randint(0, (1 << 63) - 1, (c1 - c,), generator=g, device=device, dtype=torch.int64)
+        a0, a1 = max(lo, c), min(hi, c1)
+        out[a0 - lo: a1 - lo] = vals[a0 - c: a1 - c]
+        c = c1
+    return out
+
+
+def _sort_segments(buf, b: np.ndarray, base: int):
+    """Sort every segment [b[i], b[i+1]) of buf (positions offset by base) in
+    windows of ~one chunk (two stable sorts: by value, then by segment)."""
+    import torch
+
+    device = buf.device
     bt = torch.as_tensor(b, device=device)
-    i = 0
-    nb = len(b) - 1
+    i, nb = 0, len(b) - 1
     while i < nb:
         j = i + 1
         while j < nb and b[j + 1] - b[i] <= CONFIG5_CHUNK:
             j += 1
         s, e = int(b[i]), int(b[j])
-        seg_id = torch.bucketize(torch.arange(s, e, device=device), bt[i + 1 : j + 1], right=True)
-        vals, idx = torch.sort(out[s:e], stable=True)
+        seg_id = torch.bucketize(torch.arange(s, e, device=device), bt[i + 1: j + 1], right=True)
+        vals, idx = torch.sort(buf[s - base: e - base], stable=True)
         _, order = torch.sort(seg_id[idx], stable=True)
-        out[s:e] = vals[order]
+        buf[s - base: e - base] = vals[order]
         i = j
+
+
+def config5_range(lo: int, hi: int, n: int = CONFIG5_N, seed: int = 1, device="cuda", out=None,
+                  mean: float = float(1 << 16), bounds: Optional[np.ndarray] = None):
+    """Positions [lo, hi) of the config-5 array on the device: uniform int64 in
+    [0, 2^63), geometric segments of mean 2^16, each sorted ascending.  The
+    segments overlapping the range are generated whole and sorted, then the
+    range is cut out: shards of any GPU count concatenate to the same array."""
+    import torch
+
+    b = config5_bounds(n, seed, mean) if bounds is None else bounds
+    i0 = int(np.searchsorted(b, lo, side="right")) - 1
+    j1 = int(np.searchsorted(b, hi, side="left"))
+    s0, e1 = int(b[i0]), int(b[j1])
+    if out is None:
+        out = torch.empty(hi - lo, dtype=torch.int64, device=device)
+    whole = (s0, e1) == (lo, hi)
+    buf = out if whole else torch.empty(e1 - s0, dtype=torch.int64, device=device)
+    _config5_raw(s0, e1, n, seed, device, buf)
+    _sort_segments(buf, b[i0: j1 + 1], s0)
+    if not whole:
+        out.copy_(buf[lo - s0: hi - s0])
     return out
+
+
+def config5_device(n: int = CONFIG5_N, seed: int = 1, device="cuda", out=None,
+                   mean: float = float(1 << 16)):
+    """The whole config-5 array on the device (config5_range(0, n))."""
+    return config5_range(0, n, n, seed, device, out, mean)
 
 
 @dataclass(frozen=True)
