@@ -178,6 +178,21 @@ size_t rs_kway_workspace_bytes(int key_dtype, int tag_bytes, const rs_shard* sha
 int rs_kway_merge(int key_dtype, int tag_bytes, const rs_shard* shards, int w, void* out_keys, void* out_tags,
                   void* workspace, size_t ws_bytes, void* stream);
 
+/* The same, fully on the device for the sharded sort (no host round trip
+ * between the local sorts and the merge).  rs_corank_rank: shard i is
+ * [0, dlens[i]) (dlens: device array of w lengths, e.g. an all-gather result)
+ * and dsplit (device, 2 x w) receives the split vectors of rank `rank`'s output
+ * range [sum dlens[0..rank), sum dlens[0..rank]) -- row 0 its start, row 1 its
+ * end.  rs_kway_merge_split merges the ranges dsplit describes (shards[i].lo/hi
+ * are ignored); out_len = the ranges' total length, known to the caller as its
+ * own shard length.  Both asynchronous on `stream`. */
+int rs_corank_rank(int key_dtype, const rs_shard* shards, int w, const int64_t* dlens, int rank,
+                   int64_t* dsplit, void* stream);
+size_t rs_kway_split_workspace_bytes(int key_dtype, int tag_bytes, int w, int64_t out_len);
+int rs_kway_merge_split(int key_dtype, int tag_bytes, const rs_shard* shards, int w, const int64_t* dsplit,
+                        int64_t out_len, void* out_keys, void* out_tags, void* workspace, size_t ws_bytes,
+                        void* stream);
+
 /* CUDA IPC for the peer-mapped shards: rs_ipc_alloc allocates `bytes` of device
  * memory and writes its 64-byte IPC handle; another process on the node maps it
  * with rs_ipc_open (peer access enabled lazily) and unmaps with rs_ipc_close;

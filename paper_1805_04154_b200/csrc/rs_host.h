@@ -19,6 +19,7 @@
 #include <condition_variable>
 #include <cstring>
 #include <functional>
+#include <memory>
 #include <mutex>
 #include <thread>
 #include <vector>
@@ -36,20 +37,38 @@ class Pool {
     return *p;
   }
   int size() const { return (int)threads_.size(); }
-  // Run f(0..k-1) on the pool and wait for all of them.
-  void run(int k, const std::function<void(int)>& f) {
-    std::mutex mu;
-    std::condition_variable cv;
-    int left = k;
+  // A batch of k tasks f(0..k-1) running on the pool; wait() joins them.
+  class Batch {
+   public:
+    void wait() {
+      std::unique_lock<std::mutex> lk(mu_);
+      cv_.wait(lk, [&] { return left_ == 0; });
+    }
+
+   private:
+    friend class Pool;
+    std::mutex mu_;
+    std::condition_variable cv_;
+    int left_ = 0;
+    std::function<void(int)> f_;
+  };
+  // Start f(0..k-1) on the pool (f must outlive the batch's wait()).
+  void start(Batch& b, int k, std::function<void(int)> f) {
+    b.left_ = k;
+    b.f_ = std::move(f);
     for (int i = 0; i < k; ++i) {
-      push([&, i] {
-        f(i);
-        std::lock_guard<std::mutex> lk(mu);
-        if (--left == 0) cv.notify_one();
+      push([&b, i] {
+        b.f_(i);
+        std::lock_guard<std::mutex> lk(b.mu_);
+        if (--b.left_ == 0) b.cv_.notify_all();
       });
     }
-    std::unique_lock<std::mutex> lk(mu);
-    cv.wait(lk, [&] { return left == 0; });
+  }
+  // Run f(0..k-1) on the pool and wait for all of them.
+  void run(int k, std::function<void(int)> f) {
+    Batch b;
+    start(b, k, std::move(f));
+    b.wait();
   }
 
  private:
@@ -142,12 +161,21 @@ class Session {
       if (w.st) cudaStreamDestroy(w.st);
     }
   }
+  // Workers for a transfer of total_bytes (streams, events and pinned slots
+  // are kept across calls: the session is cached per host thread and device).
   bool init(size_t total_bytes) {
     int T = Pool::get().size();
     size_t nchunks = (total_bytes + kChunk - 1) / kChunk;
     if ((size_t)T > nchunks) T = (int)std::max<size_t>(1, nchunks);
+    if ((int)w_.size() >= T) {
+      active_ = T;
+      return true;
+    }
+    size_t have = w_.size();
     w_.resize(T);
-    for (auto& w : w_) {
+    active_ = T;
+    for (size_t i = have; i < w_.size(); ++i) {
+      W& w = w_[i];
       if (cudaStreamCreateWithFlags(&w.st, cudaStreamNonBlocking) != cudaSuccess) return false;
       if (cudaEventCreateWithFlags(&w.done, cudaEventDisableTiming) != cudaSuccess) return false;
       for (int b = 0; b < 2; ++b) {
@@ -170,7 +198,7 @@ class Session {
   bool h2d(const std::vector<Span>& spans, cudaStream_t st) {
     std::vector<Chunk> c = chunks(spans);
     std::atomic<int> bad{0};
-    const int T = (int)w_.size();
+    const int T = active_;
     Pool::get().run(T, [&](int t) {
       cudaSetDevice(dev_);
       W& w = w_[t];
@@ -187,7 +215,8 @@ class Session {
       }
     });
     if (bad) return false;
-    for (auto& w : w_) {
+    for (int t = 0; t < T; ++t) {
+      W& w = w_[t];
       if (cudaEventRecord(w.done, w.st) != cudaSuccess || cudaStreamWaitEvent(st, w.done, 0) != cudaSuccess)
         return false;
     }
@@ -206,7 +235,7 @@ class Session {
     std::condition_variable cv;
     int verdict = 1;  // 1 pending, 0 ok, else error
     std::atomic<int> bad{0};
-    const int T = (int)w_.size();
+    const int T = active_;
     int rc_check = 0;
     // the DMAs are issued by the pool; this thread decides whether they may land
     auto work = [&](int t) {
@@ -241,14 +270,15 @@ class Session {
       for (size_t k = m >= 2 ? m - 2 : 0; k < m; ++k) land(k);
     };
     // the verdict comes from `check` on this thread while the pool copies
-    std::thread pool_side([&] { Pool::get().run(T, work); });
+    Pool::Batch batch;
+    Pool::get().start(batch, T, work);
     rc_check = check();
     {
       std::lock_guard<std::mutex> lk(mu);
       verdict = rc_check == 0 ? 0 : 2;
     }
     cv.notify_all();
-    pool_side.join();
+    batch.wait();
     cudaEventDestroy(ready);
     if (rc_check) return rc_check;
     return bad ? -1 : 0;
@@ -262,8 +292,17 @@ class Session {
     void* slot[2] = {nullptr, nullptr};
   };
   int dev_;
+  int active_ = 0;
   std::vector<W> w_;
 };
+
+// The calling thread's session for `dev` (created on first use).
+inline Session& session_for(int dev) {
+  thread_local std::vector<std::unique_ptr<Session>> per_dev;
+  if ((int)per_dev.size() <= dev) per_dev.resize(dev + 1);
+  if (!per_dev[dev]) per_dev[dev].reset(new Session(dev));
+  return *per_dev[dev];
+}
 
 }  // namespace host
 }  // namespace rs

@@ -60,17 +60,39 @@ __device__ __forceinline__ int64_t count_before(const K* a, int64_t lo, int64_t 
 
 // One block (kCorankThreads) per target; out[b * w + i] = c_i(targets[b]).
 constexpr int kCorankThreads = 1024;
+// With `dlens` (device, W shard lengths): shard i is [0, dlens[i]) and block
+// b in {0, 1} computes target sum(dlens[0..g+b)) -- rank g's output range,
+// entirely on the device (no host round trip between the local sorts and the
+// merge).
 template <typename K>
 __global__ void __launch_bounds__(kCorankThreads) k_corank(KwayShards S, const int64_t* __restrict__ targets,
-                                                           int64_t* __restrict__ out) {
+                                                           int64_t* __restrict__ out, const int64_t* __restrict__ dlens,
+                                                           int g) {
   const int W = S.w;
   __shared__ int64_t sL[kKwayMaxW], sH[kKwayMaxW];
+  __shared__ int64_t s_t;
+  if (dlens) {
+    if (threadIdx.x == 0) {
+      int64_t t = 0;
+      for (int i = 0; i < g + (int)blockIdx.x; ++i) t += dlens[i];
+      s_t = t;
+    }
+  } else if (threadIdx.x == 0) {
+    s_t = targets[blockIdx.x];
+  }
+  __syncthreads();
+  if (dlens) {  // every thread's copy of the range table
+    for (int i = 0; i < W; ++i) {
+      S.lo[i] = 0;
+      S.hi[i] = dlens[i];
+    }
+  }
   __shared__ int64_t s_cnt[kCorankThreads];
   __shared__ uint8_t s_flag[kCorankThreads];  // 1: below bracket (p in prefix), 2: above (p not in prefix)
   __shared__ int8_t s_cls[kCorankThreads];    // per pivot: +1 in prefix, -1 not, 0 exact, 2 inactive
   __shared__ int s_active;
   const int tid = threadIdx.x;
-  const int64_t t = targets[blockIdx.x];
+  const int64_t t = s_t;
   if (tid == 0) {
     int64_t total = 0;
     for (int i = 0; i < W; ++i) total += S.hi[i] - S.lo[i];
@@ -170,11 +192,27 @@ struct KwayPiv {
   int64_t off[kKwayMaxW + 1];  // prefix of per-shard pivot counts
 };
 
+// With `dsplit` (device, 2 x W: lo row, hi row) the ranges come from the
+// co-rank kernel instead of S.lo / S.hi; the pivot table and its count are
+// then derived here (npiv_cap bounds the grid-stride loop).  The number of
+// work items (npiv + 1) goes to *nitems for the merge kernel.
 template <typename K>
 __global__ void __launch_bounds__(256) k_kway_pivots(KwayShards S, int64_t spacing, KwayPiv piv_off,
-                                                     int64_t npiv, int64_t* __restrict__ bounds) {
+                                                     int64_t npiv, int64_t* __restrict__ bounds,
+                                                     const int64_t* __restrict__ dsplit, int64_t* __restrict__ nitems) {
   const int W = S.w;
   const int lane = threadIdx.x & 31;
+  if (dsplit) {
+    npiv = 0;
+    piv_off.off[0] = 0;
+    for (int i = 0; i < W; ++i) {
+      S.lo[i] = dsplit[i];
+      S.hi[i] = dsplit[W + i];
+      piv_off.off[i + 1] = piv_off.off[i] + (S.hi[i] - S.lo[i] + spacing - 1) / spacing;
+    }
+    npiv = piv_off.off[W];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *nitems = npiv + 1;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   if (warp == 0 && lane < W) {
@@ -237,8 +275,8 @@ __device__ __forceinline__ void cp_async_elem(void* s, const void* g) {
 
 struct KwayMergeArgs {
   KwayShards S;
-  const int64_t* bounds;  // (nitems + 1) x W split vectors
-  int64_t nitems;
+  const int64_t* bounds;  // (nitems + 1) x W split vectors; row 0 = the ranges' starts
+  const int64_t* nitems;  // written by k_kway_pivots
   void* out_keys;
   void* out_tags;
   unsigned long long* claim;  // zeroed before launch
@@ -306,12 +344,13 @@ __global__ void __launch_bounds__(512, 1) k_kway_merge(KwayMergeArgs A) {
     ls[1] = ls[0] + n0;
   }
   K* okeys = reinterpret_cast<K*>(A.out_keys);
+  const int64_t nitems = *A.nitems;
   for (;;) {
     __syncthreads();
     if (tid == 0) s_item = (int64_t)atomicAdd(A.claim, 1ull);
     __syncthreads();
     const int64_t item = s_item;
-    if (item >= A.nitems) break;
+    if (item >= nitems) break;
     if (tid < W) {
       int64_t lo = A.bounds[item * W + tid], hi = A.bounds[(item + 1) * W + tid];
       s_cur[tid] = lo;
@@ -320,7 +359,7 @@ __global__ void __launch_bounds__(512, 1) k_kway_merge(KwayMergeArgs A) {
     }
     if (tid == 0) {
       int64_t o = 0;
-      for (int i = 0; i < W; ++i) o += A.bounds[item * W + i] - A.S.lo[i];
+      for (int i = 0; i < W; ++i) o += A.bounds[item * W + i] - A.bounds[i];
       s_out = o;
     }
     __syncthreads();

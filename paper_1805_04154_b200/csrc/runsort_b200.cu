@@ -11,6 +11,7 @@
 //   6. k_classify / k_task_offsets / k_task_fill   executor task list
 //   7. k_execute       persistent dataflow executor (leaves + merges)
 #include <algorithm>
+#include <chrono>
 #include <functional>
 #include <map>
 #include <cstdio>
@@ -86,6 +87,7 @@ struct Tunables {
   bool no_pdl = false;   // RS_NO_PDL: plain launches instead of programmatic dependent launch
   bool prep_twice = false;  // RS_PREP_TWICE (RS_INSTR builds): a second, warm-code prep
   int debug_algo = -1;   // RS_DEBUG_ALGO: rs_debug_counters reads another algorithm's layout
+  bool host_trace = false;  // RS_HOST_TRACE: rs_sort_host phase timings on stderr
 };
 const Tunables& tun() {
   static const Tunables t = [] {
@@ -102,6 +104,7 @@ const Tunables& tun() {
     v.no_pdl = getenv("RS_NO_PDL") != nullptr;
     v.prep_twice = getenv("RS_PREP_TWICE") != nullptr;
     v.debug_algo = geti("RS_DEBUG_ALGO", -1);
+    v.host_trace = getenv("RS_HOST_TRACE") != nullptr;
     return v;
   }();
   return t;
@@ -914,6 +917,37 @@ int dispatch_tags(int algo, K* keys, int tb, void* tags, int64_t n, int w, int c
   return run_powersort<K, 8>(keys, tags, n, w, classic, ws, L, st);
 }
 
+// ------------------------------------------------ rs_sort_host helpers
+// The calling thread's stream for host-buffer sorts on `dev` (kept).
+cudaStream_t host_stream(int dev) {
+  thread_local std::vector<cudaStream_t> per_dev;
+  if ((int)per_dev.size() <= dev) per_dev.resize(dev + 1, nullptr);
+  if (!per_dev[dev] && cudaStreamCreateWithFlags(&per_dev[dev], cudaStreamNonBlocking) != cudaSuccess) {
+    per_dev[dev] = nullptr;
+  }
+  return per_dev[dev];
+}
+
+// RS_HOST_TRACE=1: wall-clock phases of rs_sort_host on stderr.
+struct HostTrace {
+  bool on = tun().host_trace;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now(), last = t0;
+  std::string line;
+  void mark(const char* what) {
+    if (!on) return;
+    auto t = std::chrono::steady_clock::now();
+    char b[96];
+    snprintf(b, sizeof b, " %s %.3f", what, std::chrono::duration<double, std::milli>(t - last).count());
+    line += b;
+    last = t;
+  }
+  void print(int64_t n) {
+    if (!on) return;
+    fprintf(stderr, "[rs_sort_host n=%lld total %.3f ms]%s\n", (long long)n,
+            std::chrono::duration<double, std::milli>(last - t0).count(), line.c_str());
+  }
+};
+
 // ------------------------------------------------ cross-GPU merge (rs_kway.cuh)
 int load_shards(const rs_shard* shards, int w, int tag_bytes, KwayShards* S) {
   if (w < 1 || w > kKwayMaxW) return fail(RS_EINVAL, "between 1 and 8 shards");
@@ -933,26 +967,35 @@ int load_shards(const rs_shard* shards, int w, int tag_bytes, KwayShards* S) {
 }
 
 struct KwayLayout {
-  int64_t spacing, npiv;
+  int64_t spacing, npiv, npiv_cap;
   KwayPiv piv;
-  size_t o_bounds, o_claim, total;
+  size_t o_bounds, o_nitems, o_claim, total;
 };
 
+// out_len: the merged length (the ranges' total); with device-resident ranges
+// only it is known on the host, which bounds the pivot count.
 template <typename K, int TB>
-KwayLayout kway_layout(const KwayShards& S, int sms) {
+KwayLayout kway_layout(const KwayShards& S, int64_t out_len, bool dev_ranges, int sms) {
   KwayLayout KL{};
-  int64_t M = 0;
-  for (int i = 0; i < S.w; ++i) M += S.hi[i] - S.lo[i];
+  int64_t M = out_len;
   int64_t sp = M / (8 * (int64_t)sms);  // ~8 work items per SM
   if (sp > ((int64_t)1 << 17)) sp = (int64_t)1 << 17;
   if (sp < KwayCfg<K, TB>::KS) sp = KwayCfg<K, TB>::KS;
   KL.spacing = sp;
   KL.piv.off[0] = 0;
-  for (int i = 0; i < S.w; ++i) KL.piv.off[i + 1] = KL.piv.off[i] + (S.hi[i] - S.lo[i] + sp - 1) / sp;
-  KL.npiv = KL.piv.off[S.w];
+  if (!dev_ranges) {
+    for (int i = 0; i < S.w; ++i) KL.piv.off[i + 1] = KL.piv.off[i] + (S.hi[i] - S.lo[i] + sp - 1) / sp;
+    KL.npiv = KL.piv.off[S.w];
+    KL.npiv_cap = KL.npiv;
+  } else {
+    KL.npiv = 0;
+    KL.npiv_cap = M / sp + S.w;
+  }
   size_t off = 0;
   KL.o_bounds = off;
-  off = align_up(off + (size_t)(KL.npiv + 2) * S.w * 8, 256);
+  off = align_up(off + (size_t)(KL.npiv_cap + 2) * S.w * 8, 256);
+  KL.o_nitems = off;
+  off = align_up(off + 8, 256);
   KL.o_claim = off;
   off = align_up(off + 8, 256);
   KL.total = off + 256;
@@ -960,18 +1003,20 @@ KwayLayout kway_layout(const KwayShards& S, int sms) {
 }
 
 template <typename K, int TB>
-int run_kway(const KwayShards& S, void* out_keys, void* out_tags, unsigned char* ws, size_t ws_bytes, cudaStream_t st) {
+int run_kway(const KwayShards& S, const int64_t* dsplit, int64_t out_len, void* out_keys, void* out_tags,
+             unsigned char* ws, size_t ws_bytes, cudaStream_t st) {
   int sms;
   if (int e = device_sms(&sms)) return e;
-  KwayLayout KL = kway_layout<K, TB>(S, sms);
+  KwayLayout KL = kway_layout<K, TB>(S, out_len, dsplit != nullptr, sms);
   if (ws_bytes < KL.total) return fail(RS_ENOMEM, "k-way merge workspace too small");
   int64_t* bounds = reinterpret_cast<int64_t*>(ws + KL.o_bounds);
+  int64_t* nitems = reinterpret_cast<int64_t*>(ws + KL.o_nitems);
   unsigned long long* claim = reinterpret_cast<unsigned long long*>(ws + KL.o_claim);
   RS_CUDA(cudaMemsetAsync(claim, 0, 8, st));
-  int64_t pw = KL.npiv * 32;
+  int64_t pw = (KL.npiv_cap > 0 ? KL.npiv_cap : 1) * 32;
   int pgrid = (int)std::min<int64_t>((pw + 255) / 256, (int64_t)sms * 8);
   if (pgrid < 1) pgrid = 1;
-  k_kway_pivots<K><<<pgrid, 256, 0, st>>>(S, KL.spacing, KL.piv, KL.npiv, bounds);
+  k_kway_pivots<K><<<pgrid, 256, 0, st>>>(S, KL.spacing, KL.piv, KL.npiv, bounds, dsplit, nitems);
   RS_CUDA(cudaGetLastError());
   int wp = 1;
   while (wp < S.w) wp <<= 1;
@@ -983,14 +1028,41 @@ int run_kway(const KwayShards& S, void* out_keys, void* out_tags, unsigned char*
   KwayMergeArgs A;
   A.S = S;
   A.bounds = bounds;
-  A.nitems = KL.npiv + 1;
+  A.nitems = nitems;
   A.out_keys = out_keys;
   A.out_tags = out_tags;
   A.claim = claim;
-  int grid = (int)std::min<int64_t>((int64_t)sms * occ, A.nitems);
+  int grid = (int)std::min<int64_t>((int64_t)sms * occ, KL.npiv_cap + 1);
   k_kway_merge<K, TB><<<grid, KwayCfg<K, TB>::THREADS, sm, st>>>(A);
   RS_CUDA(cudaGetLastError());
   return RS_OK;
+}
+
+template <int TB>
+int kway_dispatch_tb(int key_dtype, const KwayShards& S, const int64_t* dsplit, int64_t M, void* ok, void* ot,
+                     unsigned char* ws, size_t wsb, cudaStream_t st) {
+  if (key_dtype == RS_KEY_I64) return run_kway<int64_t, TB>(S, dsplit, M, ok, ot, ws, wsb, st);
+  return run_kway<int32_t, TB>(S, dsplit, M, ok, ot, ws, wsb, st);
+}
+
+int kway_dispatch(int key_dtype, int tag_bytes, const KwayShards& S, const int64_t* dsplit, int64_t M, void* ok,
+                  void* ot, unsigned char* ws, size_t wsb, cudaStream_t st) {
+  if (tag_bytes == 0) return kway_dispatch_tb<0>(key_dtype, S, dsplit, M, ok, ot, ws, wsb, st);
+  if (tag_bytes == 4) return kway_dispatch_tb<4>(key_dtype, S, dsplit, M, ok, ot, ws, wsb, st);
+  return kway_dispatch_tb<8>(key_dtype, S, dsplit, M, ok, ot, ws, wsb, st);
+}
+
+size_t kway_ws(int key_dtype, int tag_bytes, const KwayShards& S, int64_t M, bool dev_ranges) {
+  int sms;
+  if (device_sms(&sms)) sms = 148;
+  if (key_dtype == RS_KEY_I64) {
+    return tag_bytes == 0 ? kway_layout<int64_t, 0>(S, M, dev_ranges, sms).total
+                          : (tag_bytes == 4 ? kway_layout<int64_t, 4>(S, M, dev_ranges, sms).total
+                                            : kway_layout<int64_t, 8>(S, M, dev_ranges, sms).total);
+  }
+  return tag_bytes == 0 ? kway_layout<int32_t, 0>(S, M, dev_ranges, sms).total
+                        : (tag_bytes == 4 ? kway_layout<int32_t, 4>(S, M, dev_ranges, sms).total
+                                          : kway_layout<int32_t, 8>(S, M, dev_ranges, sms).total);
 }
 
 }  // namespace
@@ -1014,8 +1086,8 @@ int rs_corank(int key_dtype, const rs_shard* shards, int w, const int64_t* targe
   int64_t* dout = reinterpret_cast<int64_t*>(reinterpret_cast<unsigned char*>(workspace) +
                                              align_up((size_t)ntargets * 8, 256));
   RS_CUDA(cudaMemcpyAsync(dt, targets, (size_t)ntargets * 8, cudaMemcpyHostToDevice, st));
-  if (key_dtype == RS_KEY_I64) k_corank<int64_t><<<ntargets, kCorankThreads, 0, st>>>(S, dt, dout);
-  else k_corank<int32_t><<<ntargets, kCorankThreads, 0, st>>>(S, dt, dout);
+  if (key_dtype == RS_KEY_I64) k_corank<int64_t><<<ntargets, kCorankThreads, 0, st>>>(S, dt, dout, nullptr, 0);
+  else k_corank<int32_t><<<ntargets, kCorankThreads, 0, st>>>(S, dt, dout, nullptr, 0);
   RS_CUDA(cudaGetLastError());
   RS_CUDA(cudaMemcpyAsync(out, dout, (size_t)ntargets * w * 8, cudaMemcpyDeviceToHost, st));
   RS_CUDA(cudaStreamSynchronize(st));
@@ -1025,14 +1097,9 @@ int rs_corank(int key_dtype, const rs_shard* shards, int w, const int64_t* targe
 size_t rs_kway_workspace_bytes(int key_dtype, int tag_bytes, const rs_shard* shards, int w) {
   KwayShards S;
   if (load_shards(shards, w, 0, &S)) return 0;
-  int sms;
-  if (device_sms(&sms)) sms = 148;
-  if (key_dtype == RS_KEY_I64) {
-    return tag_bytes == 0 ? kway_layout<int64_t, 0>(S, sms).total
-                          : (tag_bytes == 4 ? kway_layout<int64_t, 4>(S, sms).total : kway_layout<int64_t, 8>(S, sms).total);
-  }
-  return tag_bytes == 0 ? kway_layout<int32_t, 0>(S, sms).total
-                        : (tag_bytes == 4 ? kway_layout<int32_t, 4>(S, sms).total : kway_layout<int32_t, 8>(S, sms).total);
+  int64_t M = 0;
+  for (int i = 0; i < w; ++i) M += S.hi[i] - S.lo[i];
+  return kway_ws(key_dtype, tag_bytes, S, M, false);
 }
 
 int rs_kway_merge(int key_dtype, int tag_bytes, const rs_shard* shards, int w, void* out_keys, void* out_tags,
@@ -1045,16 +1112,54 @@ int rs_kway_merge(int key_dtype, int tag_bytes, const rs_shard* shards, int w, v
   for (int i = 0; i < w; ++i) M += S.hi[i] - S.lo[i];
   if (M == 0) return RS_OK;
   if (!out_keys || (tag_bytes && !out_tags) || !workspace) return fail(RS_EINVAL, "null output or workspace");
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  unsigned char* ws = reinterpret_cast<unsigned char*>(workspace);
-  if (key_dtype == RS_KEY_I64) {
-    if (tag_bytes == 0) return run_kway<int64_t, 0>(S, out_keys, out_tags, ws, ws_bytes, st);
-    if (tag_bytes == 4) return run_kway<int64_t, 4>(S, out_keys, out_tags, ws, ws_bytes, st);
-    return run_kway<int64_t, 8>(S, out_keys, out_tags, ws, ws_bytes, st);
+  return kway_dispatch(key_dtype, tag_bytes, S, nullptr, M, out_keys, out_tags,
+                       reinterpret_cast<unsigned char*>(workspace), ws_bytes, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int rs_corank_rank(int key_dtype, const rs_shard* shards, int w, const int64_t* dlens, int rank, int64_t* dsplit,
+                   void* stream) {
+  KwayShards S;
+  if (key_dtype != RS_KEY_I32 && key_dtype != RS_KEY_I64) return fail(RS_EUNSUPPORTED, "keys must be int32 or int64");
+  if (w < 1 || w > kKwayMaxW || !shards) return fail(RS_EINVAL, "between 1 and 8 shards");
+  if (rank < 0 || rank >= w || !dlens || !dsplit) return fail(RS_EINVAL, "bad rank / null device arrays");
+  memset(&S, 0, sizeof(S));
+  S.w = w;
+  for (int i = 0; i < w; ++i) {
+    S.keys[i] = shards[i].keys;
+    S.tags[i] = shards[i].tags;
   }
-  if (tag_bytes == 0) return run_kway<int32_t, 0>(S, out_keys, out_tags, ws, ws_bytes, st);
-  if (tag_bytes == 4) return run_kway<int32_t, 4>(S, out_keys, out_tags, ws, ws_bytes, st);
-  return run_kway<int32_t, 8>(S, out_keys, out_tags, ws, ws_bytes, st);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (key_dtype == RS_KEY_I64) k_corank<int64_t><<<2, kCorankThreads, 0, st>>>(S, nullptr, dsplit, dlens, rank);
+  else k_corank<int32_t><<<2, kCorankThreads, 0, st>>>(S, nullptr, dsplit, dlens, rank);
+  RS_CUDA(cudaGetLastError());
+  return RS_OK;
+}
+
+size_t rs_kway_split_workspace_bytes(int key_dtype, int tag_bytes, int w, int64_t out_len) {
+  if (w < 1 || w > kKwayMaxW || out_len < 0) return 0;
+  KwayShards S;
+  memset(&S, 0, sizeof(S));
+  S.w = w;
+  return kway_ws(key_dtype, tag_bytes, S, out_len, true);
+}
+
+int rs_kway_merge_split(int key_dtype, int tag_bytes, const rs_shard* shards, int w, const int64_t* dsplit,
+                        int64_t out_len, void* out_keys, void* out_tags, void* workspace, size_t ws_bytes,
+                        void* stream) {
+  KwayShards S;
+  if (key_dtype != RS_KEY_I32 && key_dtype != RS_KEY_I64) return fail(RS_EUNSUPPORTED, "keys must be int32 or int64");
+  if (tag_bytes != 0 && tag_bytes != 4 && tag_bytes != 8) return fail(RS_EUNSUPPORTED, "tags must be 4 or 8 bytes wide");
+  if (w < 1 || w > kKwayMaxW || !shards || !dsplit) return fail(RS_EINVAL, "between 1 and 8 shards, device split");
+  if (out_len == 0) return RS_OK;
+  if (!out_keys || (tag_bytes && !out_tags) || !workspace) return fail(RS_EINVAL, "null output or workspace");
+  memset(&S, 0, sizeof(S));
+  S.w = w;
+  for (int i = 0; i < w; ++i) {
+    S.keys[i] = shards[i].keys;
+    S.tags[i] = shards[i].tags;
+  }
+  return kway_dispatch(key_dtype, tag_bytes, S, dsplit, out_len, out_keys, out_tags,
+                       reinterpret_cast<unsigned char*>(workspace), ws_bytes, reinterpret_cast<cudaStream_t>(stream));
 }
 
 int rs_ipc_alloc(size_t bytes, void** ptr, void* handle) {
@@ -1197,52 +1302,68 @@ int rs_sort_host_ex(int algo, int key_dtype, void* keys, int tag_bytes, void* ta
   RS_CUDA(cudaGetDevice(&dev));
   Layout L = make_layout(n, min_run_len, kb, tag_bytes, algo);
   size_t ws = L.total;
-  void *dk = nullptr, *dt = nullptr, *dws = nullptr;
-  cudaStream_t st;
-  RS_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-  int rc = RS_OK;
+  HostTrace tr;
   {
-    host::Session S(dev);
-    std::vector<host::Span> spans;
-    do {
-      if (cudaMallocAsync(&dk, (size_t)n * kb + 64, st) != cudaSuccess ||
-          (tag_bytes && cudaMallocAsync(&dt, (size_t)n * tag_bytes + 64, st) != cudaSuccess) ||
-          cudaMallocAsync(&dws, ws, st) != cudaSuccess) {
-        cudaGetLastError();
-        rc = fail(RS_ENOMEM, "device allocation failed");
-        break;
+    // device scratch comes from the stream-ordered pool; keep freed blocks
+    // cached in it instead of returning them to the driver at every sync
+    static std::once_flag pool_once[64];
+    std::call_once(pool_once[dev & 63], [dev] {
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
       }
-      spans.push_back({reinterpret_cast<unsigned char*>(keys), reinterpret_cast<unsigned char*>(dk), (size_t)n * kb});
-      if (tag_bytes)
-        spans.push_back({reinterpret_cast<unsigned char*>(tags), reinterpret_cast<unsigned char*>(dt),
-                         (size_t)n * tag_bytes});
-      if (!S.init((size_t)n * (kb + tag_bytes))) {
-        rc = fail(RS_ENOMEM, "pinned staging allocation failed");
-        break;
-      }
-      if (!S.h2d(spans, st)) {
-        rc = fail(RS_ECUDA, "host-to-device copy failed");
-        break;
-      }
-      rc = rs_sort_ex(algo, key_dtype, dk, tag_bytes, dt, n, min_run_len, merge_kind, alpha, dws, ws, st, nullptr,
-                      nullptr);
-      if (rc) break;
-      unsigned char* wsp = reinterpret_cast<unsigned char*>(dws);
-      int d = S.d2h(spans, st, [&]() -> int {
-        int e = read_metrics(L, wsp, st, out);  // synchronizes: the sort is complete
-        if (!e && tree) e = export_tree(L, wsp, st, tree);
-        return e;
-      });
-      if (d > 0) rc = d;  // the device's verdict (nothing was written back)
-      else if (d < 0) rc = fail(RS_ECUDA, "device-to-host copy failed");
-    } while (0);
-    cudaStreamSynchronize(st);
-  }  // staging session: pinned slots back to the pool
+    });
+  }
+  void *dk = nullptr, *dt = nullptr, *dws = nullptr;
+  cudaStream_t st = host_stream(dev);
+  if (!st) return fail(RS_ECUDA, "stream creation failed");
+  int rc = RS_OK;
+  host::Session& S = host::session_for(dev);
+  std::vector<host::Span> spans;
+  do {
+    if (cudaMallocAsync(&dk, (size_t)n * kb + 64, st) != cudaSuccess ||
+        (tag_bytes && cudaMallocAsync(&dt, (size_t)n * tag_bytes + 64, st) != cudaSuccess) ||
+        cudaMallocAsync(&dws, ws, st) != cudaSuccess) {
+      cudaGetLastError();
+      rc = fail(RS_ENOMEM, "device allocation failed");
+      break;
+    }
+    spans.push_back({reinterpret_cast<unsigned char*>(keys), reinterpret_cast<unsigned char*>(dk), (size_t)n * kb});
+    if (tag_bytes)
+      spans.push_back({reinterpret_cast<unsigned char*>(tags), reinterpret_cast<unsigned char*>(dt),
+                       (size_t)n * tag_bytes});
+    if (!S.init((size_t)n * (kb + tag_bytes))) {
+      rc = fail(RS_ENOMEM, "pinned staging allocation failed");
+      break;
+    }
+    tr.mark("alloc+init");
+    if (!S.h2d(spans, st)) {
+      rc = fail(RS_ECUDA, "host-to-device copy failed");
+      break;
+    }
+    tr.mark("h2d queued");
+    rc = rs_sort_ex(algo, key_dtype, dk, tag_bytes, dt, n, min_run_len, merge_kind, alpha, dws, ws, st, nullptr,
+                    nullptr);
+    if (rc) break;
+    tr.mark("sort queued");
+    unsigned char* wsp = reinterpret_cast<unsigned char*>(dws);
+    int d = S.d2h(spans, st, [&]() -> int {
+      int e = read_metrics(L, wsp, st, out);  // synchronizes: the sort is complete
+      tr.mark("sort done");
+      if (!e && tree) e = export_tree(L, wsp, st, tree);
+      return e;
+    });
+    tr.mark("d2h done");
+    if (d > 0) rc = d;  // the device's verdict (nothing was written back)
+    else if (d < 0) rc = fail(RS_ECUDA, "device-to-host copy failed");
+  } while (0);
   if (dk) cudaFreeAsync(dk, st);
   if (dt) cudaFreeAsync(dt, st);
   if (dws) cudaFreeAsync(dws, st);
   cudaStreamSynchronize(st);
-  cudaStreamDestroy(st);
+  tr.mark("freed");
+  tr.print(n);
   return rc;
 }
 

@@ -313,7 +313,17 @@ def sharded_sort_p2p(space: P2PShardSpace, n_local: int, local_sort: Optional[Ca
     """Globally stable sort of the shards in `space` (this rank: the first
     n_local elements of space.keys / space.tags), NVLink data plane.
 
-    Returns (sorted_slice, tags_slice, info) like sharded_sort.  The shard
+    Over NCCL the whole step is stream-ordered, with no host synchronisation:
+    local powersort -> all-gather of the shard lengths (an NCCL collective
+    cannot complete before every rank has finished the work queued before it,
+    so it doubles as the barrier "every shard is sorted") -> device co-rank of
+    this rank's output range over the peers' shards -> W-way merge reading the
+    peers' shards -> a one-element all-reduce (no rank rewrites its shard
+    buffer before every peer has finished reading it).  With another backend
+    (gloo: the one-GPU test) the barriers are host barriers around the same
+    kernels.
+
+    Returns (sorted_slice, tags_slice, info) like sharded_sort; the shard
     buffers hold each rank's locally sorted shard afterwards.
     """
     import torch
@@ -323,26 +333,41 @@ def sharded_sort_p2p(space: P2PShardSpace, n_local: int, local_sort: Optional[Ca
     dist = _dist()
     group = space.group
     W, g = space.W, space.rank
-    local_sort = local_sort or _default_local_sort
+    nccl = dist.get_backend(group) == "nccl"
     keys = space.keys[:n_local]
     tags = space.tags[:n_local] if space.tags is not None else None
-    m_local = local_sort(keys, tags) if n_local > 1 else None
-    # every shard sorted and visible before any peer reads it
-    torch.cuda.current_stream().synchronize()
-    ns = [None] * W
-    dist.all_gather_object(ns, int(n_local), group=group)  # doubles as the barrier
-    T = np.concatenate([[0], np.cumsum(ns)]).astype(np.int64)
-    shards = [kway.Shard(space.peer_keys[i], space.peer_tags[i], 0, ns[i]) for i in range(W)]
-    c = kway.corank(shards, [int(T[g]), int(T[g + 1])], space.keys.dtype, space.device)
-    mine = [shards[i].with_range(int(c[0][i]), int(c[1][i])) for i in range(W)]
+    if local_sort is not None:
+        m_local = local_sort(keys, tags) if n_local > 1 else None
+    else:  # enqueued without a host sync; its Metrics stay fetchable
+        from .sorters import sort_async
+
+        m_local = sort_async(keys, tags, workspace=getattr(space, "sort_ws", None))
+        if m_local is not None:
+            space.sort_ws = m_local.workspace
     if out_keys is None:
         out_keys = torch.empty(n_local, dtype=space.keys.dtype, device=space.device)
     if tags is not None and out_tags is None:
         out_tags = torch.empty(n_local, dtype=space.tags.dtype, device=space.device)
-    kway.kway_merge(mine, out_keys[:n_local], out_tags[:n_local] if tags is not None else None)
-    # peers may still be reading this rank's shard: nobody rewrites a shard
-    # buffer before every merge has finished
-    torch.cuda.current_stream().synchronize()
-    dist.barrier(group=group)
+    mine = torch.tensor([n_local], dtype=torch.int64, device=space.device)
+    if nccl:
+        dlens = torch.empty(W, dtype=torch.int64, device=space.device)
+        dist.all_gather_into_tensor(dlens, mine, group=group)
+    else:
+        torch.cuda.current_stream().synchronize()
+        ns = [None] * W
+        dist.all_gather_object(ns, int(n_local), group=group)
+        dlens = torch.tensor(ns, dtype=torch.int64, device=space.device)
+    shards = [kway.Shard(space.peer_keys[i], space.peer_tags[i], 0, 0) for i in range(W)]
+    dsplit = torch.empty(2 * W, dtype=torch.int64, device=space.device)
+    kway.corank_rank(shards, dlens, g, dsplit, space.keys.dtype)
+    space.ws = kway.kway_merge_split(shards, dsplit, n_local, out_keys[:n_local],
+                                     out_tags[:n_local] if tags is not None else None,
+                                     workspace=getattr(space, "ws", None))
+    if nccl:
+        done = torch.zeros(1, dtype=torch.int32, device=space.device)
+        dist.all_reduce(done, group=group)
+    else:
+        torch.cuda.current_stream().synchronize()
+        dist.barrier(group=group)
     return out_keys[:n_local], (out_tags[:n_local] if tags is not None else None), \
-        {"local": m_local, "splits": c, "lens": ns}
+        {"local": m_local, "split": dsplit, "lens": dlens}

@@ -103,6 +103,37 @@ def kway_merge(shards: Sequence[Shard], out_keys, out_tags=None, stream=None, wo
     return workspace
 
 
+def corank_rank(shards: Sequence[Shard], dlens, rank: int, dsplit, key_dtype, stream=None) -> None:
+    """Device-only co-rank of rank `rank`'s output range: shard i is
+    [0, dlens[i]) (device int64 tensor of W lengths); dsplit (device int64,
+    2 x W) receives the start and end split vectors.  Async."""
+    torch = _torch()
+    L = _lib.lib()
+    st = stream or torch.cuda.current_stream(dsplit.device)
+    arr = _shard_array(shards)
+    _lib.check(L.rs_corank_rank(key_code(key_dtype), arr, len(shards), dlens.data_ptr(), int(rank),
+                                dsplit.data_ptr(), st.cuda_stream))
+
+
+def kway_merge_split(shards: Sequence[Shard], dsplit, out_len: int, out_keys, out_tags=None, stream=None,
+                     workspace=None):
+    """W-way merge of the ranges in dsplit (device, 2 x W); async."""
+    torch = _torch()
+    L = _lib.lib()
+    W = len(shards)
+    tb = out_tags.element_size() if out_tags is not None else 0
+    kc = key_code(out_keys.dtype)
+    need = L.rs_kway_split_workspace_bytes(kc, tb, W, int(out_len))
+    if workspace is None or workspace.numel() < need:
+        workspace = torch.empty(max(need, 256), dtype=torch.uint8, device=out_keys.device)
+    st = stream or torch.cuda.current_stream(out_keys.device)
+    arr = _shard_array(shards)
+    _lib.check(L.rs_kway_merge_split(kc, tb, arr, W, dsplit.data_ptr(), int(out_len), out_keys.data_ptr(),
+                                     out_tags.data_ptr() if out_tags is not None else None,
+                                     workspace.data_ptr(), workspace.numel(), st.cuda_stream))
+    return workspace
+
+
 # ------------------------------------------------------------------ IPC ----
 class _CAI:
     def __init__(self, ptr: int, n: int, itemsize: int):

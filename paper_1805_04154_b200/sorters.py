@@ -31,6 +31,7 @@ __all__ = [
     "node_power_def",
     "node_power_bitwise",
     "SORTERS",
+    "sort_async",
 ]
 
 MERGE_KINDS = ("bitonic", "classic")
@@ -352,6 +353,58 @@ def _device_sort_on(algo: int, a, cfg: SortConfig, metrics: Metrics, tags, dev) 
         powers = bufs[1][: r - 1] if algo == _lib.RS_ALGO_POWERSORT else None
         metrics.merge_tree = tree_from_depths(lens, depths, powers)
     return metrics
+
+
+class PendingSort:
+    """A device sort enqueued by ``sort_async``; ``metrics()`` synchronizes the
+    stream and returns the call's Metrics (the reference's counters)."""
+
+    def __init__(self, algo, code, tb, n, w, ws, stream):
+        self._args = (algo, code, tb, n, w)
+        self.workspace = ws
+        self.stream = stream
+
+    def metrics(self) -> Metrics:
+        algo, code, tb, n, w = self._args
+        out = _lib.RsMetrics()
+        _lib.check(_lib.lib().rs_fetch_metrics(algo, code, tb, n, w, self.workspace.data_ptr(),
+                                               self.stream.cuda_stream, ctypes.byref(out)))
+        m = Metrics()
+        _accumulate(algo, m, out)
+        return m
+
+
+def sort_async(keys, tags=None, cfg: Optional[SortConfig] = None, algo: str = "powersort",
+               workspace=None) -> Optional[PendingSort]:
+    """Enqueue powersort / peeksort of contiguous int32/int64 CUDA tensors (tags
+    4 or 8 bytes) on the current stream, in place, without any host
+    synchronisation (the building block of the sharded sort: the caller's
+    next stream work follows the sort).  ``workspace`` (a uint8 CUDA tensor)
+    is reused when large enough.  Returns None for n <= 1."""
+    torch = _torch()
+    L = _lib.lib()
+    cfg = cfg or SortConfig()
+    code = {"powersort": _lib.RS_ALGO_POWERSORT, "peeksort": _lib.RS_ALGO_PEEKSORT}[algo]
+    n = int(keys.numel())
+    if n <= 1:
+        return None
+    if keys.device.type != "cuda" or not keys.is_contiguous() or keys.dtype not in (torch.int32, torch.int64):
+        raise NotImplementedError("sort_async takes contiguous int32/int64 CUDA tensors")
+    if tags is not None and (tags.device != keys.device or not tags.is_contiguous() or
+                             tags.element_size() not in (4, 8) or tags.numel() != n):
+        raise ValueError("tags must be a contiguous 4/8-byte CUDA tensor of the keys' length and device")
+    kc = _lib.RS_KEY_I32 if keys.dtype == torch.int32 else _lib.RS_KEY_I64
+    tb = tags.element_size() if tags is not None else 0
+    w = int(cfg.min_run_len)
+    need = L.rs_workspace_bytes(code, kc, tb, n, w)
+    if workspace is None or workspace.numel() < need:
+        workspace = torch.empty(need, dtype=torch.uint8, device=keys.device)
+    stream = torch.cuda.current_stream(keys.device)
+    kind = _lib.RS_MERGE_CLASSIC if cfg.merge_kind == "classic" else _lib.RS_MERGE_BITONIC
+    _lib.check(L.rs_sort_ex(code, kc, keys.data_ptr(), tb, tags.data_ptr() if tags is not None else None, n, w,
+                            kind, float(cfg.alpha), workspace.data_ptr(), workspace.numel(), stream.cuda_stream,
+                            None, None))
+    return PendingSort(code, kc, tb, n, w, workspace, stream)
 
 
 def _entry(algo, a, cfg, metrics, tags):

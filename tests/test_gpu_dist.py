@@ -108,3 +108,33 @@ def test_p2p_world2():
         order = np.argsort(allk, kind="stable")
         assert np.array_equal(np.concatenate([res[(case, r)][0] for r in range(W)]), allk[order]), case
         assert np.array_equal(np.concatenate([res[(case, r)][1] for r in range(W)]), allt[order]), case
+
+
+def test_p2p_world1_nccl_stream_ordered():
+    """The NCCL flavour of the NVLink plane (stream-ordered barriers, device
+    co-rank) at world size 1, plus sort_async's deferred Metrics."""
+    import torch
+    import torch.distributed as dist
+
+    from oracle import oracle
+    from paper_1805_04154_b200 import dist as rsd
+    from paper_1805_04154_b200 import workloads
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_port()), RANK="0", WORLD_SIZE="1")
+    dist.init_process_group("nccl", device_id=torch.device("cuda", 0))
+    try:
+        space = rsd.P2PShardSpace(300000, torch.int32, torch.int32)
+        for seed in (1, 2):
+            k, t = workloads.config4(250000 + seed, seed=seed, mean=300.0)
+            space.keys[: len(k)].copy_(torch.from_numpy(k))
+            space.tags[: len(t)].copy_(torch.from_numpy(t))
+            out, tout, info = rsd.sharded_sort_p2p(space, len(k))
+            rk, rt = k.copy(), t.copy()
+            ref = oracle.powersort(rk, 24, "bitonic", rt)
+            assert np.array_equal(out.cpu().numpy(), rk)
+            assert np.array_equal(tout.cpu().numpy(), rt)
+            m = info["local"].metrics()
+            assert (m.merge_cost, m.comparisons, m.runs_detected, m.max_stack_height) == ref.metrics_tuple()
+        space.close()
+    finally:
+        dist.destroy_process_group()
