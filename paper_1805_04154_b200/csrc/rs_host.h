@@ -3,20 +3,31 @@
 //
 // A caller's numpy array is pageable memory: a plain cudaMemcpy from it runs at
 // a fraction of PCIe speed (the driver stages it through its own small pinned
-// buffer, one CPU thread), and cudaHostRegister costs more than the copy.  Here
-// the array is cut into 4 MiB chunks; a pool of host threads copies chunks into
-// pinned slots (two per thread) and each thread issues the DMA of its chunk
+// buffer, one CPU thread), and cudaHostRegister costs more than the copy (6 ms
+// for 40 MB on the B200 boxes, tools/host_copy_probe.py).  Here the array is
+// cut into chunks (2 MiB); a crew of host threads owned by the calling
+// thread's session copies chunks into pinned slots (two per worker) with
+// streaming stores -- no read-for-ownership of the destination, so a copy costs
+// one read and one write of DRAM -- and each worker issues the DMA of its chunk
 // from its slot on its own stream, so the host copies of later chunks overlap
-// the DMA of earlier ones and the copy engine stays busy.  Device-to-host is the
-// mirror image, queued behind the sort; no byte lands in the caller's buffer
-// before the device reported success (the reference's in-place contract: an
-// AssertionError leaves the input as it was).
+// the DMA of earlier ones and the copy engine stays busy.  Device-to-host is
+// the mirror image, queued behind the sort; no byte lands in the caller's
+// buffer before the device reported success (the reference's in-place
+// contract: an AssertionError leaves the input as it was).
+//
+// Workers spin briefly on a generation counter before sleeping, so a sort's
+// two staging batches do not pay a futex wake-up per worker.
 #pragma once
 #include <cuda_runtime.h>
+#include <immintrin.h>
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <condition_variable>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <memory>
@@ -27,86 +38,69 @@
 namespace rs {
 namespace host {
 
-constexpr size_t kChunk = (size_t)4 << 20;
-
-// Fixed pool of worker threads (started on first use, never stopped).
-class Pool {
- public:
-  static Pool& get() {
-    static Pool* p = new Pool();  // intentionally leaked: workers outlive static destruction
-    return *p;
-  }
-  int size() const { return (int)threads_.size(); }
-  // A batch of k tasks f(0..k-1) running on the pool; wait() joins them.
-  class Batch {
-   public:
-    void wait() {
-      std::unique_lock<std::mutex> lk(mu_);
-      cv_.wait(lk, [&] { return left_ == 0; });
-    }
-
-   private:
-    friend class Pool;
-    std::mutex mu_;
-    std::condition_variable cv_;
-    int left_ = 0;
-    std::function<void(int)> f_;
-  };
-  // Start f(0..k-1) on the pool (f must outlive the batch's wait()).
-  void start(Batch& b, int k, std::function<void(int)> f) {
-    b.left_ = k;
-    b.f_ = std::move(f);
-    for (int i = 0; i < k; ++i) {
-      push([&b, i] {
-        b.f_(i);
-        std::lock_guard<std::mutex> lk(b.mu_);
-        if (--b.left_ == 0) b.cv_.notify_all();
-      });
-    }
-  }
-  // Run f(0..k-1) on the pool and wait for all of them.
-  void run(int k, std::function<void(int)> f) {
-    Batch b;
-    start(b, k, std::move(f));
-    b.wait();
-  }
-
- private:
-  Pool() {
+// Chunk size, crew width and trace level: RS_HOST_CHUNK_KB / RS_HOST_THREADS /
+// RS_HOST_TRACE (2 = per-batch copy statistics), read once.
+inline size_t env_or(const char* k, size_t d) {
+  const char* e = getenv(k);
+  return e && atoll(e) > 0 ? (size_t)atoll(e) : d;
+}
+inline size_t chunk_bytes() {
+  static const size_t c = env_or("RS_HOST_CHUNK_KB", 2048) << 10;
+  return c;
+}
+inline int crew_size() {
+  static const int n = [] {
     unsigned hw = std::thread::hardware_concurrency();
-    int n = (int)std::max(2u, std::min(8u, hw ? hw / 2 : 2u));
-    for (int i = 0; i < n; ++i) threads_.emplace_back([this] { loop(); });
-  }
-  void push(std::function<void()> t) {
-    {
-      std::lock_guard<std::mutex> lk(mu_);
-      q_.push_back(std::move(t));
-    }
-    cv_.notify_one();
-  }
-  void loop() {
-    for (;;) {
-      std::function<void()> t;
-      {
-        std::unique_lock<std::mutex> lk(mu_);
-        cv_.wait(lk, [&] { return !q_.empty(); });
-        t = std::move(q_.front());
-        q_.erase(q_.begin());
-      }
-      t();
-    }
-  }
-  std::vector<std::thread> threads_;
-  std::vector<std::function<void()>> q_;
-  std::mutex mu_;
-  std::condition_variable cv_;
-};
+    return (int)env_or("RS_HOST_THREADS", std::max(2u, std::min(6u, hw ? hw / 2 : 2u)));
+  }();
+  return n;
+}
+inline int trace_level() {
+  static const int t = (int)env_or("RS_HOST_TRACE", 0);
+  return t;
+}
+inline double now_us() {
+  return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
 
-// Pinned slots of kChunk bytes, recycled across calls.
+// Copy with 32-byte streaming stores to a 32-byte aligned destination part
+// (head and tail with plain stores), then a store fence.
+__attribute__((target("avx2"))) inline void copy_stream(void* dst, const void* src, size_t len) {
+  unsigned char* d = static_cast<unsigned char*>(dst);
+  const unsigned char* s = static_cast<const unsigned char*>(src);
+  size_t head = (32 - ((uintptr_t)d & 31)) & 31;
+  if (head > len) head = len;
+  memcpy(d, s, head);
+  d += head;
+  s += head;
+  len -= head;
+  size_t blocks = len / 128;
+  for (size_t i = 0; i < blocks; ++i) {
+    __m256i a = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(s));
+    __m256i b = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(s + 32));
+    __m256i c = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(s + 64));
+    __m256i e = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(s + 96));
+    _mm256_stream_si256(reinterpret_cast<__m256i*>(d), a);
+    _mm256_stream_si256(reinterpret_cast<__m256i*>(d + 32), b);
+    _mm256_stream_si256(reinterpret_cast<__m256i*>(d + 64), c);
+    _mm256_stream_si256(reinterpret_cast<__m256i*>(d + 96), e);
+    d += 128;
+    s += 128;
+  }
+  memcpy(d, s, len - blocks * 128);
+  _mm_sfence();
+}
+inline void copy_fast(void* dst, const void* src, size_t len) {
+  static const bool avx2 = __builtin_cpu_supports("avx2");
+  if (avx2) copy_stream(dst, src, len);
+  else memcpy(dst, src, len);
+}
+
+// Pinned slots of chunk_bytes(), recycled across calls and sessions.
 class Pinned {
  public:
   static Pinned& get() {
-    static Pinned* p = new Pinned();
+    static Pinned* p = new Pinned();  // intentionally leaked: slots outlive static destruction
     return *p;
   }
   void* take() {
@@ -119,7 +113,7 @@ class Pinned {
       }
     }
     void* s = nullptr;
-    if (cudaMallocHost(&s, kChunk) != cudaSuccess) {
+    if (cudaMallocHost(&s, chunk_bytes()) != cudaSuccess) {
       cudaGetLastError();
       return nullptr;
     }
@@ -135,6 +129,74 @@ class Pinned {
   std::mutex mu_;
 };
 
+// A fixed crew of worker threads: start(k, f) runs f(i) on workers i < k,
+// wait() returns when all of them are done.  One batch at a time (the crew
+// belongs to one session, used by one host thread).
+class Crew {
+ public:
+  explicit Crew(int n) {
+    for (int i = 0; i < n; ++i) th_.emplace_back([this, i] { loop(i); });
+  }
+  ~Crew() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+      gen_.fetch_add(1);
+    }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+  }
+  int size() const { return (int)th_.size(); }
+  void start(int k, std::function<void(int)> f) {
+    f_ = std::move(f);
+    k_ = k;
+    left_.store(k);
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      gen_.fetch_add(1, std::memory_order_release);
+    }
+    cv_.notify_all();
+  }
+  void wait() {
+    for (int spin = 0; left_.load(std::memory_order_acquire) != 0; ++spin) {
+      if (spin < 4096) _mm_pause();
+      else std::this_thread::yield();
+    }
+  }
+
+ private:
+  void loop(int i) {
+    uint64_t seen = 0;
+    for (;;) {
+      uint64_t g;
+      int spin = 0;
+      while ((g = gen_.load(std::memory_order_acquire)) == seen && spin < 200000) {
+        _mm_pause();
+        ++spin;
+      }
+      if (g == seen) {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return gen_.load() != seen; });
+        g = gen_.load();
+      }
+      seen = g;
+      if (stop_) return;
+      if (i < k_) {
+        f_(i);
+        left_.fetch_sub(1, std::memory_order_acq_rel);
+      }
+    }
+  }
+  std::vector<std::thread> th_;
+  std::function<void(int)> f_;
+  int k_ = 0;
+  std::atomic<int> left_{0};
+  std::atomic<uint64_t> gen_{0};
+  bool stop_ = false;
+  std::mutex mu_;
+  std::condition_variable cv_;
+};
+
 struct Span {
   unsigned char* host;
   unsigned char* dev;
@@ -146,12 +208,26 @@ struct Chunk {
   size_t off, len;
 };
 
-// One staging session: T workers, each with a stream, two pinned slots and
-// two events, reused for the copy in and the copy out.
+// Per-batch statistics (RS_HOST_TRACE=2): host copy busy time summed over the
+// workers, the batch's wall time, and its copy throughput.
+struct Stats {
+  std::atomic<long long> copy_ns{0};
+  double t0 = 0;
+  void print(const char* what, size_t bytes, int T) const {
+    double wall = now_us() - t0;
+    double busy = copy_ns.load() / 1e3;  // us, summed over workers
+    fprintf(stderr, "[rs_host %s] %zu bytes, %d workers, wall %.1f us, host copies %.1f us busy (%.2f GB/s per worker)\n",
+            what, bytes, T, wall, busy, busy > 0 ? bytes / (busy * 1e3) : 0.0);
+  }
+};
+
+// One staging session: a crew of T workers, each with a stream, two pinned
+// slots and two events, reused for the copy in and the copy out.
 class Session {
  public:
   explicit Session(int dev) : dev_(dev) {}
   ~Session() {
+    crew_.reset();
     for (auto& w : w_) {
       for (int b = 0; b < 2; ++b) {
         if (w.ev[b]) cudaEventDestroy(w.ev[b]);
@@ -160,13 +236,16 @@ class Session {
       if (w.done) cudaEventDestroy(w.done);
       if (w.st) cudaStreamDestroy(w.st);
     }
+    if (ready_) cudaEventDestroy(ready_);
   }
-  // Workers for a transfer of total_bytes (streams, events and pinned slots
-  // are kept across calls: the session is cached per host thread and device).
+  // Workers for a transfer of total_bytes (crew, streams, events and pinned
+  // slots are kept across calls: the session is cached per host thread and device).
   bool init(size_t total_bytes) {
-    int T = Pool::get().size();
-    size_t nchunks = (total_bytes + kChunk - 1) / kChunk;
+    int T = crew_size();
+    size_t nchunks = (total_bytes + chunk_bytes() - 1) / chunk_bytes();
     if ((size_t)T > nchunks) T = (int)std::max<size_t>(1, nchunks);
+    if (!crew_) crew_.reset(new Crew(crew_size()));
+    if (!ready_ && cudaEventCreateWithFlags(&ready_, cudaEventDisableTiming) != cudaSuccess) return false;
     if ((int)w_.size() >= T) {
       active_ = T;
       return true;
@@ -190,8 +269,14 @@ class Session {
   static std::vector<Chunk> chunks(const std::vector<Span>& spans) {
     std::vector<Chunk> c;
     for (const auto& s : spans)
-      for (size_t off = 0; off < s.bytes; off += kChunk) c.push_back({&s, off, std::min(kChunk, s.bytes - off)});
+      for (size_t off = 0; off < s.bytes; off += chunk_bytes())
+        c.push_back({&s, off, std::min(chunk_bytes(), s.bytes - off)});
     return c;
+  }
+  static size_t total(const std::vector<Span>& spans) {
+    size_t b = 0;
+    for (const auto& s : spans) b += s.bytes;
+    return b;
   }
 
   // Queue host -> device copies of `spans`; `st` waits for them.
@@ -199,14 +284,19 @@ class Session {
     std::vector<Chunk> c = chunks(spans);
     std::atomic<int> bad{0};
     const int T = active_;
-    Pool::get().run(T, [&](int t) {
+    Stats stats;
+    stats.t0 = now_us();
+    const bool tr = trace_level() >= 2;
+    crew_->start(T, [&](int t) {
       cudaSetDevice(dev_);
       W& w = w_[t];
       int k = 0;
       for (size_t i = t; i < c.size(); i += T, ++k) {
         int b = k & 1;
         if (cudaEventSynchronize(w.ev[b]) != cudaSuccess) { bad = 1; return; }  // slot free again
-        memcpy(w.slot[b], c[i].s->host + c[i].off, c[i].len);
+        double a = tr ? now_us() : 0;
+        copy_fast(w.slot[b], c[i].s->host + c[i].off, c[i].len);
+        if (tr) stats.copy_ns += (long long)((now_us() - a) * 1e3);
         if (cudaMemcpyAsync(c[i].s->dev + c[i].off, w.slot[b], c[i].len, cudaMemcpyHostToDevice, w.st) != cudaSuccess ||
             cudaEventRecord(w.ev[b], w.st) != cudaSuccess) {
           bad = 1;
@@ -214,6 +304,8 @@ class Session {
         }
       }
     });
+    crew_->wait();
+    if (tr) stats.print("h2d host side", total(spans), T);
     if (bad) return false;
     for (int t = 0; t < T; ++t) {
       W& w = w_[t];
@@ -228,24 +320,25 @@ class Session {
   // buffers wait for `check()` (called once, on this thread) to return 0.
   int d2h(const std::vector<Span>& spans, cudaStream_t st, const std::function<int()>& check) {
     std::vector<Chunk> c = chunks(spans);
-    cudaEvent_t ready;
-    if (cudaEventCreateWithFlags(&ready, cudaEventDisableTiming) != cudaSuccess) return -1;
-    if (cudaEventRecord(ready, st) != cudaSuccess) { cudaEventDestroy(ready); return -1; }
-    std::mutex mu;
-    std::condition_variable cv;
-    int verdict = 1;  // 1 pending, 0 ok, else error
+    if (cudaEventRecord(ready_, st) != cudaSuccess) return -1;
+    std::atomic<int> verdict{1};  // 1 pending, 0 ok, else error
     std::atomic<int> bad{0};
     const int T = active_;
-    int rc_check = 0;
-    // the DMAs are issued by the pool; this thread decides whether they may land
+    Stats stats;
+    stats.t0 = now_us();
+    const bool tr = trace_level() >= 2;
+    // the DMAs are issued by the crew; this thread decides whether they may land
     auto work = [&](int t) {
       cudaSetDevice(dev_);
       W& w = w_[t];
-      if (cudaStreamWaitEvent(w.st, ready, 0) != cudaSuccess) { bad = 1; }
+      if (cudaStreamWaitEvent(w.st, ready_, 0) != cudaSuccess) bad = 1;
       auto wait_ok = [&]() {
-        std::unique_lock<std::mutex> lk(mu);
-        cv.wait(lk, [&] { return verdict != 1; });
-        return verdict == 0;
+        int v;
+        for (int spin = 0; (v = verdict.load(std::memory_order_acquire)) == 1; ++spin) {
+          if (spin < 4096) _mm_pause();
+          else std::this_thread::yield();
+        }
+        return v == 0;
       };
       std::vector<size_t> mine;
       for (size_t i = t; i < c.size(); i += T) mine.push_back(i);
@@ -254,7 +347,9 @@ class Session {
         if (cudaEventSynchronize(w.ev[b]) != cudaSuccess) { bad = 1; return; }
         if (!wait_ok() || bad) return;
         const Chunk& ch = c[mine[k]];
-        memcpy(ch.s->host + ch.off, w.slot[b], ch.len);
+        double a = tr ? now_us() : 0;
+        copy_fast(ch.s->host + ch.off, w.slot[b], ch.len);
+        if (tr) stats.copy_ns += (long long)((now_us() - a) * 1e3);
       };
       for (size_t k = 0; k < mine.size(); ++k) {
         int b = (int)(k & 1);
@@ -269,17 +364,12 @@ class Session {
       size_t m = mine.size();
       for (size_t k = m >= 2 ? m - 2 : 0; k < m; ++k) land(k);
     };
-    // the verdict comes from `check` on this thread while the pool copies
-    Pool::Batch batch;
-    Pool::get().start(batch, T, work);
-    rc_check = check();
-    {
-      std::lock_guard<std::mutex> lk(mu);
-      verdict = rc_check == 0 ? 0 : 2;
-    }
-    cv.notify_all();
-    batch.wait();
-    cudaEventDestroy(ready);
+    // the verdict comes from `check` on this thread while the crew copies
+    crew_->start(T, work);
+    int rc_check = check();
+    verdict.store(rc_check == 0 ? 0 : 2, std::memory_order_release);
+    crew_->wait();
+    if (tr) stats.print("d2h", total(spans), T);
     if (rc_check) return rc_check;
     return bad ? -1 : 0;
   }
@@ -294,6 +384,8 @@ class Session {
   int dev_;
   int active_ = 0;
   std::vector<W> w_;
+  std::unique_ptr<Crew> crew_;
+  cudaEvent_t ready_ = nullptr;
 };
 
 // The calling thread's session for `dev` (created on first use).

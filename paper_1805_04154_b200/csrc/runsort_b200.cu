@@ -708,17 +708,26 @@ void build_alpha(HostTree& H, const std::vector<int64_t>& starts, double alpha, 
   H.max_stack = hmax;
 }
 
-// Depths (root = 0) and the workspace arrays; uploads on `st`.
-int upload_tree(const HostTree& H, const WsView& V, const Layout& L, cudaStream_t st, bool write_leaves) {
+// Depths (root = 0) and the workspace arrays; uploads on `st`.  A forest is
+// allowed: every parentless node or leaf is a root at depth 0 (writes buf[0]).
+// Boundaries that are not nodes of this tree get an empty span and an
+// unfusable leaf range, which classification turns into a class-2 node with
+// zero tiles: no task, no merge cost, no comparisons.  `leaf_info` (r entries)
+// replaces the leaf table when given (write_leaves).
+int upload_tree(const HostTree& H, const WsView& V, const Layout& L, cudaStream_t st, bool write_leaves,
+                const std::vector<uint32_t>* leaf_info = nullptr) {
   int64_t r = H.r;
   std::vector<uint8_t> depth(r > 0 ? r : 1, 0), ldepth(r, 0);
   std::vector<int32_t> parent(L.leaf_base + r, -1);
   std::vector<pos_t> ns(r, 0), ne(r, 0);
+  std::vector<int32_t> na(H.na), nb(H.nb);
+  std::vector<uint8_t> is_node(r > 0 ? r : 1, 0);
   for (int64_t k = (int64_t)H.order.size() - 1; k >= 0; --k) {  // parents before children
     uint32_t j = H.order[k];
     int d = parent[j] < 0 ? 0 : depth[parent[j]] + 1;
     if (d > 63) return fail(RS_EUNSUPPORTED, "merge tree deeper than 63 levels");
     depth[j] = (uint8_t)d;
+    is_node[j] = 1;
     ns[j] = H.start[H.na[j]];
     ne[j] = H.start[H.nb[j] + 1];
     for (int side = 0; side < 2; ++side) {
@@ -727,20 +736,127 @@ int upload_tree(const HostTree& H, const WsView& V, const Layout& L, cudaStream_
       if (c >= H.leaf_base) ldepth[c - H.leaf_base] = (uint8_t)(d + 1);
     }
   }
+  for (int64_t j = 1; j < r; ++j)
+    if (!is_node[j]) {
+      na[j] = 0;
+      nb[j] = 0x3fffffff;  // more internal nodes than any fused subtree holds
+    }
   if (write_leaves) {
-    std::vector<uint32_t> info(r, 1u);  // natural run of length 1: insertion sort from one presorted element
+    std::vector<uint32_t> info1(leaf_info ? 0 : r, 1u);  // natural run of length 1: insertion sort from one presorted element
+    const std::vector<uint32_t>& info = leaf_info ? *leaf_info : info1;
     RS_CUDA(cudaMemcpyAsync(V.leaf_start, H.start.data(), (r + 1) * sizeof(pos_t), cudaMemcpyHostToDevice, st));
     RS_CUDA(cudaMemcpyAsync(V.leaf_info, info.data(), r * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
   }
   RS_CUDA(cudaMemcpyAsync(V.leaf_depth, ldepth.data(), r, cudaMemcpyHostToDevice, st));
   RS_CUDA(cudaMemcpyAsync(V.depth, depth.data(), r, cudaMemcpyHostToDevice, st));
-  RS_CUDA(cudaMemcpyAsync(V.node_a, H.na.data(), r * sizeof(int32_t), cudaMemcpyHostToDevice, st));
-  RS_CUDA(cudaMemcpyAsync(V.node_b, H.nb.data(), r * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  RS_CUDA(cudaMemcpyAsync(V.node_a, na.data(), r * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  RS_CUDA(cudaMemcpyAsync(V.node_b, nb.data(), r * sizeof(int32_t), cudaMemcpyHostToDevice, st));
   RS_CUDA(cudaMemcpyAsync(V.node_s, ns.data(), r * sizeof(pos_t), cudaMemcpyHostToDevice, st));
   RS_CUDA(cudaMemcpyAsync(V.node_e, ne.data(), r * sizeof(pos_t), cudaMemcpyHostToDevice, st));
   RS_CUDA(cudaMemcpyAsync(V.parent, parent.data(), parent.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st));
   RS_CUDA(cudaMemcpyAsync(V.child, H.child.data(), H.child.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
   RS_CUDA(cudaStreamSynchronize(st));  // the host vectors go out of scope
+  return RS_OK;
+}
+
+// Classification + ordered task list for the tree in the workspace, then the executor.
+template <typename K, int TB>
+int exec_tree(K* keys, void* tags, int64_t n, int w, int classic, int no_detect, int fixed, const WsView& V,
+              const Layout& L, int sms, cudaStream_t st) {
+  int msuper = merge_super<K, TB>(n, sms);
+  // top-down / bottom-up: no run detection term, merges counted at run time, no
+  // fused subtrees (their merges may be skipped); alpha sorts: powersort's accounting
+  ClassifyArgs CA = classify_args<K, TB>(V, L, n, w, classic, msuper, no_detect, fixed, fixed ? 0 : -1);
+  size_t sm = (size_t)kFillSmem + 64;
+  int occ;
+  if (int e = occupancy((const void*)k_tree_tasks, 256, sm, sm, &occ, "task-list kernel")) return e;
+  uint32_t* cd = V.chunkdep;
+  void* kargs[] = {&CA, &cd};
+  RS_CUDA(cudaLaunchCooperativeKernel((void*)k_tree_tasks, dim3(sms * occ), dim3(256), kargs, sm, st));
+  prof_mark(1, st);
+  return launch_exec<K, TB>(keys, tags, n, w, classic, msuper, V, L, sms, st, fixed);
+}
+
+// Alpha-stack / alpha-merge trees can be arbitrarily deep (increasing run
+// lengths chain every run into one left spine: depth = runs - 1), while the
+// executor orders its tasks in kMaxDepth depth buckets.  Such trees run in
+// passes over height bands: pass p merges the nodes of height in
+// (62(p-1), 62p], every maximal subtree of height <= 62p being a root of the
+// pass's forest, with the previous pass's subtrees -- sorted, in place in
+// buf[0] -- as its leaves (natural runs, no detection term).  Every node is
+// merged once with the same children as in one pass, so the output, the merge
+// cost and the comparisons are the single-pass ones.
+template <typename K, int TB>
+int run_deep_tree(const HostTree& H, K* keys, void* tags, int64_t n, int w, int classic, const WsView& V,
+                  const Layout& L, int sms, cudaStream_t st) {
+  const int64_t r = H.r;
+  const uint32_t lb = H.leaf_base;
+  std::vector<int32_t> h(r, 0), par(r, -1), lpar(r, -1);
+  auto height = [&](uint32_t id) { return id >= lb ? 0 : h[id]; };
+  for (uint32_t j : H.order) {
+    uint32_t c0 = H.child[2 * (size_t)j], c1 = H.child[2 * (size_t)j + 1];
+    h[j] = 1 + std::max(height(c0), height(c1));
+    for (uint32_t c : {c0, c1}) (c >= lb ? lpar[c - lb] : par[c]) = (int32_t)j;
+  }
+  const int32_t band = 62;
+  const int32_t hroot = H.order.empty() ? 0 : h[H.order.back()];
+  for (int32_t p = 1; (int64_t)band * (p - 1) < hroot; ++p) {
+    const int32_t W0 = band * (p - 1), W1 = band * p;
+    // units (this pass's leaves): maximal subtrees of height <= W0, by first leaf
+    std::vector<int32_t> first;
+    for (int64_t i = 0; i < r; ++i)
+      if (p == 1 || lpar[i] < 0 || h[lpar[i]] > W0) first.push_back((int32_t)i);
+    if (p > 1)
+      for (uint32_t j : H.order)
+        if (h[j] <= W0 && (par[j] < 0 || h[par[j]] > W0)) first.push_back(H.na[j]);
+    std::sort(first.begin(), first.end());
+    const int64_t R = (int64_t)first.size();
+    std::vector<int32_t> unit(r);
+    for (int64_t k = 0, i = 0; i < r; ++i) {
+      while (k + 1 < R && first[k + 1] <= i) ++k;
+      unit[i] = (int32_t)k;
+    }
+    HostTree P;
+    P.leaf_base = lb;
+    P.init(R, lb);
+    P.start.resize(R + 1);
+    std::vector<uint32_t> info(R);
+    for (int64_t k = 0; k < R; ++k) {
+      P.start[k] = H.start[first[k]];
+      int64_t len = (k + 1 < R ? H.start[first[k + 1]] : n) - P.start[k];
+      info[k] = (uint32_t)std::min<int64_t>(len, w);  // a natural run: no insertion sort
+    }
+    P.start[R] = n;
+    auto pid = [&](uint32_t id) -> uint32_t {
+      if (id >= lb) return lb + (uint32_t)unit[id - lb];
+      if (h[id] <= W0) return lb + (uint32_t)unit[H.na[id]];
+      return (uint32_t)unit[id];  // a node of this pass: the boundary at its right child's first leaf
+    };
+    for (uint32_t j : H.order)
+      if (h[j] > W0 && h[j] <= W1) {
+        uint32_t got = P.join(pid(H.child[2 * (size_t)j]), pid(H.child[2 * (size_t)j + 1]));
+        if (got != (uint32_t)unit[j]) return fail(RS_EINVARIANT, "deep-tree pass: node boundary mismatch");
+      }
+    if (p > 1) {  // keep the counters, reset the scheduling state
+      DevMetrics hm;
+      RS_CUDA(cudaMemcpyAsync(&hm, V.met, sizeof(DevMetrics), cudaMemcpyDeviceToHost, st));
+      RS_CUDA(cudaStreamSynchronize(st));
+      if (hm.error) return fail(RS_EINVARIANT, "device invariant failure");
+      DevMetrics z;
+      memset(&z, 0, sizeof z);
+      z.merge_cost = hm.merge_cost;
+      z.comparisons = hm.comparisons;
+      z.runs_detected = hm.runs_detected;
+      z.max_stack_height = hm.max_stack_height;
+      z.n_leaves = (unsigned long long)R;
+      RS_CUDA(cudaMemcpyAsync(V.met, &z, sizeof z, cudaMemcpyHostToDevice, st));
+      RS_CUDA(cudaMemsetAsync(V.done, 0, (2 * L.r_max + 2) * sizeof(uint32_t), st));
+      int64_t nch_max = (L.r_max + kOrdChunkMin - 1) / kOrdChunkMin;
+      RS_CUDA(cudaMemsetAsync(V.chunkdep, 0, (nch_max + 1) * kMaxDepth * sizeof(uint32_t), st));
+    }
+    if (int e = upload_tree(P, V, L, st, p > 1, &info)) return e;
+    if (int e = exec_tree<K, TB>(keys, tags, n, w, classic, p > 1 ? 1 : 0, 0, V, L, sms, st)) return e;
+  }
   return RS_OK;
 }
 
@@ -778,22 +894,19 @@ int run_baseline(int algo, K* keys, void* tags, int64_t n, int w, int classic, d
     RS_CUDA(cudaStreamSynchronize(st));
     build_alpha(H, starts, alpha, algo == RS_ALGO_ALPHA_MERGE);
     RS_CUDA(cudaMemcpyAsync(&V.met->max_stack_height, &H.max_stack, 8, cudaMemcpyHostToDevice, st));
+    int deepest = 0;
+    {
+      std::vector<int32_t> hh(H.r > 0 ? H.r : 1, 0);
+      for (uint32_t j : H.order) {
+        uint32_t c0 = H.child[2 * (size_t)j], c1 = H.child[2 * (size_t)j + 1];
+        hh[j] = 1 + std::max(c0 >= H.leaf_base ? 0 : hh[c0], c1 >= H.leaf_base ? 0 : hh[c1]);
+      }
+      if (!H.order.empty()) deepest = hh[H.order.back()] - 1;  // depth of the deepest node
+    }
+    if (deepest > 63) return run_deep_tree<K, TB>(H, keys, tags, n, w, classic, V, L, sms, st);
     if (int e = upload_tree(H, V, L, st, false)) return e;
   }
-  int msuper = merge_super<K, TB>(n, sms);
-  // top-down / bottom-up: no run detection term, merges counted at run time, no
-  // fused subtrees (their merges may be skipped); alpha sorts: powersort's accounting
-  ClassifyArgs CA = classify_args<K, TB>(V, L, n, w, classic, msuper, fixed ? 1 : 0, fixed ? 1 : 0, fixed ? 0 : -1);
-  int64_t nch_max = (L.r_max + kOrdChunkMin - 1) / kOrdChunkMin;
-  (void)nch_max;
-  size_t sm = (size_t)kFillSmem + 64;
-  int occ;
-  if (int e = occupancy((const void*)k_tree_tasks, 256, sm, sm, &occ, "task-list kernel")) return e;
-  uint32_t* cd = V.chunkdep;
-  void* kargs[] = {&CA, &cd};
-  RS_CUDA(cudaLaunchCooperativeKernel((void*)k_tree_tasks, dim3(sms * occ), dim3(256), kargs, sm, st));
-  prof_mark(1, st);
-  return launch_exec<K, TB>(keys, tags, n, w, classic, msuper, V, L, sms, st, fixed ? 1 : 0);
+  return exec_tree<K, TB>(keys, tags, n, w, classic, fixed ? 1 : 0, fixed ? 1 : 0, V, L, sms, st);
 }
 
 template <typename K, int TB>
