@@ -72,6 +72,7 @@ struct DevMetrics {
   unsigned long long cursorA;     // phase-A slot allocator
   unsigned long long max_depth;   // deepest internal node
   unsigned long long n_merge_tasks;
+  unsigned long long n_jobs;      // small-tree path: job-list entries (rs_small.cuh)
   unsigned long long merge_cost_exec;  // sum of spans of the nodes merged by the merge executor
   unsigned long long depth_tiles[kMaxDepth];
   unsigned long long depth_base[kMaxDepth];

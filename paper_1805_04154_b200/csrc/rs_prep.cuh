@@ -33,6 +33,7 @@ struct PrepArgs {
   int64_t done_words;
   TreeArrays T;
   ClassifyArgs CA;
+  SmallJobs jobs;   // small-tree path: job list (rs_small.cuh)
   int leaves_only;  // stop after the leaf phase (alpha-stack sorts build their tree on the host)
 };
 
@@ -95,10 +96,15 @@ __global__ void __launch_bounds__(256, 3) k_prep(PrepArgs P) {
   RS_TS(met, 4);
   if (P.leaves_only) return;
   // small trees: phases 5-9 in block 0 alone, out of shared memory (rs_small.cuh)
-  if ((int64_t)met->n_leaves <= kSmallR) {
+  // small trees (n < 2^31): phases 5-8 in block 0 out of shared memory, then
+  // the whole grid writes the task records (rs_small.cuh)
+  if ((int64_t)met->n_leaves <= kSmallR && P.F == 32) {
     extern __shared__ __align__(16) unsigned char smem_prep[];
-    pdl_trigger();
-    if (blockIdx.x == 0) small_tree<256>(P.T, P.CA, P.F, smem_prep);
+    if (blockIdx.x == 0) small_tree<256>(P.T, P.CA, smem_prep, P.jobs);
+    grid.sync();
+    RS_TS(met, 10);
+    pdl_trigger();  // k_phaseA may start launching (it waits for this grid)
+    small_fill(P.CA, P.jobs, smem_prep);
     return;
   }
   // 5. node powers + ancestor-count scan (chunk aggregates); each direction's last chunk scans them

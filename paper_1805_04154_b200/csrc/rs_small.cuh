@@ -1,14 +1,20 @@
 // rs_small.cuh -- the tree half of the prep (node powers, ancestor scans, trie
 // ranges, classification, ordered task list) for trees of at most kSmallR
-// leaves, in ONE 1024-thread CTA working out of shared memory.
+// leaves (n < 2^31): the tree in ONE CTA working out of shared memory, the
+// task records written by the whole grid.
 //
 // Same outputs as k_prep's phases 5-9 (rs_tree.cuh, rs_exec.cuh: d_scan_reduce,
 // d_scan_down, d_tree, d_classify, d_task_offsets/d_order_scan, d_task_fill),
 // with the merge tasks in the identical (depth desc, position) order.  With few
 // leaves those phases are pure latency: each is a chain of L2 round trips plus
 // a grid barrier over hundreds of mostly idle CTAs.  Here the chains run at
-// shared-memory latency behind __syncthreads.  k_prep runs this in block 0
-// (the other blocks exit) when n_leaves <= kSmallR.
+// shared-memory latency behind __syncthreads (block 0, small_tree), which
+// leaves a compact job list -- {first task slot, id, task count | kind} per
+// phase-A item and per merge node, merge jobs with their node's 48-byte
+// descriptor -- and after one grid barrier every thread of the grid writes
+// task records (small_fill: one task per thread, its job found by a binary
+// search over the job slots staged in shared memory).  A single CTA writing
+// the records (16K merge tasks on config 2) was the old bottleneck.
 #pragma once
 #include "rs_exec.cuh"
 #include "rs_tree.cuh"
@@ -22,39 +28,91 @@ namespace rs {
 #define RS_SMALL_UNROLL_N 1
 #endif
 constexpr int kSmallUnroll = RS_SMALL_UNROLL_N;
-constexpr int kSmallR = 2048;  // above this the grid-wide phases of k_prep are faster
+#ifndef RS_SMALL_R
+#define RS_SMALL_R 2048
+#endif
+constexpr int kSmallR = RS_SMALL_R;  // above this the grid-wide phases of k_prep are faster
+constexpr int kJobCap = 2 * kSmallR + 2;  // <= one job per leaf and one per boundary
 
+// 32-bit shared-memory arrays (positions and midpoint keys fit: n < 2^31, F = 32)
 __host__ __device__ constexpr size_t small_arrays_bytes() {
-  return (size_t)(kSmallR + 1) * 8      // Ls: leaf starts
-         + (size_t)kSmallR * 8          // Ks: midpoint keys, later node spans
-         + (size_t)2 * kSmallR * 4      // par: parents of leaves [0, r) and nodes [r, 2r)
+  return (size_t)(kSmallR + 1) * 4      // Ls: leaf starts
+         + (size_t)kSmallR * 4          // Ks: midpoint keys, later node spans | no-fuse bit 31
+         + (size_t)2 * kSmallR * 2      // par: parents of leaves [0, r) and nodes [r, 2r)
          + (size_t)(kSmallR + 1) * 5;   // Ps, las, ras, dep, ldep
 }
-constexpr size_t kSmallMdOff = (small_arrays_bytes() + 15) / 16 * 16;  // + one round of merge descriptors
-__host__ __device__ constexpr size_t small_smem_bytes() { return kSmallMdOff + 256 * 48; }
+__host__ __device__ constexpr size_t small_smem_bytes() {
+  return small_arrays_bytes() > (size_t)kJobCap * 4 ? small_arrays_bytes() : (size_t)kJobCap * 4;
+}
+// Global job list (workspace): slots, ids, counts | kind << 30, and the merge
+// descriptors indexed by node id (a merge job's id).
+__host__ __device__ constexpr size_t small_jobs_bytes() { return (size_t)kJobCap * (12 + sizeof(MDesc)) + 64; }
+struct SmallJobs {
+  uint32_t* slot;
+  uint32_t* id;
+  uint32_t* cnt;
+  MDesc* md;
+  __host__ __device__ static SmallJobs at(unsigned char* base) {
+    SmallJobs J;
+    J.md = reinterpret_cast<MDesc*>(base);  // 16-byte aligned first
+    J.slot = reinterpret_cast<uint32_t*>(base + (size_t)kJobCap * sizeof(MDesc));
+    J.id = J.slot + kJobCap;
+    J.cnt = J.id + kJobCap;
+    return J;
+  }
+};
+
+__device__ __forceinline__ unsigned long long block_excl_scan_u64(unsigned long long v, unsigned long long* smem,
+                                                                  unsigned long long* total) {
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  unsigned long long x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  __syncthreads();
+  if (lane == 31) smem[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    unsigned long long s = lane < nw ? smem[lane] : 0, t = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      unsigned long long y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
+    }
+    if (lane < nw) smem[lane] = t - s;
+    if (lane == 31) smem[32] = t;
+  }
+  __syncthreads();
+  unsigned long long r = smem[wid] + x - v;
+  *total = smem[32];
+  __syncthreads();
+  return r;
+}
 
 // Run by one CTA of NT threads (block 0 of k_prep after its leaf phase);
-// smem_small: small_smem_bytes() of dynamic shared memory.
+// smem_small: small_smem_bytes() of dynamic shared memory.  Requires n < 2^31.
 template <int NT>
-__device__ void small_tree(const TreeArrays& T, ClassifyArgs A, int F, unsigned char* smem_small) {
+__device__ void small_tree(const TreeArrays& T, ClassifyArgs A, unsigned char* smem_small, SmallJobs J) {
   constexpr int kSmallPer = (kSmallR + NT - 1) / NT;  // items per thread
+  constexpr int F = 32;
   DevMetrics* met = A.met;
   const int64_t r = (int64_t)met->n_leaves;
   if (r > kSmallR || r < 1) return;
   set_fuse_policy(A, r);
   RS_TS(met, 5);
-  pos_t* Ls = reinterpret_cast<pos_t*>(smem_small);
-  uint64_t* Ks = reinterpret_cast<uint64_t*>(Ls + kSmallR + 1);
-  pos_t* spans = reinterpret_cast<pos_t*>(Ks);  // after the trie ranges
-  int32_t* par = reinterpret_cast<int32_t*>(Ks + kSmallR);
+  uint32_t* Ls = reinterpret_cast<uint32_t*>(smem_small);
+  uint32_t* Ks = Ls + kSmallR + 1;
+  uint32_t* spans = Ks;  // after the trie ranges: span | kNoFuse (bit 31)
+  int16_t* par = reinterpret_cast<int16_t*>(Ks + kSmallR);
   uint8_t* Ps = reinterpret_cast<uint8_t*>(par + 2 * kSmallR);
   uint8_t* las = Ps + kSmallR + 1;
   uint8_t* ras = las + kSmallR + 1;
   uint8_t* dep = ras + kSmallR + 1;
   uint8_t* ldep = dep + kSmallR + 1;
   __shared__ MC smc[33];
-  __shared__ unsigned long long sred[32];
-  __shared__ uint32_t sscan[40];
+  __shared__ unsigned long long sred[33];
   __shared__ unsigned s_maxd;
 
   const int tid = threadIdx.x, nt = blockDim.x;
@@ -65,18 +123,18 @@ __device__ void small_tree(const TreeArrays& T, ClassifyArgs A, int F, unsigned 
   uint8_t* lag = const_cast<uint8_t*>(T.la);
   uint8_t* rag = const_cast<uint8_t*>(T.ra);
 
-  for (int64_t i = tid; i <= r; i += nt) Ls[i] = T.leaf_start[i];
+  for (int64_t i = tid; i <= r; i += nt) Ls[i] = (uint32_t)T.leaf_start[i];
   if (tid == 0) s_maxd = 0;
   __syncthreads();
   // ---- keys and powers (sorters.py:414-423 via the midpoint-key closed form)
   for (int64_t i = tid; i < r; i += nt) {
     uint64_t k = mid_key(Ls[i], Ls[i + 1], n, F);
-    Ks[i] = k;
+    Ks[i] = (uint32_t)k;
     Kg[i] = k;
   }
   __syncthreads();
   for (int64_t j = 1 + tid; j < r; j += nt) {
-    int p = F + 1 - bitlen64(Ks[j - 1] ^ Ks[j]);
+    int p = F + 1 - bitlen64((uint64_t)(Ks[j - 1] ^ Ks[j]));
     Ps[j] = (uint8_t)p;
     Pg[j] = (uint8_t)p;
   }
@@ -124,7 +182,7 @@ __device__ void small_tree(const TreeArrays& T, ClassifyArgs A, int F, unsigned 
   }
   RS_TS(met, 6);
   // ---- trie ranges, parents, children, spans (d_tree)
-  pos_t myspan[kSmallPer];
+  uint32_t myspan[kSmallPer];
 #pragma unroll kSmallUnroll
   for (int q = 0; q < kSmallPer; ++q) {
     int64_t i = tid + (int64_t)q * nt;
@@ -140,7 +198,7 @@ __device__ void small_tree(const TreeArrays& T, ClassifyArgs A, int F, unsigned 
       else if (hasR) { p = i + 1; side = 0; }
       uint32_t lid = T.leaf_base + (uint32_t)i;
       T.parent[lid] = (int32_t)p;
-      par[i] = (int32_t)p;
+      par[i] = (int16_t)p;
       uint8_t ld = 0;
       if (p >= 0) {
         T.child[2 * p + side] = lid;
@@ -157,11 +215,11 @@ __device__ void small_tree(const TreeArrays& T, ClassifyArgs A, int F, unsigned 
       uint64_t pre = sh >= 64 ? 0 : (kj >> sh);
       uint64_t lo_key = sh >= 64 ? 0 : (pre << sh);
       int64_t hi = j - 1, step = 1, x = j - 1 - step;
-      while (x >= 0 && Ks[x] >= lo_key) { hi = x; step <<= 1; x = j - 1 - step; }
+      while (x >= 0 && (uint64_t)Ks[x] >= lo_key) { hi = x; step <<= 1; x = j - 1 - step; }
       int64_t lo = x < 0 ? 0 : x + 1;
       while (lo < hi) {
         int64_t md = lo + (hi - lo) / 2;
-        if (Ks[md] >= lo_key) hi = md; else lo = md + 1;
+        if ((uint64_t)Ks[md] >= lo_key) hi = md; else lo = md + 1;
       }
       int64_t a = lo, b;
       if (sh >= 64) b = r - 1;
@@ -170,11 +228,11 @@ __device__ void small_tree(const TreeArrays& T, ClassifyArgs A, int F, unsigned 
         int64_t lo2 = j;
         step = 1;
         x = j + step;
-        while (x <= r - 1 && Ks[x] < hi_key) { lo2 = x; step <<= 1; x = j + step; }
+        while (x <= r - 1 && (uint64_t)Ks[x] < hi_key) { lo2 = x; step <<= 1; x = j + step; }
         int64_t hi2 = x > r - 1 ? r - 1 : x - 1;
         while (lo2 < hi2) {
           int64_t md = lo2 + (hi2 - lo2 + 1) / 2;
-          if (Ks[md] < hi_key) lo2 = md; else hi2 = md - 1;
+          if ((uint64_t)Ks[md] < hi_key) lo2 = md; else hi2 = md - 1;
         }
         b = lo2;
       }
@@ -183,8 +241,8 @@ __device__ void small_tree(const TreeArrays& T, ClassifyArgs A, int F, unsigned 
       pos_t s0 = Ls[a], e0 = Ls[b + 1];
       T.node_s[j] = s0;
       T.node_e[j] = e0;
-      // bit 62: not fusable (fusable_span: node table, average leaf length)
-      myspan[q] = (e0 - s0) | (fusable_span(A, e0 - s0, b - a) ? (pos_t)0 : ((pos_t)1 << 62));
+      // bit 31: not fusable (fusable_span: node table, average leaf length)
+      myspan[q] = (uint32_t)(e0 - s0) | (fusable_span(A, e0 - s0, b - a) ? 0u : 0x80000000u);
       uint8_t dd = (uint8_t)(las[j] + ras[j]);
       T.depth[j] = dd;
       dep[j] = dd;
@@ -196,7 +254,7 @@ __device__ void small_tree(const TreeArrays& T, ClassifyArgs A, int F, unsigned 
       } else if (hasL) { pp = a; side = 1; }
       else if (hasR) { pp = b + 1; side = 0; }
       T.parent[j] = (int32_t)pp;
-      par[r + j] = (int32_t)pp;
+      par[r + j] = (int16_t)pp;
       if (pp >= 0) T.child[2 * pp + side] = (uint32_t)j;
     }
   }
@@ -211,15 +269,14 @@ __device__ void small_tree(const TreeArrays& T, ClassifyArgs A, int F, unsigned 
   // ---- classification (d_classify), contiguous items per thread
   const int64_t per = (r + nt - 1) / nt;
   const int64_t i0 = (int64_t)tid * per;
-  constexpr pos_t kNoFuse = (pos_t)1 << 62;
-  auto fusable_s = [&](int64_t j) { return spans[j] <= A.fcap; };  // kNoFuse set -> > fcap
+  constexpr uint32_t kNoFuse = 0x80000000u;
+  auto fusable_s = [&](int64_t j) { return (pos_t)spans[j] <= (pos_t)A.fcap; };  // kNoFuse set -> > fcap
   auto parent_small_s = [&](int32_t p) { return p >= 0 && fusable_s(p); };
   unsigned long long comps = 0, mcost = 0, mbig = 0;
-  uint32_t cntA = 0;
-  unsigned maxd = 0;
   uint32_t tk_of[kSmallPer];   // merge tasks of node i0+q (0 unless big)
   uint32_t a_of[kSmallPer];    // phase-A tasks of item i0+q
   uint8_t lcls[kSmallPer], ncls[kSmallPer];
+  unsigned maxd = 0;
 #pragma unroll kSmallUnroll
   for (int q = 0; q < kSmallPer; ++q) {
     int64_t i = i0 + q;
@@ -228,7 +285,7 @@ __device__ void small_tree(const TreeArrays& T, ClassifyArgs A, int F, unsigned 
     lcls[q] = 0;
     ncls[q] = 0;
     if (q >= per || i >= r) continue;
-    pos_t s0 = Ls[i], len = Ls[i + 1] - s0;
+    pos_t s0 = Ls[i], len = (pos_t)Ls[i + 1] - s0;
     uint32_t info = A.leaf_info[i];
     uint32_t nl = info & 0x7fffffffu;
     if (!A.peek && s0 < n - 1) {
@@ -254,7 +311,7 @@ __device__ void small_tree(const TreeArrays& T, ClassifyArgs A, int F, unsigned 
     a_of[q] = c == 1 ? 1u : (uint32_t)tl;
     if (i >= 1) {
       bool fz = fusable_s(i);
-      pos_t span = spans[i] & (kNoFuse - 1);
+      pos_t span = (pos_t)(spans[i] & ~kNoFuse);
       mcost += span;
       if (!A.classic) comps += span;  // runcore.py:299-301
       int cn;
@@ -273,7 +330,6 @@ __device__ void small_tree(const TreeArrays& T, ClassifyArgs A, int F, unsigned 
         maxd = dep[i] > maxd ? dep[i] : maxd;
       } else A.need[i] = 0;
     }
-    cntA += a_of[q];
   }
   unsigned long long sc = block_sum(comps, sred);
   if (tid == 0) met->comparisons += sc;
@@ -284,103 +340,114 @@ __device__ void small_tree(const TreeArrays& T, ClassifyArgs A, int F, unsigned 
   maxd = warp_max(maxd);
   if ((tid & 31) == 0 && maxd) atomicMax(&s_maxd, maxd);
   RS_TS(met, 8);
-  // ---- task records.  Slots come from block scans; the records are written
-  // from a job list {first slot, id, count | kind << 30} (in the dead Ks / par
-  // regions) by whole warps, so a node with many tiles is not written by one thread.
-  __syncthreads();  // classification reads of spans / par are over
-  uint32_t* jslot = reinterpret_cast<uint32_t*>(Ks);
-  uint32_t* jid = jslot + kSmallR;
-  uint32_t* jcnt = reinterpret_cast<uint32_t*>(par);
-  __shared__ uint32_t s_nj;
-  const int wid = tid >> 5, lane = tid & 31, nw = nt >> 5;
-  auto push = [&](uint32_t slot, uint32_t id, uint32_t cnt, uint32_t kind) {
-    uint32_t e = atomicAdd(&s_nj, 1u);
-    jslot[e] = slot;
-    jid[e] = id;
-    jcnt[e] = cnt | (kind << 30);
-  };
-  uint32_t s_mbase = 0;  // first merge-task slot (set once the phase-A count is known)
-  auto drain = [&]() {
-    __syncthreads();
-    uint32_t nj = s_nj;
-    MDesc* s_md = reinterpret_cast<MDesc*>(smem_small + kSmallMdOff);
-    for (uint32_t g = 0; g < nj; g += nt) {
-      // merge descriptors of this round's jobs: one thread per job, parallel round trips
-      uint32_t e = g + tid;
-      if (e < nj && (jcnt[e] >> 30) == kTaskMerge) s_md[tid] = load_mdesc(A, jid[e]);
-      __syncthreads();
-      uint32_t ny = nj - g < (uint32_t)nt ? nj - g : (uint32_t)nt;
-      for (uint32_t y = wid; y < ny; y += nw) {
-        uint32_t slot = jslot[g + y], id = jid[g + y], c = jcnt[g + y];
-        uint32_t kind = c >> 30, cnt = c & 0x3fffffffu;
-        if (kind == kTaskMerge) {
-          const MDesc md = s_md[y];
-          for (uint32_t k = lane; k < cnt; k += 32) store_merge_task(A, slot + k, s_mbase, md, k);
-        } else {
-          for (uint32_t k = lane; k < cnt; k += 32) A.tasks[slot + k] = make_task(kind, kind == kTaskFuse ? 0 : k, id);
-        }
-      }
-      __syncthreads();
-    }
-    __syncthreads();
-    if (tid == 0) s_nj = 0;
-    __syncthreads();
-  };
-  if (tid == 0) s_nj = 0;
-  // phase-A tasks (any order; here by position)
-  uint32_t totA;
-  uint32_t slotA = block_excl_scan_u32(cntA, sscan, &totA);
-  s_mbase = totA;  // first merge-task slot
+  __syncthreads();  // A.need / A.cls / T.child of every item written (descriptors read them)
+  // ---- job list: phase-A jobs by position, then merge jobs by (depth desc, position).
+  // Each job's first task slot and its own index come from one packed scan
+  // (jobs << 32 | tasks); merge jobs carry their node's descriptor.
+  unsigned long long vA = 0;
 #pragma unroll kSmallUnroll
   for (int q = 0; q < kSmallPer; ++q) {
-    int64_t i = i0 + q;
-    if (q >= per || i >= r) continue;
-    uint32_t lid = A.leaf_base + (uint32_t)i;
-    if (lcls[q] == 1) push(slotA++, lid, 1u, kTaskFuse);
-    else if (lcls[q] == 2) {
-      uint32_t tl = a_of[q] - (ncls[q] == 1 ? 1u : 0u);
-      push(slotA, lid, tl, kTaskLeaf);
-      slotA += tl;
-    }
-    if (ncls[q] == 1) push(slotA++, (uint32_t)i, 1u, kTaskFuse);
+    if (q >= per || i0 + q >= r) continue;
+    uint32_t tl = a_of[q] - (ncls[q] == 1 ? 1u : 0u);  // the leaf's own tasks
+    uint32_t jobs = (lcls[q] == 1 || (lcls[q] == 2 && tl > 0) ? 1u : 0u) + (ncls[q] == 1 ? 1u : 0u);
+    vA += ((unsigned long long)jobs << 32) | a_of[q];
   }
-  drain();
-  // merge tasks: depth desc, then position (d_task_offsets + d_task_fill)
-  const int dmax = (int)s_maxd;
+  unsigned long long totv;
+  unsigned long long ex = block_excl_scan_u64(vA, sred, &totv);
+  const uint32_t totA = (uint32_t)totv;
+  {
+    uint32_t slot = (uint32_t)ex, jb = (uint32_t)(ex >> 32);
+#pragma unroll kSmallUnroll
+    for (int q = 0; q < kSmallPer; ++q) {
+      int64_t i = i0 + q;
+      if (q >= per || i >= r) continue;
+      uint32_t lid = A.leaf_base + (uint32_t)i;
+      uint32_t tl = a_of[q] - (ncls[q] == 1 ? 1u : 0u);
+      if (lcls[q] == 1 || (lcls[q] == 2 && tl > 0)) {
+        uint32_t kind = lcls[q] == 1 ? (uint32_t)kTaskFuse : (uint32_t)kTaskLeaf;
+        J.slot[jb] = slot;
+        J.id[jb] = lid;
+        J.cnt[jb] = tl | (kind << 30);
+        ++jb;
+        slot += tl;
+      }
+      if (ncls[q] == 1) {
+        J.slot[jb] = slot;
+        J.id[jb] = (uint32_t)i;
+        J.cnt[jb] = 1u | ((uint32_t)kTaskFuse << 30);
+        ++jb;
+        slot += 1;
+      }
+    }
+  }
+  // merge descriptors, node-indexed, all at once: one strided pass of
+  // independent round trips instead of one dependent chain per depth
+  for (int64_t i = 1 + tid; i < r; i += nt)
+    if (A.cls[i] == 2) J.md[i] = load_mdesc(A, (uint32_t)i);
+  uint32_t jbase = (uint32_t)(totv >> 32);
   uint64_t base = totA;
+  const int dmax = (int)s_maxd;
   for (int d = dmax; d >= 0; --d) {
-    uint32_t mine = 0;
+    unsigned long long v = 0;
 #pragma unroll kSmallUnroll
     for (int q = 0; q < kSmallPer; ++q)
-      if (q < per && i0 + q < r && ncls[q] == 2 && dep[i0 + q] == d) mine += tk_of[q];
-    uint32_t tot;
-    uint32_t slot = block_excl_scan_u32(mine, sscan, &tot);
+      if (q < per && i0 + q < r && ncls[q] == 2 && dep[i0 + q] == d) v += (1ull << 32) | tk_of[q];
+    unsigned long long tot;
+    unsigned long long e = block_excl_scan_u64(v, sred, &tot);
     if (tid == 0) {
-      met->depth_tiles[d] = tot;
+      met->depth_tiles[d] = (uint32_t)tot;
       met->depth_base[d] = base;
       met->depth_cursor[d] = base;
     }
-    slot += (uint32_t)base;
+    uint32_t slot = (uint32_t)(base + (uint32_t)e), jb = jbase + (uint32_t)(e >> 32);
 #pragma unroll kSmallUnroll
     for (int q = 0; q < kSmallPer; ++q) {
       int64_t i = i0 + q;
       if (q < per && i < r && ncls[q] == 2 && dep[i] == d) {
-        push(slot, (uint32_t)i, tk_of[q], kTaskMerge);
+        J.slot[jb] = slot;
+        J.id[jb] = (uint32_t)i;
+        J.cnt[jb] = tk_of[q] | ((uint32_t)kTaskMerge << 30);
+        ++jb;
         slot += tk_of[q];
       }
     }
-    base += tot;
+    base += (uint32_t)tot;
+    jbase += (uint32_t)(tot >> 32);
   }
-  drain();
   if (tid == 0) {
     met->phaseA = totA;
     met->max_depth = (unsigned long long)dmax;
     met->n_tasks = base;
+    met->n_jobs = jbase;
     met->cursorA = totA;
     met->task_ctr = totA;
     met->task_ctr_A = 0;
   }
   RS_TS(met, 9);
+}
+
+// All blocks, after the grid barrier that follows small_tree: one task per
+// thread, grid-stride; the job is the last one whose first slot is <= the task.
+__device__ void small_fill(const ClassifyArgs& A, SmallJobs J, unsigned char* smem_small) {
+  const DevMetrics* met = A.met;
+  const uint32_t nj = (uint32_t)met->n_jobs;
+  const unsigned long long ntask = met->n_tasks;
+  const uint32_t mbase = (uint32_t)met->phaseA;
+  uint32_t* sslot = reinterpret_cast<uint32_t*>(smem_small);
+  copy_g2s(sslot, J.slot, (int)nj, threadIdx.x, blockDim.x);
+  __syncthreads();
+  for (unsigned long long q = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; q < ntask;
+       q += (unsigned long long)gridDim.x * blockDim.x) {
+    uint32_t lo = 0, hi = nj - 1;  // last job k with sslot[k] <= q
+    while (lo < hi) {
+      uint32_t md = (lo + hi + 1) >> 1;
+      if (sslot[md] <= (uint32_t)q) lo = md; else hi = md - 1;
+    }
+    const uint32_t c = J.cnt[lo], id = J.id[lo];
+    const uint32_t kind = c >> 30, k = (uint32_t)q - sslot[lo];
+    if (kind == kTaskMerge) store_merge_task(A, (uint32_t)q, mbase, J.md[id], k);
+    else A.tasks[q] = make_task(kind, kind == kTaskFuse ? 0u : k, id);
+  }
 }
 
 }  // namespace rs

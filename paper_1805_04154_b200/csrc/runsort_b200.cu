@@ -160,7 +160,7 @@ struct Layout {
   size_t o_key1, o_tag1, o_key2, o_tag2, o_ascw, o_tables, o_gtab, o_gentry, o_goff, o_tentry, o_toff;
   size_t o_leaf_start, o_leaf_info, o_leaf_depth, o_K, o_P, o_la, o_ra, o_depth;
   size_t o_node_a, o_node_b, o_node_s, o_node_e, o_parent, o_child, o_need, o_done;
-  size_t o_agg, o_tasks, o_mdesc, o_chunkdep, o_cls, o_met, total;
+  size_t o_agg, o_tasks, o_mdesc, o_chunkdep, o_cls, o_jobs, o_met, total;
   int64_t mdesc_cap;  // merge-task descriptors (indexed from the first merge task)
   // peeksort replay
   int algo;
@@ -245,6 +245,7 @@ Layout make_layout(int64_t n, int w, int kb, int tb, int algo) {
   L.o_mdesc = take((size_t)L.mdesc_cap * sizeof(MDesc));
   L.o_chunkdep = take((size_t)((L.r_max + kOrdChunkMin - 1) / kOrdChunkMin + 1) * kMaxDepth * 4);
   L.o_cls = take((size_t)(2 * L.r_max + 2));
+  L.o_jobs = take(small_jobs_bytes());
   if (pk) {
     L.front_cap = n + 1;
     L.rec_cap = n + 1;
@@ -396,6 +397,7 @@ struct WsView {
   void* tag1;
   void* key2;
   void* tag2;
+  unsigned char* jobs;
 };
 
 WsView view(unsigned char* ws, const Layout& L) {
@@ -430,6 +432,7 @@ WsView view(unsigned char* ws, const Layout& L) {
   V.mdesc = reinterpret_cast<MDesc*>(at(L.o_mdesc));
   V.chunkdep = reinterpret_cast<uint32_t*>(at(L.o_chunkdep));
   V.cls = reinterpret_cast<uint8_t*>(at(L.o_cls));
+  V.jobs = at(L.o_jobs);
   V.key1 = at(L.o_key1);
   V.tag1 = at(L.o_tag1);
   V.key2 = at(L.o_key2);
@@ -577,6 +580,7 @@ int run_powersort(K* keys, void* tags, int64_t n, int w, int classic, unsigned c
   PA.leaves_only = leaves_only;
   int msuper = merge_super<K, TB>(n, sms);
   PA.CA = classify_args<K, TB>(V, L, n, w, classic, msuper, 0);
+  PA.jobs = SmallJobs::at(V.jobs);
   int grid_p;
   void* kprep = ct == 1024 ? (void*)k_prep<K, 1024> : ct == 2560 ? (void*)k_prep<K, 2560> : (void*)k_prep<K, 2048>;
   if (int e = (ct == 1024   ? prep_grid<K, 1024>(sms, sm, &grid_p)
