@@ -31,6 +31,7 @@
 //              with the windows refilled by cp.async one step ahead.
 #pragma once
 #include "rs_common.cuh"
+#include "rs_exec.cuh"
 
 namespace rs {
 
@@ -242,36 +243,29 @@ __global__ void __launch_bounds__(256) k_kway_pivots(KwayShards S, int64_t spaci
   }
 }
 
+// k_kway_merge: persistent CTAs claim work items (the intervals between
+// consecutive pivots in global order: at most `spacing` elements of each
+// shard, so at most ITEM in all).  An item's W windows arrive in shared memory
+// by 1D bulk copies (TMA, local or peer memory alike) while the previous item
+// is merged: a pairwise merge tree inside shared memory, every level's
+// outputs split evenly over the CTA's threads by merge-path searches (ties to
+// the lower shard at every level => the (key, shard, position) order), keys
+// and tags moved together; the last level lands in shared memory and the CTA
+// writes it out with coalesced stores.
 template <typename K, int TB>
 struct KwayCfg {
-  static constexpr int THREADS = 512;
+  static constexpr int THREADS = 256;
   static constexpr int kb = sizeof(K);
-  // outputs per step: windows hold 2K elements per shard (K in use, K in flight)
-  static constexpr int KS = (kb + TB) <= 8 ? 1024 : 512;
-  static constexpr int WIN = 2 * KS;
-  // level entries: key + 16-bit window slot (shard * WIN + index)
-  __host__ __device__ static constexpr size_t win_bytes(int wp) { return (size_t)wp * WIN * (kb + TB); }
-  __host__ __device__ static constexpr size_t lvl_bytes(int wp) {
-    return (size_t)((wp / 2 > 1 ? wp / 2 : 1) + (wp / 4 > 1 ? wp / 4 : 1)) * KS * (kb + 2);
-  }
-  __host__ __device__ static constexpr size_t smem(int wp) { return win_bytes(wp) + lvl_bytes(wp) + 256; }
+  static constexpr int eb = kb + TB;
+  static constexpr int ITEM = eb <= 4 ? 8192 : (eb <= 8 ? 4096 : (eb <= 12 ? 2688 : 2048));  // elements per item
+  static constexpr int PAD = 16 * kKwayMaxW;  // per-window 16-byte phase slack (elements)
+  static constexpr int CAP = ITEM + PAD;
+  static constexpr size_t KBUF = ((size_t)CAP * kb + 127) / 128 * 128;
+  static constexpr size_t TBUF = TB ? ((size_t)CAP * (TB ? TB : 1) + 127) / 128 * 128 : 0;
+  static constexpr size_t BUF = KBUF + TBUF;
+  static constexpr size_t SMEM = 3 * BUF + 256;  // two load buffers + one merge buffer
+  static int64_t spacing(int w) { return ITEM / (w > 0 ? w : 1); }
 };
-
-__device__ __forceinline__ void cp_async4(void* s, const void* g) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(s)), "l"(g) : "memory");
-}
-__device__ __forceinline__ void cp_async8(void* s, const void* g) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr(s)), "l"(g) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
-
-template <int B>
-__device__ __forceinline__ void cp_async_elem(void* s, const void* g) {
-  if (B == 4) cp_async4(s, g);
-  else cp_async8(s, g);
-}
 
 struct KwayMergeArgs {
   KwayShards S;
@@ -282,213 +276,156 @@ struct KwayMergeArgs {
   unsigned long long* claim;  // zeroed before launch
 };
 
-// Stable merge of two sorted sequences a (len na) and b (len nb), producing
-// outputs [d0, d1) of their merge (ties to a).  Accessors return (key, slot).
-template <typename K, typename FA, typename FB, typename FO>
-__device__ __forceinline__ void merge_range(FA fa, int na, FB fb, int nb, int d0, int d1, FO emit) {
-  // merge path: i = #a among the first d0 outputs
-  int lo = d0 - nb > 0 ? d0 - nb : 0, hi = d0 < na ? d0 : na;
-  while (lo < hi) {
-    int i = (lo + hi) >> 1;  // take a[i] before b[d0-1-i]?  a[i] <= b[d0-1-i] (ties to a)
-    K ai, bj;
-    uint16_t s;
-    fa(i, ai, s);
-    fb(d0 - 1 - i, bj, s);
-    if (ai <= bj) lo = i + 1;
-    else hi = i;
-  }
-  int i = lo, j = d0 - lo;
-  for (int d = d0; d < d1; ++d) {
-    K ka = K(), kb2 = K();
-    uint16_t sa = 0, sb = 0;
-    if (i < na) fa(i, ka, sa);
-    if (j < nb) fb(j, kb2, sb);
-    bool ta = j >= nb || (i < na && ka <= kb2);
-    if (ta) {
-      emit(d, ka, sa);
-      ++i;
-    } else {
-      emit(d, kb2, sb);
-      ++j;
-    }
-  }
-}
-
 template <typename K, int TB>
-__global__ void __launch_bounds__(512, 1) k_kway_merge(KwayMergeArgs A) {
+__global__ void __launch_bounds__(256, 2) k_kway_merge(KwayMergeArgs A) {
   using C = KwayCfg<K, TB>;
-  constexpr int KS = C::KS, WIN = C::WIN, T = C::THREADS;
-  extern __shared__ __align__(16) unsigned char smem_kw[];
+  using T = typename TagT<TB>::type;
+  constexpr bool HT = TB != 0;
+  constexpr int NT = C::THREADS;
+  constexpr int kHalf = kKwayMaxW / 2 + 1;
+  extern __shared__ __align__(128) unsigned char smem_kw[];
+  __shared__ __align__(8) uint64_t lbar[2];
+  __shared__ int64_t s_item[2], s_out[2];
+  __shared__ int s_kseg[2][kKwayMaxW], s_tseg[2][kKwayMaxW], s_len[2][kKwayMaxW];  // per load buffer
   const int W = A.S.w;
-  int wp = 1;
-  while (wp < W) wp <<= 1;
-  K* wk = reinterpret_cast<K*>(smem_kw);                                   // [wp][WIN]
-  unsigned char* wt = smem_kw + (size_t)wp * WIN * sizeof(K);               // [wp][WIN] tags
-  unsigned char* lv = smem_kw + C::win_bytes(wp);                           // level buffers
-  // level l (1..levels) list p: entries at lvl_off(l) + p*KS; keys then slots
-  __shared__ int64_t s_cur[kKwayMaxW], s_loaded[kKwayMaxW], s_hi[kKwayMaxW];
-  __shared__ int s_len[2 * kKwayMaxW];  // current level's list lengths (read side)
-  __shared__ int s_cons[kKwayMaxW];
-  __shared__ int64_t s_item, s_out;
   const int tid = threadIdx.x;
-  int levels = 0;
-  while ((1 << levels) < wp) ++levels;
-  // level buffers: ping = wp/2 lists, pong = wp/4 lists (+1 for the wp = 2 case)
-  K* lk[2];
-  uint16_t* ls[2];
-  {
-    size_t n0 = (size_t)(wp / 2 > 0 ? wp / 2 : 1) * KS, n1 = (size_t)(wp / 4 > 0 ? wp / 4 : 1) * KS;
-    lk[0] = reinterpret_cast<K*>(lv);
-    lk[1] = lk[0] + n0;
-    ls[0] = reinterpret_cast<uint16_t*>(lk[1] + n1);
-    ls[1] = ls[0] + n0;
+  auto kbuf = [&](int b) { return reinterpret_cast<K*>(smem_kw + (size_t)b * C::BUF); };
+  auto tbuf = [&](int b) { return reinterpret_cast<T*>(smem_kw + (size_t)b * C::BUF + C::KBUF); };
+  if (tid == 0) {
+    mbar_init(&lbar[0], 1);
+    mbar_init(&lbar[1], 1);
+    mbar_fence_init();
   }
-  K* okeys = reinterpret_cast<K*>(A.out_keys);
+  __syncthreads();
   const int64_t nitems = *A.nitems;
-  for (;;) {
-    __syncthreads();
-    if (tid == 0) s_item = (int64_t)atomicAdd(A.claim, 1ull);
-    __syncthreads();
-    const int64_t item = s_item;
-    if (item >= nitems) break;
-    if (tid < W) {
-      int64_t lo = A.bounds[item * W + tid], hi = A.bounds[(item + 1) * W + tid];
-      s_cur[tid] = lo;
-      s_loaded[tid] = lo;
-      s_hi[tid] = hi;
-    }
-    if (tid == 0) {
-      int64_t o = 0;
-      for (int i = 0; i < W; ++i) o += A.bounds[item * W + i] - A.bounds[i];
-      s_out = o;
-    }
-    __syncthreads();
-    int64_t remaining = 0;
-    for (int i = 0; i < W; ++i) remaining += s_hi[i] - s_cur[i];
-    // initial fill: two groups (the first K and the next K of every shard)
-    for (int g = 0; g < 2; ++g) {
-      for (int i = 0; i < W; ++i) {
-        int64_t p0 = s_cur[i] + (int64_t)g * KS, p1 = p0 + KS;
-        if (p1 > s_hi[i]) p1 = s_hi[i];
-        const K* gk = reinterpret_cast<const K*>(A.S.keys[i]);
-        for (int64_t p = p0 + tid; p < p1; p += T) {
-          int sl = (int)(p & (WIN - 1));
-          cp_async_elem<sizeof(K)>(&wk[i * WIN + sl], gk + p);
-          if (TB) cp_async_elem<(TB ? TB : 4)>(wt + ((size_t)i * WIN + sl) * TB, (const unsigned char*)A.S.tags[i] + p * TB);
-        }
+  // Thread 0: claim an item and issue its windows' bulk copies into load buffer
+  // b (16-byte covers; s_kseg / s_tseg = where each window's first element lands).
+  auto fetch = [&](int b) {
+    if (tid != 0) return;
+    const int64_t item = (int64_t)atomicAdd(A.claim, 1ull);
+    s_item[b] = item;
+    if (item >= nitems) return;
+    int64_t o = 0;
+    uint32_t bytes = 0;
+    for (int i = 0; i < W; ++i) {
+      const int64_t lo = A.bounds[item * W + i], hi = A.bounds[(item + 1) * W + i];
+      o += lo - A.bounds[i];
+      s_len[b][i] = (int)(hi - lo);
+      if (hi <= lo) continue;
+      uintptr_t a0 = reinterpret_cast<uintptr_t>(reinterpret_cast<const K*>(A.S.keys[i]) + lo);
+      uintptr_t a1 = reinterpret_cast<uintptr_t>(reinterpret_cast<const K*>(A.S.keys[i]) + hi);
+      bytes += (uint32_t)(((a1 + 15) & ~(uintptr_t)15) - (a0 & ~(uintptr_t)15));
+      if (HT) {
+        uintptr_t t0 = reinterpret_cast<uintptr_t>(reinterpret_cast<const T*>(A.S.tags[i]) + lo);
+        uintptr_t t1 = reinterpret_cast<uintptr_t>(reinterpret_cast<const T*>(A.S.tags[i]) + hi);
+        bytes += (uint32_t)(((t1 + 15) & ~(uintptr_t)15) - (t0 & ~(uintptr_t)15));
       }
-      cp_async_commit();
     }
-    __syncthreads();
-    if (tid < W) {
-      int64_t e = s_cur[tid] + 2 * KS;
-      s_loaded[tid] = e < s_hi[tid] ? e : s_hi[tid];
+    s_out[b] = o;
+    fence_proxy_async_smem();  // the buffer's earlier generic reads -> these async writes
+    mbar_arrive_tx(&lbar[b], bytes);
+    unsigned char* kd = reinterpret_cast<unsigned char*>(kbuf(b));
+    unsigned char* td = HT ? reinterpret_cast<unsigned char*>(tbuf(b)) : nullptr;
+    int kdo = 0, tdo = 0;  // bytes used so far (16-aligned)
+    for (int i = 0; i < W; ++i) {
+      const int64_t lo = A.bounds[item * W + i], hi = A.bounds[(item + 1) * W + i];
+      s_kseg[b][i] = kdo / (int)sizeof(K);
+      s_tseg[b][i] = HT ? tdo / (HT ? TB : 1) : 0;
+      if (hi <= lo) continue;
+      int32_t off;
+      kdo += (int)tma_window(kd + kdo, A.S.keys[i], lo, hi, sizeof(K), &lbar[b], &off);
+      s_kseg[b][i] += off;
+      if (HT) {
+        tdo += (int)tma_window(td + tdo, A.S.tags[i], lo, hi, TB, &lbar[b], &off);
+        s_tseg[b][i] += off;
+      }
     }
-    while (remaining > 0) {
-      cp_async_wait1();  // every group but the latest has landed (this thread's)
-      __syncthreads();
-      const int nout = remaining < KS ? (int)remaining : KS;
-      // level 1..levels: pairwise merges truncated to nout outputs
-      for (int l = 1; l <= levels; ++l) {
-        const int npairs = wp >> l;
-        const int tpp = T / npairs;  // threads per pair
-        const int pair = tid / tpp, r = tid % tpp;
-        const int out_buf = (l - 1) & 1, in_buf = (l - 2) & 1;
-        int la, lb;
-        if (l == 1) {
-          int a = 2 * pair, b = 2 * pair + 1;
-          la = a < W ? (int)min((int64_t)KS, s_hi[a] - s_cur[a]) : 0;
-          lb = b < W ? (int)min((int64_t)KS, s_hi[b] - s_cur[b]) : 0;
-        } else {
-          la = s_len[2 * pair];
-          lb = s_len[2 * pair + 1];
+  };
+  uint32_t ph[2] = {0u, 0u};
+  fetch(0);
+  int cur = 0;
+  for (;;) {
+    __syncthreads();  // s_item / segment tables visible; the last item's buffers are read
+    if (s_item[cur] >= nitems) break;
+    fetch(cur ^ 1);  // the next item's windows stream in while this one merges
+    mbar_wait(&lbar[cur], ph[cur]);
+    ph[cur] ^= 1u;
+    int N = 0;
+    for (int i = 0; i < W; ++i) N += s_len[cur][i];
+    // segments of the current level: key / tag starts and lengths (registers, uniform)
+    int kst[kKwayMaxW], tst[kKwayMaxW], len[kKwayMaxW];
+    for (int i = 0; i < W; ++i) {
+      kst[i] = s_kseg[cur][i];
+      tst[i] = s_tseg[cur][i];
+      len[i] = s_len[cur][i];
+    }
+    int nseg = W, src = cur, dst = 2;
+    while (nseg > 1) {
+      const int npairs = (nseg + 1) / 2;
+      int ost[kHalf + 1];
+      ost[0] = 0;
+      for (int p = 0; p < npairs; ++p) ost[p + 1] = ost[p] + len[2 * p] + (2 * p + 1 < nseg ? len[2 * p + 1] : 0);
+      const K* sk = kbuf(src);
+      const T* stg = HT ? tbuf(src) : nullptr;
+      K* dk = kbuf(dst);
+      T* dtg = HT ? tbuf(dst) : nullptr;
+      const int per = (N + NT - 1) / NT;
+      const int d0 = tid * per < N ? tid * per : N, d1 = d0 + per < N ? d0 + per : N;
+      for (int p = 0; p < npairs; ++p) {
+        const int s0 = d0 > ost[p] ? d0 : ost[p], s1 = d1 < ost[p + 1] ? d1 : ost[p + 1];
+        if (s0 >= s1) continue;
+        const int ia_ = 2 * p, ib_ = 2 * p + 1;
+        const K* Ak = sk + kst[ia_];
+        const int la = len[ia_];
+        const K* Bk = ib_ < nseg ? sk + kst[ib_] : Ak;
+        const int lb = ib_ < nseg ? len[ib_] : 0;
+        const T* At = HT ? stg + tst[ia_] : nullptr;
+        const T* Bt = HT ? (ib_ < nseg ? stg + tst[ib_] : At) : nullptr;
+        const int x0 = s0 - ost[p];
+        int lo = x0 - lb > 0 ? x0 - lb : 0, hi = x0 < la ? x0 : la;  // #A among the first x0 outputs
+        while (lo < hi) {
+          int mid = (lo + hi) >> 1;
+          if (Ak[mid] <= Bk[x0 - 1 - mid]) lo = mid + 1;
+          else hi = mid;
         }
-        int tot = la + lb < nout ? la + lb : nout;
-        int per = (tot + tpp - 1) / tpp;
-        int d0 = r * per, d1 = d0 + per < tot ? d0 + per : tot;
-        K* ok = lk[out_buf] + (size_t)pair * KS;
-        uint16_t* os = ls[out_buf] + (size_t)pair * KS;
-        auto emit = [&](int d, K k, uint16_t s) {
-          ok[d] = k;
-          os[d] = s;
-        };
-        if (d0 < d1) {
-          if (l == 1) {
-            int a = 2 * pair, b = 2 * pair + 1;
-            int64_t ca = a < W ? s_cur[a] : 0, cb = b < W ? s_cur[b] : 0;
-            auto fa = [&](int x, K& k, uint16_t& s) {
-              int sl = (int)((ca + x) & (WIN - 1));
-              k = wk[a * WIN + sl];
-              s = (uint16_t)(a * WIN + sl);
-            };
-            auto fb = [&](int x, K& k, uint16_t& s) {
-              int sl = (int)((cb + x) & (WIN - 1));
-              k = wk[b * WIN + sl];
-              s = (uint16_t)(b * WIN + sl);
-            };
-            merge_range<K>(fa, la, fb, lb, d0, d1, emit);
+        int ia = lo, ib = x0 - lo;
+        for (int d = s0; d < s1; ++d) {
+          const bool ta = ib >= lb || (ia < la && Ak[ia] <= Bk[ib]);  // ties: the lower shard
+          if (ta) {
+            dk[d] = Ak[ia];
+            if (HT) dtg[d] = At[ia];
+            ++ia;
           } else {
-            const K* ak = lk[in_buf] + (size_t)(2 * pair) * KS;
-            const uint16_t* as = ls[in_buf] + (size_t)(2 * pair) * KS;
-            const K* bk = lk[in_buf] + (size_t)(2 * pair + 1) * KS;
-            const uint16_t* bs = ls[in_buf] + (size_t)(2 * pair + 1) * KS;
-            auto fa = [&](int x, K& k, uint16_t& s) { k = ak[x]; s = as[x]; };
-            auto fb = [&](int x, K& k, uint16_t& s) { k = bk[x]; s = bs[x]; };
-            merge_range<K>(fa, la, fb, lb, d0, d1, emit);
+            dk[d] = Bk[ib];
+            if (HT) dtg[d] = Bt[ib];
+            ++ib;
           }
         }
-        __syncthreads();
-        if (r == 0) s_len[pair] = tot;  // read side of the next level
-        __syncthreads();
       }
-      // wp == 1: the single shard's window is the output
-      const K* fk = lk[(levels - 1) & 1];
-      const uint16_t* fs = ls[(levels - 1) & 1];
-      if (tid < W) s_cons[tid] = 0;
-      __syncthreads();
-      const int64_t ob = s_out;
-      for (int d = tid; d < nout; d += T) {
-        K k;
-        uint16_t s;
-        if (levels == 0) {
-          int sl = (int)((s_cur[0] + d) & (WIN - 1));
-          k = wk[sl];
-          s = (uint16_t)sl;
-        } else {
-          k = fk[d];
-          s = fs[d];
-        }
-        okeys[ob + d] = k;
-        if (TB == 4)
-          reinterpret_cast<uint32_t*>(A.out_tags)[ob + d] = *reinterpret_cast<const uint32_t*>(wt + (size_t)s * 4);
-        else if (TB == 8)
-          reinterpret_cast<uint64_t*>(A.out_tags)[ob + d] = *reinterpret_cast<const uint64_t*>(wt + (size_t)s * 8);
-        atomicAdd(&s_cons[s / WIN], 1);
+      __syncthreads();  // the level is complete
+      for (int p = 0; p < npairs; ++p) {
+        kst[p] = ost[p];
+        tst[p] = ost[p];
+        len[p] = ost[p + 1] - ost[p];
       }
-      __syncthreads();
-      if (tid < W) s_cur[tid] += s_cons[tid];
-      if (tid == 0) s_out = ob + nout;
-      remaining -= nout;
-      __syncthreads();
-      // refill: [loaded, min(cur + 2K, hi)) into the slots just consumed
-      for (int i = 0; i < W; ++i) {
-        int64_t p0 = s_loaded[i], p1 = s_cur[i] + 2 * KS;
-        if (p1 > s_hi[i]) p1 = s_hi[i];
-        const K* gk = reinterpret_cast<const K*>(A.S.keys[i]);
-        for (int64_t p = p0 + tid; p < p1; p += T) {
-          int sl = (int)(p & (WIN - 1));
-          cp_async_elem<sizeof(K)>(&wk[i * WIN + sl], gk + p);
-          if (TB) cp_async_elem<(TB ? TB : 4)>(wt + ((size_t)i * WIN + sl) * TB, (const unsigned char*)A.S.tags[i] + p * TB);
-        }
-      }
-      cp_async_commit();
-      __syncthreads();
-      if (tid < W) {
-        int64_t e = s_cur[tid] + 2 * KS;
-        s_loaded[tid] = e < s_hi[tid] ? e : s_hi[tid];
+      nseg = npairs;
+      const int t = src;  // ping-pong: the merge buffer and this item's own load buffer
+      src = dst;
+      dst = t;
+    }
+    // coalesced write-out of the single remaining segment
+    {
+      const K* fk = kbuf(src) + kst[0];
+      const T* ft = HT ? tbuf(src) + tst[0] : nullptr;
+      const int64_t ob = s_out[cur];
+      K* ok = reinterpret_cast<K*>(A.out_keys) + ob;
+      T* ot = HT ? reinterpret_cast<T*>(A.out_tags) + ob : nullptr;
+      for (int d = tid; d < N; d += NT) {
+        ok[d] = fk[d];
+        if (HT) ot[d] = ft[d];
       }
     }
-    cp_async_wait0();
+    cur ^= 1;
   }
 }
 

@@ -1095,9 +1095,11 @@ template <typename K, int TB>
 KwayLayout kway_layout(const KwayShards& S, int64_t out_len, bool dev_ranges, int sms) {
   KwayLayout KL{};
   int64_t M = out_len;
-  int64_t sp = M / (8 * (int64_t)sms);  // ~8 work items per SM
-  if (sp > ((int64_t)1 << 17)) sp = (int64_t)1 << 17;
-  if (sp < KwayCfg<K, TB>::KS) sp = KwayCfg<K, TB>::KS;
+  (void)sms;
+  // pivots every `sp` elements of each shard: a work item (between consecutive
+  // pivots in global order) holds at most sp elements of each shard, so at most
+  // ITEM in all -- it fits the merge kernel's shared-memory buffers
+  int64_t sp = KwayCfg<K, TB>::spacing(S.w);
   KL.spacing = sp;
   KL.piv.off[0] = 0;
   if (!dev_ranges) {
@@ -1135,12 +1137,10 @@ int run_kway(const KwayShards& S, const int64_t* dsplit, int64_t out_len, void* 
   if (pgrid < 1) pgrid = 1;
   k_kway_pivots<K><<<pgrid, 256, 0, st>>>(S, KL.spacing, KL.piv, KL.npiv, bounds, dsplit, nitems);
   RS_CUDA(cudaGetLastError());
-  int wp = 1;
-  while (wp < S.w) wp <<= 1;
-  size_t sm = KwayCfg<K, TB>::smem(wp);
+  size_t sm = KwayCfg<K, TB>::SMEM;
   int occ;
-  if (int e = occupancy((const void*)k_kway_merge<K, TB>, KwayCfg<K, TB>::THREADS, sm,
-                        KwayCfg<K, TB>::smem(kKwayMaxW), &occ, "k-way merge kernel"))
+  if (int e = occupancy((const void*)k_kway_merge<K, TB>, KwayCfg<K, TB>::THREADS, sm, sm, &occ,
+                        "k-way merge kernel"))
     return e;
   KwayMergeArgs A;
   A.S = S;
