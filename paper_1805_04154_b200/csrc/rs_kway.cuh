@@ -243,6 +243,37 @@ __global__ void __launch_bounds__(256) k_kway_pivots(KwayShards S, int64_t spaci
   }
 }
 
+// Item boundaries: item k starts at the first pivot row whose global rank is
+// >= k * group (rank(q) = sum_i bounds[q][i] - bounds[0][i], monotone in q;
+// rows 0 .. nrows-1 with nrows = *npiv_items + 1).  item_rows[nitems] = the
+// last row; *nitems_out = the item count.
+__global__ void __launch_bounds__(256) k_kway_items(const int64_t* __restrict__ bounds, int w,
+                                                    const int64_t* __restrict__ npiv_items, int64_t group,
+                                                    int64_t kmax, int64_t* __restrict__ item_rows,
+                                                    int64_t* __restrict__ nitems_out) {
+  const int64_t last = *npiv_items;  // row index of the ends
+  int64_t total = 0;
+  for (int i = 0; i < w; ++i) total += bounds[last * w + i] - bounds[i];
+  const int64_t K = total > 0 ? (total + group - 1) / group : 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *nitems_out = K;
+    item_rows[K] = last;
+  }
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < K && k < kmax;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = k * group;
+    int64_t lo = 0, hi = last;  // smallest row with rank >= t
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      int64_t r = 0;
+      for (int i = 0; i < w; ++i) r += bounds[mid * w + i] - bounds[i];
+      if (r >= t) hi = mid;
+      else lo = mid + 1;
+    }
+    item_rows[k] = lo;
+  }
+}
+
 // k_kway_merge: persistent CTAs claim work items (the intervals between
 // consecutive pivots in global order: at most `spacing` elements of each
 // shard, so at most ITEM in all).  An item's W windows arrive in shared memory
@@ -264,13 +295,25 @@ struct KwayCfg {
   static constexpr size_t TBUF = TB ? ((size_t)CAP * (TB ? TB : 1) + 127) / 128 * 128 : 0;
   static constexpr size_t BUF = KBUF + TBUF;
   static constexpr size_t SMEM = 3 * BUF + 256;  // two load buffers + one merge buffer
-  static int64_t spacing(int w) { return ITEM / (w > 0 ? w : 1); }
+  // Items are cut where the pivots' global ranks cross multiples of GROUP, and
+  // consecutive pivots are at most W * spacing apart, so an item holds fewer
+  // than GROUP + W * spacing <= ITEM elements (about GROUP on average).
+  static constexpr int GROUP = ITEM / 2;
+  static int64_t spacing(int w) { return GROUP / (w > 0 ? w : 1); }
 };
+
+__device__ __forceinline__ void cp_async16(void* s, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(s)), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 struct KwayMergeArgs {
   KwayShards S;
   const int64_t* bounds;  // (nitems + 1) x W split vectors; row 0 = the ranges' starts
-  const int64_t* nitems;  // written by k_kway_pivots
+  const int64_t* nitems;     // written by k_kway_items
+  const int64_t* item_rows;  // item k = pivot rows [item_rows[k], item_rows[k + 1])
   void* out_keys;
   void* out_tags;
   unsigned long long* claim;  // zeroed before launch
@@ -284,72 +327,96 @@ __global__ void __launch_bounds__(256, 2) k_kway_merge(KwayMergeArgs A) {
   constexpr int NT = C::THREADS;
   constexpr int kHalf = kKwayMaxW / 2 + 1;
   extern __shared__ __align__(128) unsigned char smem_kw[];
-  __shared__ __align__(8) uint64_t lbar[2];
   __shared__ int64_t s_item[2], s_out[2];
   __shared__ int s_kseg[2][kKwayMaxW], s_tseg[2][kKwayMaxW], s_len[2][kKwayMaxW];  // per load buffer
   const int W = A.S.w;
   const int tid = threadIdx.x;
   auto kbuf = [&](int b) { return reinterpret_cast<K*>(smem_kw + (size_t)b * C::BUF); };
   auto tbuf = [&](int b) { return reinterpret_cast<T*>(smem_kw + (size_t)b * C::BUF + C::KBUF); };
-  if (tid == 0) {
-    mbar_init(&lbar[0], 1);
-    mbar_init(&lbar[1], 1);
-    mbar_fence_init();
-  }
-  __syncthreads();
   const int64_t nitems = *A.nitems;
-  // Thread 0: claim an item and issue its windows' bulk copies into load buffer
-  // b (16-byte covers; s_kseg / s_tseg = where each window's first element lands).
+  // Collective: claim an item and stream its windows into load buffer b with
+  // 16-byte cp.async copies spread over all threads (one commit group per call,
+  // empty when no item is left).  Windows are copied as their 16-byte covers;
+  // s_kseg / s_tseg = where each window's first element lands.  (Whole-window
+  // 1D bulk copies cost ~1 us each for the few-hundred-byte windows of an
+  // 8-way item; the W bounds are read by W threads at once.)
+  __shared__ int64_t s_lo[kKwayMaxW], s_base[kKwayMaxW];
+  __shared__ uint32_t s_kc[kKwayMaxW + 1], s_tc[kKwayMaxW + 1];  // chunk prefix (16-byte units)
+  __shared__ uintptr_t s_ka[kKwayMaxW], s_ta[kKwayMaxW];            // aligned source addresses
   auto fetch = [&](int b) {
-    if (tid != 0) return;
-    const int64_t item = (int64_t)atomicAdd(A.claim, 1ull);
-    s_item[b] = item;
-    if (item >= nitems) return;
-    int64_t o = 0;
-    uint32_t bytes = 0;
-    for (int i = 0; i < W; ++i) {
-      const int64_t lo = A.bounds[item * W + i], hi = A.bounds[(item + 1) * W + i];
-      o += lo - A.bounds[i];
-      s_len[b][i] = (int)(hi - lo);
-      if (hi <= lo) continue;
-      uintptr_t a0 = reinterpret_cast<uintptr_t>(reinterpret_cast<const K*>(A.S.keys[i]) + lo);
-      uintptr_t a1 = reinterpret_cast<uintptr_t>(reinterpret_cast<const K*>(A.S.keys[i]) + hi);
-      bytes += (uint32_t)(((a1 + 15) & ~(uintptr_t)15) - (a0 & ~(uintptr_t)15));
+    if (tid == 0) s_item[b] = (int64_t)atomicAdd(A.claim, 1ull);
+    __syncthreads();
+    const int64_t item = s_item[b];
+    if (item < nitems) {
+      if (tid < W) {
+        const int64_t r0 = A.item_rows[item], r1 = A.item_rows[item + 1];
+        const int64_t lo = A.bounds[r0 * W + tid], hi = A.bounds[r1 * W + tid], base = A.bounds[tid];
+        s_lo[tid] = lo;
+        s_base[tid] = base;
+        s_len[b][tid] = (int)(hi - lo);
+        uint32_t kc = 0, tc = 0;
+        if (hi > lo) {
+          uintptr_t a0 = reinterpret_cast<uintptr_t>(reinterpret_cast<const K*>(A.S.keys[tid]) + lo);
+          uintptr_t a1 = reinterpret_cast<uintptr_t>(reinterpret_cast<const K*>(A.S.keys[tid]) + hi);
+          s_ka[tid] = a0 & ~(uintptr_t)15;
+          kc = (uint32_t)((((a1 + 15) & ~(uintptr_t)15) - s_ka[tid]) / 16);
+          s_kseg[b][tid] = (int)((a0 & 15) / sizeof(K));  // + the window's base, below
+          if (HT) {
+            uintptr_t t0 = reinterpret_cast<uintptr_t>(reinterpret_cast<const T*>(A.S.tags[tid]) + lo);
+            uintptr_t t1 = reinterpret_cast<uintptr_t>(reinterpret_cast<const T*>(A.S.tags[tid]) + hi);
+            s_ta[tid] = t0 & ~(uintptr_t)15;
+            tc = (uint32_t)((((t1 + 15) & ~(uintptr_t)15) - s_ta[tid]) / 16);
+            s_tseg[b][tid] = (int)((t0 & 15) / (HT ? TB : 1));
+          }
+        } else {
+          s_kseg[b][tid] = 0;
+          s_tseg[b][tid] = 0;
+        }
+        s_kc[tid + 1] = kc;
+        s_tc[tid + 1] = tc;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        int64_t o = 0;
+        s_kc[0] = 0;
+        s_tc[0] = 0;
+        for (int i = 0; i < W; ++i) {
+          o += s_lo[i] - s_base[i];
+          s_kseg[b][i] += (int)(s_kc[i] * 16 / sizeof(K));
+          if (HT) s_tseg[b][i] += (int)(s_tc[i] * 16 / (HT ? TB : 1));
+          s_kc[i + 1] += s_kc[i];
+          s_tc[i + 1] += s_tc[i];
+        }
+        s_out[b] = o;
+      }
+      __syncthreads();
+      unsigned char* kd = reinterpret_cast<unsigned char*>(kbuf(b));
+      for (uint32_t c = tid; c < s_kc[W]; c += NT) {
+        int i = 0;
+        while (s_kc[i + 1] <= c) ++i;
+        const uint32_t r = c - s_kc[i];
+        cp_async16(kd + (size_t)c * 16, reinterpret_cast<const void*>(s_ka[i] + (uintptr_t)r * 16));
+      }
       if (HT) {
-        uintptr_t t0 = reinterpret_cast<uintptr_t>(reinterpret_cast<const T*>(A.S.tags[i]) + lo);
-        uintptr_t t1 = reinterpret_cast<uintptr_t>(reinterpret_cast<const T*>(A.S.tags[i]) + hi);
-        bytes += (uint32_t)(((t1 + 15) & ~(uintptr_t)15) - (t0 & ~(uintptr_t)15));
+        unsigned char* td = reinterpret_cast<unsigned char*>(tbuf(b));
+        for (uint32_t c = tid; c < s_tc[W]; c += NT) {
+          int i = 0;
+          while (s_tc[i + 1] <= c) ++i;
+          const uint32_t r = c - s_tc[i];
+          cp_async16(td + (size_t)c * 16, reinterpret_cast<const void*>(s_ta[i] + (uintptr_t)r * 16));
+        }
       }
     }
-    s_out[b] = o;
-    fence_proxy_async_smem();  // the buffer's earlier generic reads -> these async writes
-    mbar_arrive_tx(&lbar[b], bytes);
-    unsigned char* kd = reinterpret_cast<unsigned char*>(kbuf(b));
-    unsigned char* td = HT ? reinterpret_cast<unsigned char*>(tbuf(b)) : nullptr;
-    int kdo = 0, tdo = 0;  // bytes used so far (16-aligned)
-    for (int i = 0; i < W; ++i) {
-      const int64_t lo = A.bounds[item * W + i], hi = A.bounds[(item + 1) * W + i];
-      s_kseg[b][i] = kdo / (int)sizeof(K);
-      s_tseg[b][i] = HT ? tdo / (HT ? TB : 1) : 0;
-      if (hi <= lo) continue;
-      int32_t off;
-      kdo += (int)tma_window(kd + kdo, A.S.keys[i], lo, hi, sizeof(K), &lbar[b], &off);
-      s_kseg[b][i] += off;
-      if (HT) {
-        tdo += (int)tma_window(td + tdo, A.S.tags[i], lo, hi, TB, &lbar[b], &off);
-        s_tseg[b][i] += off;
-      }
-    }
+    cp_async_commit();
   };
-  uint32_t ph[2] = {0u, 0u};
   fetch(0);
   int cur = 0;
   for (;;) {
     __syncthreads();  // s_item / segment tables visible; the last item's buffers are read
     if (s_item[cur] >= nitems) break;
     fetch(cur ^ 1);  // the next item's windows stream in while this one merges
-    mbar_wait(&lbar[cur], ph[cur]);
-    ph[cur] ^= 1u;
+    cp_async_wait1();  // this thread's copies of the current item have landed
+    __syncthreads();   // ... and everyone's
     int N = 0;
     for (int i = 0; i < W; ++i) N += s_len[cur][i];
     // segments of the current level: key / tag starts and lengths (registers, uniform)
@@ -427,6 +494,7 @@ __global__ void __launch_bounds__(256, 2) k_kway_merge(KwayMergeArgs A) {
     }
     cur ^= 1;
   }
+  cp_async_wait0();
 }
 
 }  // namespace rs

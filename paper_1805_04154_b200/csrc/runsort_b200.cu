@@ -1086,7 +1086,8 @@ int load_shards(const rs_shard* shards, int w, int tag_bytes, KwayShards* S) {
 struct KwayLayout {
   int64_t spacing, npiv, npiv_cap;
   KwayPiv piv;
-  size_t o_bounds, o_nitems, o_claim, total;
+  size_t o_bounds, o_nitems, o_claim, o_items, o_nitems2, total;
+  int64_t kmax;  // item-count bound
 };
 
 // out_len: the merged length (the ranges' total); with device-resident ranges
@@ -1117,6 +1118,11 @@ KwayLayout kway_layout(const KwayShards& S, int64_t out_len, bool dev_ranges, in
   off = align_up(off + 8, 256);
   KL.o_claim = off;
   off = align_up(off + 8, 256);
+  KL.kmax = M / KwayCfg<K, TB>::GROUP + 2;
+  KL.o_items = off;
+  off = align_up(off + (size_t)(KL.kmax + 1) * 8, 256);
+  KL.o_nitems2 = off;
+  off = align_up(off + 8, 256);
   KL.total = off + 256;
   return KL;
 }
@@ -1137,6 +1143,12 @@ int run_kway(const KwayShards& S, const int64_t* dsplit, int64_t out_len, void* 
   if (pgrid < 1) pgrid = 1;
   k_kway_pivots<K><<<pgrid, 256, 0, st>>>(S, KL.spacing, KL.piv, KL.npiv, bounds, dsplit, nitems);
   RS_CUDA(cudaGetLastError());
+  int64_t* item_rows = reinterpret_cast<int64_t*>(ws + KL.o_items);
+  int64_t* nitems2 = reinterpret_cast<int64_t*>(ws + KL.o_nitems2);
+  int igrid = (int)std::min<int64_t>((KL.kmax + 255) / 256, (int64_t)sms * 8);
+  if (igrid < 1) igrid = 1;
+  k_kway_items<<<igrid, 256, 0, st>>>(bounds, S.w, nitems, KwayCfg<K, TB>::GROUP, KL.kmax, item_rows, nitems2);
+  RS_CUDA(cudaGetLastError());
   size_t sm = KwayCfg<K, TB>::SMEM;
   int occ;
   if (int e = occupancy((const void*)k_kway_merge<K, TB>, KwayCfg<K, TB>::THREADS, sm, sm, &occ,
@@ -1145,11 +1157,12 @@ int run_kway(const KwayShards& S, const int64_t* dsplit, int64_t out_len, void* 
   KwayMergeArgs A;
   A.S = S;
   A.bounds = bounds;
-  A.nitems = nitems;
+  A.nitems = nitems2;
+  A.item_rows = item_rows;
   A.out_keys = out_keys;
   A.out_tags = out_tags;
   A.claim = claim;
-  int grid = (int)std::min<int64_t>((int64_t)sms * occ, KL.npiv_cap + 1);
+  int grid = (int)std::min<int64_t>((int64_t)sms * occ, KL.kmax);
   k_kway_merge<K, TB><<<grid, KwayCfg<K, TB>::THREADS, sm, st>>>(A);
   RS_CUDA(cudaGetLastError());
   return RS_OK;
