@@ -110,6 +110,11 @@ struct ClassifyArgs {
   const uint32_t* child;
   MDesc* mdesc;      // per merge task, index = task slot - first merge slot (met->phaseA)
   int64_t mdesc_cap;
+  // k_prep's grid path: the ancestor counts, from which classification derives
+  // (and writes) depth / leaf_depth itself -- the trie phase then no longer
+  // waits for the ancestor scans (null: depths are already in place)
+  const uint8_t* la = nullptr;
+  const uint8_t* ra = nullptr;
 };
 
 // Merge descriptor of node i (two dependent round trips: the node's fields,
@@ -220,6 +225,11 @@ __device__ void d_classify(ClassifyArgs A, uint32_t* __restrict__ chunk_depth) {
     __syncthreads();
     const int64_t i = i0 + threadIdx.x;
     if (i < r) {
+    if (A.la) {  // depths from the ancestor counts (sorters.py:500-502: depth = left + right ancestors)
+      int32_t pl = A.parent[A.leaf_base + (uint32_t)i];
+      const_cast<uint8_t*>(A.leaf_depth)[i] = pl >= 0 ? (uint8_t)(A.la[pl] + A.ra[pl] + 1) : (uint8_t)0;
+      if (i >= 1) const_cast<uint8_t*>(A.depth)[i] = (uint8_t)(A.la[i] + A.ra[i]);
+    }
     // leaf: detection comparisons (runcore.py:154/157 closed form)
     pos_t s0 = A.leaf_start[i], len = A.leaf_start[i + 1] - s0;
     if (!A.peek && s0 < A.n - 1) {

@@ -113,13 +113,15 @@ __global__ void __launch_bounds__(256, 3) k_prep(PrepArgs P) {
   RS_ARR(met, 5);
   grid.sync();
   RS_TS(met, 5);
-  // 6. depths, max stack height (sorters.py:500-502)
-  d_scan_down(P.T.P, met, P.agg, P.nchunks, const_cast<uint8_t*>(P.T.la), const_cast<uint8_t*>(P.T.ra));
-  RS_ARR(met, 6);
-  grid.sync();
-  RS_TS(met, 6);
-  // 7. trie ranges, parents, children, spans
-  d_tree(P.T, P.F, met);
+  // 6+7. ancestor counts -> max stack height (sorters.py:500-502), and in the
+  // same phase on the other blocks: trie ranges, parents, children, spans
+  // (independent of the counts; classification derives the depths)
+  {
+    const int b0 = scan_down_blocks((int64_t)met->n_leaves);
+    if (b0 == 0 || (int)blockIdx.x < b0)
+      d_scan_down(P.T.P, met, P.agg, P.nchunks, const_cast<uint8_t*>(P.T.la), const_cast<uint8_t*>(P.T.ra));
+    d_tree(P.T, P.F, met, b0);
+  }
   RS_ARR(met, 7);
   grid.sync();
   RS_TS(met, 7);

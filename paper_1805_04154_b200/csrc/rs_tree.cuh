@@ -210,6 +210,16 @@ __device__ void d_scan_top(const DevMetrics* __restrict__ met, MC* __restrict__ 
   }
 }
 
+// Blocks that d_scan_down keeps busy (2 directions x chunks), capped so the
+// trie items keep at least half of the grid.
+__device__ __forceinline__ int scan_down_blocks(int64_t r) {
+  int64_t m = r - 1;
+  if (m <= 0) return 0;
+  const int64_t chunk = (int64_t)scan_items(m) * kScanThreads;
+  int64_t b = 2 * ((m + chunk - 1) / chunk);
+  return b > (int64_t)gridDim.x / 2 ? 0 : (int)b;
+}
+
 __device__ void d_scan_down(const uint8_t* __restrict__ P,
                                                             DevMetrics* __restrict__ met,
                                                             const MC* __restrict__ agg, int64_t nchunks_max,
@@ -286,9 +296,14 @@ struct TreeArrays {
   uint32_t leaf_base;
 };
 
-__device__ void d_tree(TreeArrays T, int F, const DevMetrics* __restrict__ met) {
+// Blocks [b0, gridDim.x) take the items (the first b0 blocks run the ancestor
+// scans of the same phase).  Depths are not written here: classification
+// derives them from the ancestor counts (ClassifyArgs::la / ra).
+__device__ void d_tree(TreeArrays T, int F, const DevMetrics* __restrict__ met, int b0 = 0) {
   int64_t r = (int64_t)met->n_leaves;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < r; i += (int64_t)gridDim.x * blockDim.x) {
+  if ((int)blockIdx.x < b0) return;
+  const int64_t nb = (int64_t)gridDim.x - b0;
+  for (int64_t i = ((int64_t)blockIdx.x - b0) * blockDim.x + threadIdx.x; i < r; i += nb * blockDim.x) {
     // leaf i
     {
       int64_t par = -1;
@@ -300,12 +315,7 @@ __device__ void d_tree(TreeArrays T, int F, const DevMetrics* __restrict__ met) 
       else if (hasR) { par = i + 1; side = 0; }
       uint32_t lid = T.leaf_base + (uint32_t)i;
       T.parent[lid] = (int32_t)par;
-      if (par >= 0) {
-        T.child[2 * par + side] = lid;
-        T.leaf_depth[i] = (uint8_t)(T.la[par] + T.ra[par] + 1);
-      } else {
-        T.leaf_depth[i] = 0;
-      }
+      if (par >= 0) T.child[2 * par + side] = lid;
     }
     if (i >= 1) {
       int64_t j = i;
@@ -343,7 +353,6 @@ __device__ void d_tree(TreeArrays T, int F, const DevMetrics* __restrict__ met) 
       T.node_b[j] = (int32_t)b;
       T.node_s[j] = T.leaf_start[a];
       T.node_e[j] = T.leaf_start[b + 1];
-      T.depth[j] = (uint8_t)(T.la[j] + T.ra[j]);
       int64_t par = -1;
       int side = 0;
       bool hasL = a >= 1, hasR = b + 1 <= r - 1;

@@ -580,6 +580,8 @@ int run_powersort(K* keys, void* tags, int64_t n, int w, int classic, unsigned c
   PA.leaves_only = leaves_only;
   int msuper = merge_super<K, TB>(n, sms);
   PA.CA = classify_args<K, TB>(V, L, n, w, classic, msuper, 0);
+  PA.CA.la = V.la;  // the grid path's classification derives the depths
+  PA.CA.ra = V.ra;
   PA.jobs = SmallJobs::at(V.jobs);
   int grid_p;
   void* kprep = ct == 1024 ? (void*)k_prep<K, 1024> : ct == 2560 ? (void*)k_prep<K, 2560> : (void*)k_prep<K, 2048>;
