@@ -243,6 +243,32 @@ __global__ void __launch_bounds__(256) k_kway_pivots(KwayShards S, int64_t spaci
   }
 }
 
+// W = 1: the merge is a copy of the one range (from S.lo / S.hi, or from the
+// device split rows).  Coalesced, 16 bytes per thread when both sides allow.
+template <typename K, int TB>
+__global__ void __launch_bounds__(256) k_kway_copy1(KwayShards S, const int64_t* __restrict__ dsplit, void* out_keys,
+                                                    void* out_tags) {
+  using T = typename TagT<TB>::type;
+  const int64_t lo = dsplit ? dsplit[0] : S.lo[0], hi = dsplit ? dsplit[1] : S.hi[0];
+  const int64_t len = hi - lo;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
+  const K* sk = reinterpret_cast<const K*>(S.keys[0]) + lo;
+  K* dk = reinterpret_cast<K*>(out_keys);
+  constexpr int VK = 16 / sizeof(K);
+  if (((reinterpret_cast<uintptr_t>(sk) | reinterpret_cast<uintptr_t>(dk)) & 15) == 0) {
+    const int64_t nv = len / VK;
+    for (int64_t i = tid; i < nv; i += nt) reinterpret_cast<uint4*>(dk)[i] = reinterpret_cast<const uint4*>(sk)[i];
+    for (int64_t i = nv * VK + tid; i < len; i += nt) dk[i] = sk[i];
+  } else {
+    for (int64_t i = tid; i < len; i += nt) dk[i] = sk[i];
+  }
+  if (TB) {
+    const T* st = reinterpret_cast<const T*>(S.tags[0]) + lo;
+    T* dt = reinterpret_cast<T*>(out_tags);
+    for (int64_t i = tid; i < len; i += nt) dt[i] = st[i];
+  }
+}
+
 // Item boundaries: item k starts at the first pivot row whose global rank is
 // >= k * group (rank(q) = sum_i bounds[q][i] - bounds[0][i], monotone in q;
 // rows 0 .. nrows-1 with nrows = *npiv_items + 1).  item_rows[nitems] = the

@@ -1136,6 +1136,12 @@ int run_kway(const KwayShards& S, const int64_t* dsplit, int64_t out_len, void* 
   if (int e = device_sms(&sms)) return e;
   KwayLayout KL = kway_layout<K, TB>(S, out_len, dsplit != nullptr, sms);
   if (ws_bytes < KL.total) return fail(RS_ENOMEM, "k-way merge workspace too small");
+  if (S.w == 1) {  // a copy, no pivots or items
+    int g = (int)std::min<int64_t>((out_len + 255) / 256, (int64_t)sms * 8);
+    k_kway_copy1<K, TB><<<g > 0 ? g : 1, 256, 0, st>>>(S, dsplit, out_keys, out_tags);
+    RS_CUDA(cudaGetLastError());
+    return RS_OK;
+  }
   int64_t* bounds = reinterpret_cast<int64_t*>(ws + KL.o_bounds);
   int64_t* nitems = reinterpret_cast<int64_t*>(ws + KL.o_nitems);
   unsigned long long* claim = reinterpret_cast<unsigned long long*>(ws + KL.o_claim);

@@ -348,7 +348,9 @@ def sharded_sort_p2p(space: P2PShardSpace, n_local: int, local_sort: Optional[Ca
         out_keys = torch.empty(n_local, dtype=space.keys.dtype, device=space.device)
     if tags is not None and out_tags is None:
         out_tags = torch.empty(n_local, dtype=space.tags.dtype, device=space.device)
-    mine = torch.tensor([n_local], dtype=torch.int64, device=space.device)
+    # a device fill, not torch.tensor(..., device=): that is a blocking host-to-device
+    # copy, which would hold the host until the local sort has finished
+    mine = torch.full((1,), int(n_local), dtype=torch.int64, device=space.device)
     if nccl:
         dlens = torch.empty(W, dtype=torch.int64, device=space.device)
         dist.all_gather_into_tensor(dlens, mine, group=group)
