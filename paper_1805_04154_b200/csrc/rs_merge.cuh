@@ -50,7 +50,15 @@ constexpr int kConsumerThreads = 32 * RS_CONSUMER_WARPS;  // consumer warps
 #define RS_PRODUCERS 1
 #endif
 constexpr int kProducers = RS_PRODUCERS;  // 1: one producer feeds both stages; 2: one stage each
-constexpr int kMergeThreads = kConsumerThreads + 32 * (kProducers + 1);  // + producers + signaller
+// RS_FETCHER: a fetcher warp claims the next task, loads its descriptor and
+// acquires its children's counters while the producer searches and issues
+// the current one (a one-slot shared-memory ticket queue between them).
+#ifndef RS_FETCHER
+#define RS_FETCHER 0
+#endif
+constexpr int kFetchers = RS_FETCHER ? 1 : 0;
+constexpr int kRoleWarps = kProducers + 1 + kFetchers;  // producers, signaller, fetcher
+constexpr int kMergeThreads = kConsumerThreads + 32 * kRoleWarps;
 
 template <typename K, int TB>
 struct MergeCfg {
@@ -316,6 +324,8 @@ __global__ void __launch_bounds__(kMergeThreads, RS_MERGE_CTAS) k_merge_exec(Mer
   __shared__ __align__(8) uint64_t empty_bar[kStages];
   __shared__ __align__(8) uint64_t stored_bar[kStages];
   __shared__ StageHdr hdr[kStages];
+  __shared__ __align__(8) uint64_t tk_full, tk_empty;  // fetcher -> producer ticket slot
+  __shared__ PTask tk_box;
 
   int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -324,6 +334,8 @@ __global__ void __launch_bounds__(kMergeThreads, RS_MERGE_CTAS) k_merge_exec(Mer
       mbar_init(&empty_bar[s], 1);
       mbar_init(&stored_bar[s], kConsumerThreads / 32);
     }
+    mbar_init(&tk_full, 1);
+    mbar_init(&tk_empty, 1);
     mbar_fence_init();
   }
   __syncthreads();
@@ -331,6 +343,32 @@ __global__ void __launch_bounds__(kMergeThreads, RS_MERGE_CTAS) k_merge_exec(Mer
   unsigned long long ntasks = E.met->n_tasks;
   // first merge task (after the phase-A tasks); not task_ctr, which other CTAs may already have advanced
   const unsigned long long t_first = E.met->phaseA;
+
+  if (kFetchers && warp == kProducers + 1) {
+    // -------------------------------------------------------------- fetcher
+    // Claims tasks in order and hands each, descriptor loaded and children's
+    // counters acquired, to the producer through the one-slot ticket: the
+    // claim -> descriptor -> counters chain of task t+1 runs while the
+    // producer searches and issues task t.  Tasks still wait only on tasks
+    // claimed before them, and the CTA finishes its tasks in claim order, so
+    // the resident grid cannot deadlock.
+    uint32_t ph = 0;
+    for (;;) {
+      PTask p;
+      p.tbase = t_first;
+      p.claim(E.met);
+      p.finish(E, ntasks);
+      if (lane == 0) {
+        mbar_wait(&tk_empty, ph ^ 1);
+        tk_box = p;
+        mbar_arrive(&tk_full);
+      }
+      ph ^= 1;
+      __syncwarp();
+      if (!p.valid) break;
+    }
+    return;
+  }
 
   if (warp < kProducers) {
     // ------------------------------------------------------------- producer
@@ -361,9 +399,24 @@ __global__ void __launch_bounds__(kMergeThreads, RS_MERGE_CTAS) k_merge_exec(Mer
     unsigned long long snext = t_first + (unsigned long long)blockIdx.x * kProducers + (unsigned long long)warp;
     PTask cur, nxt;
     cur.tbase = nxt.tbase = t_first;
-    if (kStatic) cur.claim_static(snext, sstride);
-    else cur.claim(E.met);
-    cur.finish(E, ntasks);
+    uint32_t tph = 0;
+    auto pop = [&](PTask& x) {  // the fetcher's next ticket
+      if (lane == 0) mbar_wait(&tk_full, tph);
+      __syncwarp();
+      x = tk_box;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tk_empty);
+      tph ^= 1;
+      // the fetcher's acquire of the children's counters, made this warp's
+      // (the ticket's mbarrier hand-off orders it; the fence extends it GPU-wide)
+      fence_acquire_gpu();
+    };
+    if (kFetchers) pop(cur);
+    else {
+      if (kStatic) cur.claim_static(snext, sstride);
+      else cur.claim(E.met);
+      cur.finish(E, ntasks);
+    }
     while (cur.valid) {
       RS_T0(tw);
       if (!cur.ready(E.done)) {
@@ -374,7 +427,7 @@ __global__ void __launch_bounds__(kMergeThreads, RS_MERGE_CTAS) k_merge_exec(Mer
         } while (!cur.ready(E.done));
       }
       if (lane == 0) RS_ACC(E.met, 5, tw);
-      if (ahead) {
+      if (ahead && !kFetchers) {
         if (kStatic) nxt.claim_static(snext, sstride);
         else nxt.claim(E.met);
       }
@@ -410,9 +463,9 @@ __global__ void __launch_bounds__(kMergeThreads, RS_MERGE_CTAS) k_merge_exec(Mer
       bool trivial = diag == 0 || diag == tot;
       int64_t split = group_merge_path(srcA + s, na, srcB + m, nb, diag, in_range && !trivial, G,
                                        [&]() {
-                                         if (ahead) nxt.advance(E, ntasks);
+                                         if (ahead && !kFetchers) nxt.advance(E, ntasks);
                                        });
-      if (ahead) nxt.finish(E, ntasks);
+      if (ahead && !kFetchers) nxt.finish(E, ntasks);
       if (diag == 0) split = 0;
       else if (diag == tot) split = na;
       if (lane == 0) RS_ACC(E.met, 1, tsrch);
@@ -421,7 +474,7 @@ __global__ void __launch_bounds__(kMergeThreads, RS_MERGE_CTAS) k_merge_exec(Mer
 #define RS_CLAIM_EARLY 0  // 1: measured 1-2 us slower (a task claimed during the issue is held)
 #endif
       // just in time, but the claim's atomic round trip overlaps this task's issue
-      if (!ahead && RS_CLAIM_EARLY) nxt.claim(E.met);
+      if (!ahead && !kFetchers && RS_CLAIM_EARLY) nxt.claim(E.met);
       bool merged = true;  // the reference performs this merge (Metrics)
       if (E.skipchk && kbeg == 0) {
         // sorters.py:545-550 / 575-578: one comparison; an in-order pair is not
@@ -525,7 +578,8 @@ __global__ void __launch_bounds__(kMergeThreads, RS_MERGE_CTAS) k_merge_exec(Mer
         }
       }
       if (lane == 0) RS_ACC(E.met, 7, tiss);
-      if (!ahead) {  // just in time: no task held ahead
+      if (kFetchers) pop(nxt);
+      else if (!ahead) {  // just in time: no task held ahead
         if (!RS_CLAIM_EARLY) nxt.claim(E.met);
         nxt.finish(E, ntasks);
       }
@@ -632,7 +686,7 @@ __global__ void __launch_bounds__(kMergeThreads, RS_MERGE_CTAS) k_merge_exec(Mer
   }
 
   // --------------------------------------------------------------- consumers
-  int ct = threadIdx.x - 32 * (kProducers + 1);
+  int ct = threadIdx.x - 32 * kRoleWarps;
   int cl = ct & 31;
   int stage = 0;
   uint32_t phase = 0;
