@@ -125,6 +125,8 @@ class _Staged:
         self.obj = obj
         self.flip = None
         self.host_out = None
+        self.zero_signs = None
+        self.orig_dtype = None
         if isinstance(obj, torch.Tensor):
             self.is_torch = True
             if obj.dim() != 1:
@@ -168,8 +170,47 @@ class _Staged:
             return "flip32", _lib.RS_KEY_I32
         if npdt == np.dtype(np.uint64):
             return "flip64", _lib.RS_KEY_I64
+        if npdt in (np.dtype(np.float16), np.dtype(np.float32)):
+            return "float32", _lib.RS_KEY_I32
+        if npdt == np.dtype(np.float64):
+            return "float64", _lib.RS_KEY_I64
         raise NotImplementedError(f"keys of dtype {npdt} are not supported on the device path "
-                                  "(integers only)")
+                                  "(integers and floats only)")
+
+    # Floating-point keys sort as the order-preserving integers of their bit
+    # patterns (i ^ ((i >> 63) & 0x7f..f): negative values reversed below the
+    # non-negative ones), which compare exactly like the reference's float
+    # comparisons (sorters.py / runcore.py use <= and <) for every pair except
+    # -0.0 vs +0.0, equal as floats: both zeros map to key 0, so the stable
+    # sort keeps all zeros in their input order, and the output's zero block
+    # gets back the input zeros' signs in that same order.  NaN keys, which
+    # the reference's comparisons do not order, are rejected.
+    def _float_to_key(self, d):
+        torch = _torch()
+        if self.kind == "float32" and d.dtype != torch.float32:
+            self.orig_dtype = d.dtype
+            d = d.to(torch.float32)
+        if bool(torch.isnan(d).any().item()):
+            raise NotImplementedError("NaN keys are not supported: the reference's comparisons do not order them")
+        zero = d == 0
+        self.zero_signs = torch.signbit(d[zero]) if bool(zero.any().item()) else None
+        it, bits, mask = (torch.int32, 31, 0x7fffffff) if self.kind == "float32" else \
+            (torch.int64, 63, 0x7fffffffffffffff)
+        i = torch.where(zero, torch.zeros_like(d), d).view(it)
+        return i ^ ((i >> bits) & mask)
+
+    def _key_to_float(self, k):
+        torch = _torch()
+        it, ft, bits, mask = (torch.int32, torch.float32, 31, 0x7fffffff) if self.kind == "float32" else \
+            (torch.int64, torch.float64, 63, 0x7fffffffffffffff)
+        f = (k ^ ((k >> bits) & mask)).view(ft)
+        if self.zero_signs is not None:
+            zs = self.zero_signs
+            f = f.clone()
+            f[f == 0] = torch.where(zs, torch.full_like(zs, -0.0, dtype=ft), torch.full_like(zs, 0.0, dtype=ft))
+        if getattr(self, "orig_dtype", None) is not None:
+            f = f.to(self.orig_dtype)
+        return f
 
     def _to_work(self, d):
         torch = _torch()
@@ -188,6 +229,8 @@ class _Staged:
             return d.view(torch.int32) ^ torch.tensor(-(1 << 31), dtype=torch.int32, device=d.device)
         if self.kind == "flip64":
             return d.view(torch.int64) ^ torch.tensor(-(1 << 63), dtype=torch.int64, device=d.device)
+        if self.kind in ("float32", "float64"):
+            return self._float_to_key(d)
         raise AssertionError(self.kind)
 
     def _result(self):
@@ -199,6 +242,8 @@ class _Staged:
             d = (d ^ torch.tensor(-(1 << 31), dtype=torch.int32, device=d.device)).view(torch.uint32)
         elif self.kind == "flip64":
             d = (d ^ torch.tensor(-(1 << 63), dtype=torch.int64, device=d.device)).view(torch.uint64)
+        elif self.kind in ("float32", "float64"):
+            d = self._key_to_float(d)
         return d
 
     def finish_device(self):

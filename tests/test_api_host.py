@@ -77,7 +77,9 @@ def test_unsupported_key_dtype_is_loud():
     torch = pytest.importorskip("torch")
     if torch.cuda.is_available():
         with pytest.raises(NotImplementedError):
-            rs.powersort(np.array([1.5, 0.5]))
+            rs.powersort(np.array([1.5, np.nan]))  # NaN keys: no order to follow
+        with pytest.raises(NotImplementedError):
+            rs.powersort(np.array(["b", "a"]))
     else:
         with pytest.raises(RuntimeError):
             rs.powersort(np.array([3, 1, 2], dtype=np.int64))
