@@ -686,6 +686,9 @@ struct Exec {
     const int64_t la = f.la, lb = f.lb;
     const pos_t s = f.s, e = f.e;
     const int droot = f.droot;
+#ifdef RS_INSTR
+    long long ti0 = clock64(), ti1 = 0, ti2 = 0, ti3 = 0;
+#endif
     int len = int(e - s);
     RS_CHECK(0 < len && len <= C::FCAP && lb >= la && lb - la <= E.maxb - 2, "fuse task s %lld e %lld la %lld lb %lld",
              (long long)s, (long long)e, (long long)la, (long long)lb);
@@ -732,6 +735,9 @@ struct Exec {
     X[1] = reinterpret_cast<K*>(kbuf(smem, ib ^ 1));
     Y[0] = HAS_TAGS ? reinterpret_cast<T*>(tbuf(smem, ib)) + off[1] : nullptr;
     Y[1] = HAS_TAGS ? reinterpret_cast<T*>(tbuf(smem, ib ^ 1)) : nullptr;
+#ifdef RS_INSTR
+    ti1 = clock64();
+#endif
     __builtin_assume(__isShared(X[0]));
     __builtin_assume(__isShared(X[1]));
     if (HAS_TAGS) {
@@ -835,6 +841,9 @@ struct Exec {
     }
     if (threadIdx.x == 0) step();
     __syncthreads();
+#ifdef RS_INSTR
+    ti2 = clock64();
+#endif
     if (nbd > 0) {
       int dmax = s_dmax;
       const int per = (nbd + blockDim.x - 1) / blockDim.x;
@@ -872,7 +881,10 @@ struct Exec {
           __builtin_assume(__isShared(Yd));
         }
         // every thread merges one equal share of the level's concatenated output
-        const int cs = (tot + (int)blockDim.x - 1) / (int)blockDim.x;
+        // odd shares: thread t starts at output t * cs, so the merge's reads and
+        // writes of neighbouring threads fall in different banks (an even share,
+        // 16 for a 4096-element span, made them 16-way conflicted)
+        const int cs = ((tot + (int)blockDim.x - 1) / (int)blockDim.x) | 1;
         int o0 = threadIdx.x * cs;
         const int o1 = o0 + cs < tot ? o0 + cs : tot;
         if (o0 < o1) {
@@ -910,6 +922,19 @@ struct Exec {
         __syncthreads();
       }
     }
+#ifdef RS_INSTR
+    ti3 = clock64();
+    if (threadIdx.x == 0) {  // sub-phases of the slowest fused task: tables+span, leaves, levels (cycles)
+      unsigned long long tot = (unsigned long long)(ti3 - ti0);
+      if (tot > E.met->peek[0]) {
+        E.met->peek[0] = tot;
+        E.met->peek[1] = (unsigned long long)(ti1 - ti0);
+        E.met->peek[2] = (unsigned long long)(ti2 - ti1);
+        E.met->peek[3] = (unsigned long long)(ti3 - ti2);
+        E.met->peek[4] = (unsigned long long)(s_dmax - droot + 1);
+      }
+    }
+#endif
     hook();  // result in X[droot & 1]; the other buffer is free
     K* gd = reinterpret_cast<K*>(E.key[item_buf(droot)]);  // in place unless depth 1
     T* hd = HAS_TAGS ? reinterpret_cast<T*>(E.tag[item_buf(droot)]) : nullptr;
@@ -981,6 +1006,9 @@ __global__ void __launch_bounds__(kExecThreads, 3) k_phaseA(ExecArgs E) {
       break;
     }
     uint32_t kind = task_kind(rec), id = task_id(rec), tile = task_tile(rec);
+#ifdef RS_INSTR
+    const long long t_task0 = clock64();
+#endif
     __syncthreads();  // everyone has read the shared slots
     if (threadIdx.x == 0) {
       nst = 0;
@@ -1013,6 +1041,21 @@ __global__ void __launch_bounds__(kExecThreads, 3) k_phaseA(ExecArgs E) {
     }
     __syncthreads();
     if (threadIdx.x == 0) release_add_u32(E.done + id, 1u);
+#ifdef RS_INSTR
+    if (threadIdx.x == 0) {  // phase-A task durations: max, sum, count, and the max task's size
+      unsigned long long dur = (unsigned long long)(clock64() - t_task0);
+      atomicMax(&E.met->prep_dbg[25], dur);
+      atomicAdd(&E.met->prep_dbg[26], dur);
+      atomicAdd(&E.met->prep_dbg[27], 1ull);
+      if (kind != kTaskLeaf) {
+        Span f = X::span_of(E, id);
+        atomicMax(&E.met->prep_dbg[28], (dur << 24) | (unsigned long long)(f.e - f.s));
+        atomicMax(&E.met->prep_dbg[29], (dur << 24) | (unsigned long long)(f.lb - f.la));
+      }
+      atomicMax(&E.met->prep_dbg[30], (dur << 24) | (unsigned long long)kind);
+      atomicMax(&E.met->prep_dbg[31], (unsigned long long)clock64());  // latest end (SM clock, rough)
+    }
+#endif
   }
   unsigned long long sum = block_sum(comps, sred);
   if (threadIdx.x == 0 && sum) atomicAdd(&E.met->comparisons, sum);

@@ -1524,6 +1524,7 @@ int rs_debug_counters(int key_dtype, int tag_bytes, int64_t n, int32_t min_run_l
   for (int d = 0; d < 16 && k < cap; ++d) out[k++] = hm.prep_ts[d];
   for (int d = 0; d < 16 && k < cap; ++d) out[k++] = hm.prep_arr[d];
   for (int d = 0; d < 32 && k < cap; ++d) out[k++] = hm.prep_dbg[d];
+  for (int d = 0; d < 8 && k < cap; ++d) out[k++] = hm.peek[d];
   return k;
 }
 

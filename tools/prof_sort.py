@@ -32,8 +32,8 @@ for i in range(a.reps):
 torch.cuda.synchronize()
 print('ok', m.merge_cost, m.runs_detected)
 if __import__('os').environ.get('RS_LIB'):
-    buf = (ctypes.c_uint64 * 202)()
-    k = L.rs_debug_counters(kc, tb, n, a.w, ws.data_ptr(), buf, 202)
+    buf = (ctypes.c_uint64 * 210)()
+    k = L.rs_debug_counters(kc, tb, n, a.w, ws.data_ptr(), buf, 210)
     ts = list(buf[138:154]); print('prep phase us', [round((ts[i] - ts[i-1]) / 1e3, 1) for i in range(1, 12) if ts[i] and ts[i-1]])
     arr = list(buf[154:170]); print('phase work (latest arrival - prev exit) / barrier (exit - latest arrival) us', [(i, round((arr[i] - ts[i-1]) / 1e3, 1), round((ts[i] - arr[i]) / 1e3, 1)) for i in range(1, 10) if arr[i] and ts[i] and ts[i-1]])
     dbg = list(buf[170:202]); t4 = min([x for x in dbg if x] or [0]); print('dbg us after first dbg', [(i, round((dbg[i] - t4) / 1e3, 1)) for i in range(32) if dbg[i]])
@@ -43,3 +43,8 @@ if __import__('os').environ.get('RS_LIB'):
     print('depth: wait_cycles(M) tasks', [(d, round(dw[d] / 1e6, 1), dt[d]) for d in range(64) if dt[d]])
     names = ['prod_dep_wait', 'prod_search', 'prod_stage_wait', 'cons_full_wait', 'cons_tile_work', 'prod_ready', 'prod_pfence', 'prod_issue', 'n_tasks', 'phaseA']
     print({nm: buf[i] for i, nm in enumerate(names[:k])})
+    dur_max, dur_sum, ntask = buf[170 + 25], buf[170 + 26], buf[170 + 27]
+    if ntask:
+        print('phaseA tasks', ntask, 'max cycles', dur_max, 'mean', dur_sum // ntask,
+              'max-task span', buf[170 + 28] & 0xffffff, 'leaves-1', buf[170 + 29] & 0xffffff, 'kind', buf[170 + 30] & 0xffffff)
+    print('slowest fused task: total/tables+span/leaves/levels cycles, levels:', list(buf[202:207]) if len(buf) > 206 else 'n/a')
