@@ -124,6 +124,7 @@ def test_config5_full_size_bit_exact():
     import paper_1805_04154_b200 as rs
     from paper_1805_04154_b200 import workloads
 
+    torch.cuda.empty_cache()
     free, _ = torch.cuda.mem_get_info()
     if free < 120 * (1 << 30):
         pytest.skip("needs ~120 GB of free device memory")
@@ -132,6 +133,36 @@ def test_config5_full_size_bit_exact():
     a = workloads.config5_device(n, seed=1)
     res = _analytic_from_device(a)
     assert res["runs_detected"] > 30000
+    ref = _reference_sorted(a)
+    m = rs.powersort(a, rs.SortConfig(record_tree=True))
+    torch.cuda.synchronize()
+    assert torch.equal(a, ref)
+    del ref
+    _check_against(a, res, m)
+
+
+@pytest.mark.slow
+def test_above_2_31_int32_bit_exact():
+    """n = 2^31 + 3*2^20 + 7 int32 keys: above 2^31 the device's node powers
+    take the 63-bit midpoint-key path (128-bit division) and 64-bit positions
+    with 32-bit keys; the reference takes node_power_def (sorters.py:416-423).
+    Output vs torch's sort, all Metrics and every node power vs the analytic
+    oracle, as for config 5."""
+    import torch
+
+    import paper_1805_04154_b200 as rs
+    from paper_1805_04154_b200 import workloads
+
+    torch.cuda.empty_cache()  # blocks cached by the tests before
+    free, _ = torch.cuda.mem_get_info()
+    if free < 110 * (1 << 30):
+        pytest.skip("needs ~110 GB of free device memory")
+    n = (1 << 31) + 3 * (1 << 20) + 7
+    a64 = workloads.config5_device(n, seed=5, mean=float(1 << 15))
+    a = (a64 >> 33).to(torch.int32)  # monotone: the sorted segments stay sorted, with many ties
+    del a64
+    torch.cuda.empty_cache()
+    res = _analytic_from_device(a)
     ref = _reference_sorted(a)
     m = rs.powersort(a, rs.SortConfig(record_tree=True))
     torch.cuda.synchronize()
