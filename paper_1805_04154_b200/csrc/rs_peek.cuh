@@ -591,6 +591,9 @@ __global__ void __launch_bounds__(256, 2) k_peek(PeekArgs P) {
     ++lev;
   }
   grid.sync();
+#ifdef RS_INSTR
+  if (gtid == 0) met->prep_arr[15] = (unsigned long long)lev;  // replay levels
+#endif
   if (blockIdx.x == 0) RS_DBG(met, 3);
   // 3. leaf-start bitmap and its word prefix popcount
   unsigned long long R = pc->n_leaves;

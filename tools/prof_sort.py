@@ -48,3 +48,5 @@ if __import__('os').environ.get('RS_LIB'):
         print('phaseA tasks', ntask, 'max cycles', dur_max, 'mean', dur_sum // ntask,
               'max-task span', buf[170 + 28] & 0xffffff, 'leaves-1', buf[170 + 29] & 0xffffff, 'kind', buf[170 + 30] & 0xffffff)
     print('slowest fused task: total/tables+span/leaves/levels cycles, levels:', list(buf[202:207]) if len(buf) > 206 else 'n/a')
+    if a.algo == 1:
+        print('peeksort replay levels', buf[154 + 15])
