@@ -208,6 +208,15 @@ const char* rs_last_error(void);
 /* ABI version (major * 100 + minor). */
 int rs_version(void);
 
+/* W sorted runs stored back to back in keys[0, n) (and tags) merged in place
+ * into one sorted run, stable (ties to the earlier run): the executor along a
+ * balanced binary tree.  run_starts: host, nruns + 1 positions from 0 to n.
+ * Used by the NCCL plane of the sharded sort for the runs it received
+ * (replaces a W-way merge pass; reference order: runcore.py:262-263 left-wins). */
+size_t rs_merge_runs_workspace_bytes(int key_dtype, int tag_bytes, int64_t n, int nruns);
+int rs_merge_runs(int key_dtype, void* keys, int tag_bytes, void* tags, int64_t n, const int64_t* run_starts,
+                  int nruns, void* workspace, size_t ws_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -22,6 +22,7 @@ RS_EIO = 6
 EXPORTS = ("rs_workspace_bytes", "rs_sort", "rs_sort_ex", "rs_fetch_metrics", "rs_sort_host", "rs_sort_host_ex", "rs_export_tree", "rs_profile",
            "rs_profile_read", "rs_debug_counters", "rs_max_min_run_len", "rs_load_bin", "rs_corank", "rs_kway_workspace_bytes", "rs_kway_merge",
            "rs_corank_rank", "rs_kway_split_workspace_bytes", "rs_kway_merge_split",
+           "rs_merge_runs_workspace_bytes", "rs_merge_runs",
            "rs_ipc_alloc", "rs_ipc_open", "rs_ipc_close", "rs_ipc_free", "rs_last_error",
            "rs_version")
 
@@ -103,6 +104,12 @@ def lib():
                                      ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]
         L.rs_kway_split_workspace_bytes.restype = ctypes.c_size_t
         L.rs_kway_split_workspace_bytes.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int64]
+        L.rs_merge_runs_workspace_bytes.restype = ctypes.c_size_t
+        L.rs_merge_runs_workspace_bytes.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_int]
+        L.rs_merge_runs.restype = ctypes.c_int
+        L.rs_merge_runs.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_int64,
+                                    ctypes.POINTER(ctypes.c_int64), ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t,
+                                    ctypes.c_void_p]
         L.rs_kway_merge_split.restype = ctypes.c_int
         L.rs_kway_merge_split.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.POINTER(RsShard), ctypes.c_int,
                                           ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,

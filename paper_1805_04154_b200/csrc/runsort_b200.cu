@@ -1018,6 +1018,52 @@ int export_tree(const Layout& L, unsigned char* ws, cudaStream_t st, rs_tree* tr
   return RS_OK;
 }
 
+// ------------------------------------------------ sorted runs -> one run
+// W sorted runs laid out back to back in one buffer merged in place by the
+// executor along a balanced binary tree (log2 W passes of the tuned merge,
+// ties to the earlier run).  The NCCL plane of the sharded sort merges its
+// received runs this way (dist.py); the runs are natural leaves, so phase A
+// has nothing to do except copying depth-1 leaves (W = 2).
+int merge_runs_w(int64_t n, int nruns, int kb, int tb) {
+  int64_t w = n / (2 * (int64_t)(nruns > 0 ? nruns : 1));
+  int64_t cap = exec_fcap(kb, tb);
+  if (w > cap) w = cap;
+  if (w < 2) w = 2;
+  return (int)w;
+}
+
+template <typename K, int TB>
+int run_merge_runs(K* keys, void* tags, int64_t n, const std::vector<int64_t>& starts, unsigned char* ws,
+                   const Layout& L, cudaStream_t st) {
+  int sms;
+  if (int e = device_sms(&sms)) return e;
+  WsView V = view(ws, L);
+  const int64_t R = (int64_t)starts.size() - 1;
+  if (R > L.r_max) return fail(RS_EINVARIANT, "more runs than the layout holds");
+  HostTree H;
+  H.leaf_base = L.leaf_base;
+  H.init(R, L.leaf_base);
+  H.start = starts;
+  std::vector<uint32_t> cur(R);
+  for (int64_t k = 0; k < R; ++k) cur[k] = L.leaf_base + (uint32_t)k;
+  while (cur.size() > 1) {
+    std::vector<uint32_t> nxt;
+    for (size_t k = 0; k + 1 < cur.size(); k += 2) nxt.push_back(H.join(cur[k], cur[k + 1]));
+    if (cur.size() & 1) nxt.push_back(cur.back());
+    cur.swap(nxt);
+  }
+  RS_CUDA(cudaMemsetAsync(V.met, 0, sizeof(DevMetrics), st));
+  RS_CUDA(cudaMemsetAsync(V.done, 0, (2 * L.r_max + 2) * sizeof(uint32_t), st));
+  int64_t nch_max = (L.r_max + kOrdChunkMin - 1) / kOrdChunkMin;
+  RS_CUDA(cudaMemsetAsync(V.chunkdep, 0, (nch_max + 1) * kMaxDepth * sizeof(uint32_t), st));
+  uint64_t r64 = (uint64_t)R;
+  RS_CUDA(cudaMemcpyAsync(&V.met->n_leaves, &r64, 8, cudaMemcpyHostToDevice, st));
+  std::vector<uint32_t> info(R);
+  for (int64_t k = 0; k < R; ++k) info[k] = (uint32_t)std::min<int64_t>(starts[k + 1] - starts[k], L.w);  // natural
+  if (int e = upload_tree(H, V, L, st, true, &info)) return e;
+  return exec_tree<K, TB>(keys, tags, n, L.w, 0, 1, 0, V, L, sms, st);
+}
+
 template <typename K>
 int dispatch_tags(int algo, K* keys, int tb, void* tags, int64_t n, int w, int classic, double alpha,
                   unsigned char* ws, const Layout& L, cudaStream_t st) {
@@ -1384,6 +1430,47 @@ int rs_sort_ex(int algo, int key_dtype, void* keys, int tag_bytes, void* tags, i
     if (tree && (e = export_tree(L, ws, st, tree))) return e;
   }
   return RS_OK;
+}
+
+size_t rs_merge_runs_workspace_bytes(int key_dtype, int tag_bytes, int64_t n, int nruns) {
+  int kb = key_dtype == RS_KEY_I64 ? 8 : 4;
+  if (n <= 1 || nruns <= 1) return 256;
+  return make_layout(n, merge_runs_w(n, nruns, kb, tag_bytes), kb, tag_bytes, RS_ALGO_BOTTOM_UP).total;
+}
+
+int rs_merge_runs(int key_dtype, void* keys, int tag_bytes, void* tags, int64_t n, const int64_t* run_starts,
+                  int nruns, void* workspace, size_t ws_bytes, void* stream) {
+  if (key_dtype != RS_KEY_I32 && key_dtype != RS_KEY_I64) return fail(RS_EUNSUPPORTED, "keys must be int32 or int64");
+  if (tag_bytes != 0 && tag_bytes != 4 && tag_bytes != 8) return fail(RS_EUNSUPPORTED, "tags must be 4 or 8 bytes wide");
+  if (tags == nullptr) tag_bytes = 0;
+  if (nruns < 0 || (nruns > 0 && !run_starts)) return fail(RS_EINVAL, "null run starts");
+  if (n < 0) return fail(RS_EINVAL, "n must be >= 0");
+  std::vector<int64_t> starts;  // non-empty runs only
+  for (int k = 0; k < nruns; ++k) {
+    if (run_starts[k] < 0 || run_starts[k + 1] < run_starts[k] || run_starts[k + 1] > n)
+      return fail(RS_EINVAL, "run starts must be non-decreasing within [0, n]");
+    if (run_starts[k + 1] > run_starts[k]) starts.push_back(run_starts[k]);
+  }
+  if (nruns > 0 && (run_starts[0] != 0 || run_starts[nruns] != n)) return fail(RS_EINVAL, "the runs must cover [0, n)");
+  if (starts.size() <= 1) return RS_OK;  // already one run
+  starts.push_back(n);
+  if (!keys || !workspace) return fail(RS_EINVAL, "null keys or workspace");
+  const int kb = key_dtype == RS_KEY_I64 ? 8 : 4;
+  // the layout as rs_merge_runs_workspace_bytes sized it (nruns, empty runs included)
+  Layout L = make_layout(n, merge_runs_w(n, nruns, kb, tag_bytes), kb, tag_bytes, RS_ALGO_BOTTOM_UP);
+  if (ws_bytes < L.total) return fail(RS_ENOMEM, "workspace too small");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  unsigned char* ws = reinterpret_cast<unsigned char*>(workspace);
+  if (kb == 4) {
+    int32_t* k = reinterpret_cast<int32_t*>(keys);
+    if (tag_bytes == 0) return run_merge_runs<int32_t, 0>(k, nullptr, n, starts, ws, L, st);
+    if (tag_bytes == 4) return run_merge_runs<int32_t, 4>(k, tags, n, starts, ws, L, st);
+    return run_merge_runs<int32_t, 8>(k, tags, n, starts, ws, L, st);
+  }
+  int64_t* k = reinterpret_cast<int64_t*>(keys);
+  if (tag_bytes == 0) return run_merge_runs<int64_t, 0>(k, nullptr, n, starts, ws, L, st);
+  if (tag_bytes == 4) return run_merge_runs<int64_t, 4>(k, tags, n, starts, ws, L, st);
+  return run_merge_runs<int64_t, 8>(k, tags, n, starts, ws, L, st);
 }
 
 int rs_fetch_metrics(int algo, int key_dtype, int tag_bytes, int64_t n, int32_t min_run_len, void* workspace,

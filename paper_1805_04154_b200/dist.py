@@ -211,19 +211,15 @@ def _default_local_sort(keys, tags):
 
 
 def _device_merge(out, tout, recv):
-    """Stable W-way merge of the received runs (rank order) on the device."""
-    import torch
-
+    """Stable merge of the received runs (rank order), in place on the device:
+    they are contiguous in the receive buffer, so the powersort executor merges
+    them along a balanced binary tree (rs_merge_runs; log2 W passes of the
+    tuned two-way merge, which outruns one W-way pass of the k-way kernel for
+    W > 2 on one GPU)."""
     from . import kway
 
-    shards, off = [], 0
-    for c in recv:
-        shards.append(kway.Shard(out.data_ptr(), tout.data_ptr() if tout is not None else None, off, off + c))
-        off += c
-    mk = torch.empty_like(out)
-    mt = torch.empty_like(tout) if tout is not None else None
-    kway.kway_merge(shards, mk, mt)
-    return mk, mt
+    kway.merge_runs(out, tout, [int(c) for c in recv])
+    return out, tout
 
 
 def sharded_sort(keys, tags=None, group=None, local_sort: Optional[Callable] = None,

@@ -134,6 +134,29 @@ def kway_merge_split(shards: Sequence[Shard], dsplit, out_len: int, out_keys, ou
     return workspace
 
 
+def merge_runs(keys, tags, run_lengths: Sequence[int], stream=None, workspace=None):
+    """Merge the sorted runs stored back to back in `keys` (and `tags`) in place
+    into one sorted run, ties to the earlier run (rs_merge_runs: the executor
+    along a balanced binary tree, log2 W passes); async.  Returns the workspace."""
+    torch = _torch()
+    L = _lib.lib()
+    n = int(keys.numel())
+    starts = np.concatenate([[0], np.cumsum(np.asarray(run_lengths, dtype=np.int64))]).astype(np.int64)
+    if int(starts[-1]) != n:
+        raise ValueError("run lengths must add up to the array length")
+    W = len(run_lengths)
+    tb = tags.element_size() if tags is not None else 0
+    kc = key_code(keys.dtype)
+    need = L.rs_merge_runs_workspace_bytes(kc, tb, n, W)
+    if workspace is None or workspace.numel() < need:
+        workspace = torch.empty(max(need, 256), dtype=torch.uint8, device=keys.device)
+    st = stream or torch.cuda.current_stream(keys.device)
+    _lib.check(L.rs_merge_runs(kc, keys.data_ptr(), tb, tags.data_ptr() if tags is not None else None, n,
+                               starts.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), W, workspace.data_ptr(),
+                               workspace.numel(), st.cuda_stream))
+    return workspace
+
+
 # ------------------------------------------------------------------ IPC ----
 class _CAI:
     def __init__(self, ptr: int, n: int, itemsize: int):

@@ -136,3 +136,29 @@ def test_rejects_bad_shards():
         kway.corank([kway.Shard.of(d)], [11], torch.int64)
     with pytest.raises(ValueError):
         kway.kway_merge([kway.Shard.of(d)] * 9, d)
+
+
+@pytest.mark.parametrize("W", [2, 3, 5, 8])
+def test_merge_runs_in_place_matches_stable_sort(W):
+    """rs_merge_runs: W sorted runs back to back merged in place (the NCCL
+    plane's merge of its received runs), ties to the earlier run; empty runs,
+    heavy ties, int32 / int64 keys, no / 4- / 8-byte tags."""
+    import torch
+
+    from paper_1805_04154_b200 import kway
+
+    rng = np.random.default_rng(7 * W)
+    dev = torch.device("cuda", 0)
+    for dtype, tdt, big in ((np.int32, None, False), (np.int64, np.int64, False), (np.int32, np.int32, True)):
+        lens = [int(rng.choice([0, 1, 5, 3000, int(rng.integers(0, 400000 if big else 60000))])) for _ in range(W)]
+        runs = [np.sort(rng.integers(0, 50, size=L).astype(dtype), kind="stable") for L in lens]
+        k = np.concatenate(runs) if sum(lens) else np.zeros(0, dtype=dtype)
+        t = np.arange(len(k)).astype(tdt) if tdt is not None else None
+        order = np.argsort(k, kind="stable")
+        dk = torch.from_numpy(k.copy()).to(dev)
+        dt = torch.from_numpy(t.copy()).to(dev) if t is not None else None
+        kway.merge_runs(dk, dt, lens)
+        torch.cuda.synchronize()
+        assert np.array_equal(dk.cpu().numpy(), k[order]), (W, dtype, lens)
+        if t is not None:
+            assert np.array_equal(dt.cpu().numpy(), t[order]), (W, dtype, lens)

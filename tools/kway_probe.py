@@ -41,5 +41,27 @@ for n, kdt, tdt in ((10**7, torch.int32, None), (10**8, torch.int32, torch.int64
         ms = sum(ts) / len(ts)
         ok = bool(torch.all(out[1:] >= out[:-1]).item())
         print(f"n={n} B={B} W={W} ms={ms:.4f} GB/s={2 * n * B / ms / 1e6:.0f} sorted={ok}", flush=True)
+        # the same runs merged in place by the executor along a binary tree (rs_merge_runs)
+        lens = [bounds[i + 1] - bounds[i] for i in range(W)]
+        ts2 = []
+        wsr = None
+        for rep in range(6):
+            kk = keys.clone()
+            tt = tags.clone() if tags is not None else None
+            flush.fill_(1)
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            wsr = kway.merge_runs(kk, tt, lens, workspace=wsr)
+            e1.record()
+            torch.cuda.synchronize()
+            if rep >= 2:
+                ts2.append(e0.elapsed_time(e1))
+        ms2 = sum(ts2) / len(ts2)
+        ok2 = bool(torch.equal(kk, out))
+        print(f"   merge_runs (binary tree, in place) ms={ms2:.4f} GB/s(one-pass equiv)={2 * n * B / ms2 / 1e6:.0f} "
+              f"same={ok2}", flush=True)
+        del kk, tt, wsr
         del keys, tags, out, tout, ws
         torch.cuda.empty_cache()
