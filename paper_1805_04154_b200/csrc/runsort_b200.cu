@@ -134,15 +134,15 @@ size_t prep_smem_bytes(int w, int kb, int ct) {
 
 // Positions per chain tile (k_prep is instantiated for 1024, 2048 and 2560):
 // below ~7M keys 2048-position tiles leave most prep warps without a tile and
-// 1024 is faster (cfg1, n = 2^20: -9%); from ~12M keys 2560 balances the
-// warps' tile counts better.  A function of n only, so every layout agrees.
+// 1024 is faster (cfg1, n = 2^20: -9%); above that 2560 (fewer tiles for
+// the group/emit phases; 2048 remains the shared-memory fallback).  A function of n only, so every layout agrees.
 // Large min_run_len values step the tile down until the prep's per-warp
 // windows fit in shared memory (a function of (n, w, key bytes) only).
 inline int chain_tile_for(int64_t n, int w, int kb) {
   int ct;
   if (int v = tun().chain_tile) ct = v >= 2560 ? 2560 : (v >= 2048 ? 2048 : 1024);  // tuning override
   else if (n < (int64_t)2048 * 3552) ct = 1024;
-  else ct = n < (int64_t)12000000 ? 2048 : 2560;  // 2560 from ~12M keys: cfg3 -4 us, cfg4 -30 us (cfg2 even)
+  else ct = 2560;  // round 2: cfg2 (1e7) -2.8 us vs 2048 (3 repeats), cfg3 -4 us, cfg4 -30 us
   while (ct > 1024 && prep_smem_bytes(w, kb, ct) > kMaxSmemPerBlock) ct = ct == 2560 ? 2048 : 1024;
   return ct;
 }
