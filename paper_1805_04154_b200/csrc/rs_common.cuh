@@ -110,6 +110,7 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 #ifdef RS_INSTR
 #define RS_TS(met, i) do { if (blockIdx.x == 0 && threadIdx.x == 0) (met)->prep_ts[i] = globaltimer_ns(); } while (0)
 #define RS_DBG(met, i) do { if (threadIdx.x == 0) atomicMax(&(met)->prep_dbg[i], globaltimer_ns()); } while (0)
+#define RS_TSD(met, i) do { if (threadIdx.x == 0) (met)->prep_dbg[i] = globaltimer_ns(); } while (0)
 #define RS_ARR(met, i) do { __syncthreads(); if (threadIdx.x == 0) atomicMax(&(met)->prep_arr[i], globaltimer_ns()); } while (0)
 #define RS_T0(v) long long v = clock64()
 #define RS_ACC(met, i, v) atomicAdd(&(met)->instr[i], (unsigned long long)(clock64() - (v)))
@@ -117,6 +118,7 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 #define RS_TS(met, i)
 #define RS_ARR(met, i)
 #define RS_DBG(met, i)
+#define RS_TSD(met, i)
 #define RS_T0(v)
 #define RS_ACC(met, i, v)
 #endif

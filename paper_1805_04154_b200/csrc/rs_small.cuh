@@ -37,9 +37,10 @@ constexpr int kJobCap = 2 * kSmallR + 2;  // <= one job per leaf and one per bou
 // 32-bit shared-memory arrays (positions and midpoint keys fit: n < 2^31, F = 32)
 __host__ __device__ constexpr size_t small_arrays_bytes() {
   return (size_t)(kSmallR + 1) * 4      // Ls: leaf starts
-         + (size_t)kSmallR * 4          // Ks: midpoint keys, later node spans | no-fuse bit 31
+         + (size_t)kSmallR * 4 * 4      // Ks: midpoint keys; spans | no-fuse bit 31; phase-A / merge task counts
          + (size_t)2 * kSmallR * 2      // par: parents of leaves [0, r) and nodes [r, 2r)
-         + (size_t)(kSmallR + 1) * 5;   // Ps, las, ras, dep, ldep
+         + (size_t)(kSmallR + 1) * 5    // Ps, las, ras, dep, ldep
+         + (size_t)kSmallR * 2;         // leaf / node classes
 }
 __host__ __device__ constexpr size_t small_smem_bytes() {
   return small_arrays_bytes() > (size_t)kJobCap * 4 ? small_arrays_bytes() : (size_t)kJobCap * 4;
@@ -104,13 +105,20 @@ __device__ void small_tree(const TreeArrays& T, ClassifyArgs A, unsigned char* s
   RS_TS(met, 5);
   uint32_t* Ls = reinterpret_cast<uint32_t*>(smem_small);
   uint32_t* Ks = Ls + kSmallR + 1;
-  uint32_t* spans = Ks;  // after the trie ranges: span | kNoFuse (bit 31)
-  int16_t* par = reinterpret_cast<int16_t*>(Ks + kSmallR);
+  // per-item state lives in shared memory, indexed by item: local arrays
+  // indexed by a rolled loop spill to local memory, whose loads missed L1
+  // (measured: 14.6 us for config 3's 50-leaf per-depth loop)
+  uint32_t* spans = Ks + kSmallR;     // node span | kNoFuse (bit 31)
+  uint32_t* s_aof = spans + kSmallR;  // phase-A tasks of item i (its leaf, its fused node)
+  uint32_t* s_tk = s_aof + kSmallR;   // merge tasks of node i (0 unless big)
+  int16_t* par = reinterpret_cast<int16_t*>(s_tk + kSmallR);
   uint8_t* Ps = reinterpret_cast<uint8_t*>(par + 2 * kSmallR);
   uint8_t* las = Ps + kSmallR + 1;
   uint8_t* ras = las + kSmallR + 1;
   uint8_t* dep = ras + kSmallR + 1;
   uint8_t* ldep = dep + kSmallR + 1;
+  uint8_t* s_lc = ldep + kSmallR + 1;  // leaf classes
+  uint8_t* s_nc = s_lc + kSmallR;       // node classes
   __shared__ MC smc[33];
   __shared__ unsigned long long sred[33];
   __shared__ unsigned s_maxd;
@@ -182,11 +190,10 @@ __device__ void small_tree(const TreeArrays& T, ClassifyArgs A, unsigned char* s
   }
   RS_TS(met, 6);
   // ---- trie ranges, parents, children, spans (d_tree)
-  uint32_t myspan[kSmallPer];
+  if (tid == 0) spans[0] = 0;
 #pragma unroll kSmallUnroll
   for (int q = 0; q < kSmallPer; ++q) {
     int64_t i = tid + (int64_t)q * nt;
-    myspan[q] = 0;
     if (i >= r) continue;
     {
       int64_t p = -1;
@@ -242,7 +249,7 @@ __device__ void small_tree(const TreeArrays& T, ClassifyArgs A, unsigned char* s
       T.node_s[j] = s0;
       T.node_e[j] = e0;
       // bit 31: not fusable (fusable_span: node table, average leaf length)
-      myspan[q] = (uint32_t)(e0 - s0) | (fusable_span(A, e0 - s0, b - a) ? 0u : 0x80000000u);
+      spans[j] = (uint32_t)(e0 - s0) | (fusable_span(A, e0 - s0, b - a) ? 0u : 0x80000000u);
       uint8_t dd = (uint8_t)(las[j] + ras[j]);
       T.depth[j] = dd;
       dep[j] = dd;
@@ -258,12 +265,6 @@ __device__ void small_tree(const TreeArrays& T, ClassifyArgs A, unsigned char* s
       if (pp >= 0) T.child[2 * pp + side] = (uint32_t)j;
     }
   }
-  __syncthreads();  // Ks dead from here: spans reuse it
-#pragma unroll kSmallUnroll
-  for (int q = 0; q < kSmallPer; ++q) {
-    int64_t i = tid + (int64_t)q * nt;
-    if (i < r) spans[i] = myspan[q];
-  }
   __syncthreads();
   RS_TS(met, 7);
   // ---- classification (d_classify), contiguous items per thread
@@ -273,18 +274,12 @@ __device__ void small_tree(const TreeArrays& T, ClassifyArgs A, unsigned char* s
   auto fusable_s = [&](int64_t j) { return (pos_t)spans[j] <= (pos_t)A.fcap; };  // kNoFuse set -> > fcap
   auto parent_small_s = [&](int32_t p) { return p >= 0 && fusable_s(p); };
   unsigned long long comps = 0, mcost = 0, mbig = 0;
-  uint32_t tk_of[kSmallPer];   // merge tasks of node i0+q (0 unless big)
-  uint32_t a_of[kSmallPer];    // phase-A tasks of item i0+q
-  uint8_t lcls[kSmallPer], ncls[kSmallPer];
   unsigned maxd = 0;
-#pragma unroll kSmallUnroll
-  for (int q = 0; q < kSmallPer; ++q) {
+  for (int q = 0; q < per; ++q) {
     int64_t i = i0 + q;
-    tk_of[q] = 0;
-    a_of[q] = 0;
-    lcls[q] = 0;
-    ncls[q] = 0;
-    if (q >= per || i >= r) continue;
+    if (i >= r) break;
+    uint32_t tk_i = 0, a_i = 0;
+    uint8_t nc_i = 0;
     pos_t s0 = Ls[i], len = (pos_t)Ls[i + 1] - s0;
     uint32_t info = A.leaf_info[i];
     uint32_t nl = info & 0x7fffffffu;
@@ -307,8 +302,8 @@ __device__ void small_tree(const TreeArrays& T, ClassifyArgs A, unsigned char* s
     }
     A.need[lid] = c == 1 ? 1u : (uint32_t)tl;
     A.cls[lid] = (uint8_t)c;
-    lcls[q] = (uint8_t)c;
-    a_of[q] = c == 1 ? 1u : (uint32_t)tl;
+    s_lc[i] = (uint8_t)c;
+    a_i = c == 1 ? 1u : (uint32_t)tl;
     if (i >= 1) {
       bool fz = fusable_s(i);
       pos_t span = (pos_t)(spans[i] & ~kNoFuse);
@@ -318,18 +313,21 @@ __device__ void small_tree(const TreeArrays& T, ClassifyArgs A, unsigned char* s
       if (fz) cn = parent_small_s(par[r + i]) ? 0 : 1;
       else cn = 2;
       A.cls[i] = (uint8_t)cn;
-      ncls[q] = (uint8_t)cn;
+      nc_i = (uint8_t)cn;
       if (cn == 1) {
         A.need[i] = 1;
-        a_of[q] += 1;
+        a_i += 1;
       } else if (cn == 2) {
         int64_t tn = ceil_div64(span, A.mtile);
         A.need[i] = (uint32_t)tn;
-        tk_of[q] = (uint32_t)ceil_div64(tn, A.msuper);
+        tk_i = (uint32_t)ceil_div64(tn, A.msuper);
         mbig += span;
         maxd = dep[i] > maxd ? dep[i] : maxd;
       } else A.need[i] = 0;
     }
+    s_nc[i] = nc_i;
+    s_tk[i] = tk_i;
+    s_aof[i] = a_i;
   }
   unsigned long long sc = block_sum(comps, sred);
   if (tid == 0) met->comparisons += sc;
@@ -345,33 +343,35 @@ __device__ void small_tree(const TreeArrays& T, ClassifyArgs A, unsigned char* s
   // Each job's first task slot and its own index come from one packed scan
   // (jobs << 32 | tasks); merge jobs carry their node's descriptor.
   unsigned long long vA = 0;
-#pragma unroll kSmallUnroll
-  for (int q = 0; q < kSmallPer; ++q) {
-    if (q >= per || i0 + q >= r) continue;
-    uint32_t tl = a_of[q] - (ncls[q] == 1 ? 1u : 0u);  // the leaf's own tasks
-    uint32_t jobs = (lcls[q] == 1 || (lcls[q] == 2 && tl > 0) ? 1u : 0u) + (ncls[q] == 1 ? 1u : 0u);
-    vA += ((unsigned long long)jobs << 32) | a_of[q];
+  for (int q = 0; q < per; ++q) {
+    const int64_t i = i0 + q;
+    if (i >= r) break;
+    uint32_t tl = s_aof[i] - (s_nc[i] == 1 ? 1u : 0u);  // the leaf's own tasks
+    uint32_t jobs = (s_lc[i] == 1 || (s_lc[i] == 2 && tl > 0) ? 1u : 0u) + (s_nc[i] == 1 ? 1u : 0u);
+    vA += ((unsigned long long)jobs << 32) | s_aof[i];
   }
   unsigned long long totv;
+  RS_TSD(met, 0);
   unsigned long long ex = block_excl_scan_u64(vA, sred, &totv);
+  RS_TSD(met, 1);
   const uint32_t totA = (uint32_t)totv;
   {
     uint32_t slot = (uint32_t)ex, jb = (uint32_t)(ex >> 32);
-#pragma unroll kSmallUnroll
-    for (int q = 0; q < kSmallPer; ++q) {
+    for (int q = 0; q < per; ++q) {
       int64_t i = i0 + q;
-      if (q >= per || i >= r) continue;
+      if (i >= r) break;
       uint32_t lid = A.leaf_base + (uint32_t)i;
-      uint32_t tl = a_of[q] - (ncls[q] == 1 ? 1u : 0u);
-      if (lcls[q] == 1 || (lcls[q] == 2 && tl > 0)) {
-        uint32_t kind = lcls[q] == 1 ? (uint32_t)kTaskFuse : (uint32_t)kTaskLeaf;
+      const uint8_t lc = s_lc[i], nc = s_nc[i];
+      uint32_t tl = s_aof[i] - (nc == 1 ? 1u : 0u);
+      if (lc == 1 || (lc == 2 && tl > 0)) {
+        uint32_t kind = lc == 1 ? (uint32_t)kTaskFuse : (uint32_t)kTaskLeaf;
         J.slot[jb] = slot;
         J.id[jb] = lid;
         J.cnt[jb] = tl | (kind << 30);
         ++jb;
         slot += tl;
       }
-      if (ncls[q] == 1) {
+      if (nc == 1) {
         J.slot[jb] = slot;
         J.id[jb] = (uint32_t)i;
         J.cnt[jb] = 1u | ((uint32_t)kTaskFuse << 30);
@@ -384,14 +384,18 @@ __device__ void small_tree(const TreeArrays& T, ClassifyArgs A, unsigned char* s
   // independent round trips instead of one dependent chain per depth
   for (int64_t i = 1 + tid; i < r; i += nt)
     if (A.cls[i] == 2) J.md[i] = load_mdesc(A, (uint32_t)i);
+  RS_TSD(met, 2);
   uint32_t jbase = (uint32_t)(totv >> 32);
   uint64_t base = totA;
   const int dmax = (int)s_maxd;
+  RS_TSD(met, 3);
   for (int d = dmax; d >= 0; --d) {
     unsigned long long v = 0;
-#pragma unroll kSmallUnroll
-    for (int q = 0; q < kSmallPer; ++q)
-      if (q < per && i0 + q < r && ncls[q] == 2 && dep[i0 + q] == d) v += (1ull << 32) | tk_of[q];
+    for (int q = 0; q < per; ++q) {
+      const int64_t i = i0 + q;
+      if (i >= r) break;
+      if (s_nc[i] == 2 && dep[i] == d) v += (1ull << 32) | s_tk[i];
+    }
     unsigned long long tot;
     unsigned long long e = block_excl_scan_u64(v, sred, &tot);
     if (tid == 0) {
@@ -400,15 +404,15 @@ __device__ void small_tree(const TreeArrays& T, ClassifyArgs A, unsigned char* s
       met->depth_cursor[d] = base;
     }
     uint32_t slot = (uint32_t)(base + (uint32_t)e), jb = jbase + (uint32_t)(e >> 32);
-#pragma unroll kSmallUnroll
-    for (int q = 0; q < kSmallPer; ++q) {
-      int64_t i = i0 + q;
-      if (q < per && i < r && ncls[q] == 2 && dep[i] == d) {
+    for (int q = 0; q < per; ++q) {
+      const int64_t i = i0 + q;
+      if (i >= r) break;
+      if (s_nc[i] == 2 && dep[i] == d) {
         J.slot[jb] = slot;
         J.id[jb] = (uint32_t)i;
-        J.cnt[jb] = tk_of[q] | ((uint32_t)kTaskMerge << 30);
+        J.cnt[jb] = s_tk[i] | ((uint32_t)kTaskMerge << 30);
         ++jb;
-        slot += tk_of[q];
+        slot += s_tk[i];
       }
     }
     base += (uint32_t)tot;
@@ -423,6 +427,7 @@ __device__ void small_tree(const TreeArrays& T, ClassifyArgs A, unsigned char* s
     met->task_ctr = totA;
     met->task_ctr_A = 0;
   }
+  RS_TSD(met, 4);
   RS_TS(met, 9);
 }
 

@@ -37,6 +37,7 @@ if __import__('os').environ.get('RS_LIB'):
     ts = list(buf[138:154]); print('prep phase us', [round((ts[i] - ts[i-1]) / 1e3, 1) for i in range(1, 12) if ts[i] and ts[i-1]])
     arr = list(buf[154:170]); print('phase work (latest arrival - prev exit) / barrier (exit - latest arrival) us', [(i, round((arr[i] - ts[i-1]) / 1e3, 1), round((ts[i] - arr[i]) / 1e3, 1)) for i in range(1, 10) if arr[i] and ts[i] and ts[i-1]])
     dbg = list(buf[170:202]); t4 = min([x for x in dbg if x] or [0]); print('dbg us after first dbg', [(i, round((dbg[i] - t4) / 1e3, 1)) for i in range(32) if dbg[i]])
+    if ts[8]: print('small-path dbg[0..4] us after ts8', [round((dbg[i] - ts[8]) / 1e3, 2) for i in range(5) if dbg[i]], 'ts9', round((ts[9] - ts[8]) / 1e3, 2))
     print('ts us after ts4', [(i, round((ts[i] - t4) / 1e3, 1)) for i in range(4, 12) if ts[i]])
     print('phase-1 max-warp cycles wait/bits/bwords/walk', ts[12:16])
     dw = list(buf[10:74]); dt = list(buf[74:138])
