@@ -115,6 +115,10 @@ struct ClassifyArgs {
   // waits for the ancestor scans (null: depths are already in place)
   const uint8_t* la = nullptr;
   const uint8_t* ra = nullptr;
+  // small-tree path: ready-time model of the merge-job order (ns; rs_small.cuh)
+  int est_c0 = 6000;  // one tile's latency through the executor
+  int est_c1 = 12;    // a tile's service time over the whole grid
+  int small_fuse = 1; // small-tree path: fuse subtrees of >= 3 leaves even when the leaves are long on average
 };
 
 // Merge descriptor of node i (two dependent round trips: the node's fields,

@@ -5,7 +5,8 @@
 //
 // Same outputs as k_prep's phases 5-9 (rs_tree.cuh, rs_exec.cuh: d_scan_reduce,
 // d_scan_down, d_tree, d_classify, d_task_offsets/d_order_scan, d_task_fill),
-// with the merge tasks in the identical (depth desc, position) order.  With few
+// with the merge tasks ordered by estimated ready time instead of (depth desc,
+// position) -- any topological order gives the same output.  With few
 // leaves those phases are pure latency: each is a chain of L2 round trips plus
 // a grid barrier over hundreds of mostly idle CTAs.  Here the chains run at
 // shared-memory latency behind __syncthreads (block 0, small_tree), which
@@ -101,7 +102,17 @@ __device__ void small_tree(const TreeArrays& T, ClassifyArgs A, unsigned char* s
   DevMetrics* met = A.met;
   const int64_t r = (int64_t)met->n_leaves;
   if (r > kSmallR || r < 1) return;
-  set_fuse_policy(A, r);
+  // Fuse policy.  Short leaves on average: every subtree that fits (as in the
+  // grid path).  Long leaves: the grid path fuses nothing (pairs of ~1K-element
+  // runs merge faster in the executor); a small tree is latency-bound instead
+  // -- every executor level under a big node costs a full tile latency (~10 us)
+  // on its critical path -- so subtrees of >= 3 leaves that fit are still fused
+  // (config 3: the chain of nine small levels below a 4M-element merge loses three).
+  int min_nodes = 0;  // 2: see the demotion pass after the trie phase
+  if (A.n >= (pos_t)A.fuse_avg * r) {
+    if (A.small_fuse) min_nodes = 2;
+    else A.fcap = 0;
+  }
   RS_TS(met, 5);
   uint32_t* Ls = reinterpret_cast<uint32_t*>(smem_small);
   uint32_t* Ks = Ls + kSmallR + 1;
@@ -266,6 +277,19 @@ __device__ void small_tree(const TreeArrays& T, ClassifyArgs A, unsigned char* s
     }
   }
   __syncthreads();
+  // long leaves: a fusable subtree of only two leaves whose parent is not
+  // fusable stays with the executor (marked not fusable; nothing reads the
+  // entries written here in this pass: such a node has no node child, and its
+  // parent, having one, is not rewritten)
+  if (min_nodes) {
+    for (int64_t j = 1 + tid; j < r; j += nt) {
+      const int pp = par[r + j];
+      if ((pos_t)spans[j] <= (pos_t)A.fcap && par[j - 1] == (int16_t)j && par[j] == (int16_t)j &&
+          !(pp >= 0 && (pos_t)spans[pp] <= (pos_t)A.fcap))
+        spans[j] |= 0x80000000u;
+    }
+    __syncthreads();
+  }
   RS_TS(met, 7);
   // ---- classification (d_classify), contiguous items per thread
   const int64_t per = (r + nt - 1) / nt;
@@ -389,34 +413,92 @@ __device__ void small_tree(const TreeArrays& T, ClassifyArgs A, unsigned char* s
   uint64_t base = totA;
   const int dmax = (int)s_maxd;
   RS_TSD(met, 3);
-  for (int d = dmax; d >= 0; --d) {
-    unsigned long long v = 0;
-    for (int q = 0; q < per; ++q) {
-      const int64_t i = i0 + q;
-      if (i >= r) break;
-      if (s_nc[i] == 2 && dep[i] == d) v += (1ull << 32) | s_tk[i];
-    }
-    unsigned long long tot;
-    unsigned long long e = block_excl_scan_u64(v, sred, &tot);
-    if (tid == 0) {
-      met->depth_tiles[d] = (uint32_t)tot;
-      met->depth_base[d] = base;
-      met->depth_cursor[d] = base;
-    }
-    uint32_t slot = (uint32_t)(base + (uint32_t)e), jb = jbase + (uint32_t)(e >> 32);
+  // ---- merge jobs in the order of their estimated ready times.  The executor
+  // claims tasks strictly in list order and a producer that claimed a task
+  // waits for the node's children, so a (depth desc, position) list lets one
+  // node with a deep subtree below it hold every producer while its ready
+  // siblings' tiles sit behind it (config 3: three 4M-element depth-2 nodes
+  // queued behind the fourth, which waits for a chain of nine small levels).
+  // ready(node) = max over its executor children of ready + c0 + c1 * tasks
+  // (c0: one tile's latency through the executor, c1: a tile's service time
+  // over the whole grid), 0 below phase-A children.  ready(parent) > ready(child),
+  // so the list stays a topological order (every wait is on an earlier task).
+  uint32_t* ready = spans;  // spans are dead after classification
+  unsigned long long* skey = reinterpret_cast<unsigned long long*>(smem_small);  // over Ls + Ks (dead)
+  for (int64_t i = tid; i < r; i += nt) ready[i] = 0;
+  __syncthreads();
+  for (int d = dmax; d >= 1; --d) {
     for (int q = 0; q < per; ++q) {
       const int64_t i = i0 + q;
       if (i >= r) break;
       if (s_nc[i] == 2 && dep[i] == d) {
-        J.slot[jb] = slot;
-        J.id[jb] = (uint32_t)i;
-        J.cnt[jb] = s_tk[i] | ((uint32_t)kTaskMerge << 30);
-        ++jb;
-        slot += s_tk[i];
+        const int p = par[r + i];
+        if (p >= 0) atomicMax(&ready[p], ready[i] + (uint32_t)A.est_c0 + (uint32_t)A.est_c1 * s_tk[i]);
       }
     }
-    base += (uint32_t)tot;
-    jbase += (uint32_t)(tot >> 32);
+    __syncthreads();
+  }
+  // compact the big nodes' sort keys: ready << 32 | min(tasks, 2^20 - 1) << 12 | node
+  unsigned long long vb = 0;
+  for (int q = 0; q < per; ++q) {
+    const int64_t i = i0 + q;
+    if (i >= r) break;
+    if (s_nc[i] == 2) vb += 1;
+  }
+  unsigned long long totb;
+  const unsigned long long exb = block_excl_scan_u64(vb, sred, &totb);
+  const int m2 = (int)totb;
+  int P2 = 1;
+  while (P2 < m2) P2 <<= 1;
+  {
+    int k = (int)exb;
+    for (int q = 0; q < per; ++q) {
+      const int64_t i = i0 + q;
+      if (i >= r) break;
+      if (s_nc[i] == 2) {
+        const uint32_t tk = s_tk[i] < 0xfffffu ? s_tk[i] : 0xfffffu;
+        skey[k++] = ((unsigned long long)ready[i] << 32) | ((unsigned long long)tk << 12) | (unsigned long long)i;
+      }
+    }
+    for (int x = m2 + tid; x < P2; x += nt) skey[x] = ~0ull;
+  }
+  __syncthreads();
+  // bitonic sort of P2 <= 2048 keys (all distinct: the node id is in the key)
+  for (int k = 2; k <= P2; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int t = tid; t < (P2 >> 1); t += nt) {
+        const int lo = ((t & ~(j - 1)) << 1) | (t & (j - 1));
+        const int hi = lo | j;
+        const unsigned long long a = skey[lo], b = skey[hi];
+        const bool up = (lo & k) == 0;
+        if ((a > b) == up) { skey[lo] = b; skey[hi] = a; }
+      }
+      __syncthreads();
+    }
+  }
+  // first task slot of every job: scan of the task counts in sorted order
+  {
+    const int per2 = (m2 + nt - 1) / nt;
+    const int x0 = tid * per2;
+    unsigned long long v = 0;
+    for (int q = 0; q < per2; ++q) {
+      const int x = x0 + q;
+      if (x < m2) v += s_tk[(uint32_t)skey[x] & 0xfffu];
+    }
+    unsigned long long tot;
+    const unsigned long long e = block_excl_scan_u64(v, sred, &tot);
+    uint32_t slot = (uint32_t)(base + e);
+    for (int q = 0; q < per2; ++q) {
+      const int x = x0 + q;
+      if (x >= m2) break;
+      const uint32_t i = (uint32_t)skey[x] & 0xfffu;
+      J.slot[jbase + x] = slot;
+      J.id[jbase + x] = i;
+      J.cnt[jbase + x] = s_tk[i] | ((uint32_t)kTaskMerge << 30);
+      slot += s_tk[i];
+    }
+    base += tot;
+    jbase += (uint32_t)m2;
   }
   if (tid == 0) {
     met->phaseA = totA;

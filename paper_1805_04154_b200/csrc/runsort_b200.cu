@@ -88,6 +88,8 @@ struct Tunables {
   bool prep_twice = false;  // RS_PREP_TWICE (RS_INSTR builds): a second, warm-code prep
   int debug_algo = -1;   // RS_DEBUG_ALGO: rs_debug_counters reads another algorithm's layout
   bool host_trace = false;  // RS_HOST_TRACE: rs_sort_host phase timings on stderr
+  int small_fuse = 1;          // RS_SMALL_FUSE: small-tree path fuses >= 3-leaf subtrees of long leaves
+  int est_c0 = 0, est_c1 = 0;  // RS_EST_C0 / RS_EST_C1: small-tree merge-job order model (ns; 0 = defaults)
 };
 const Tunables& tun() {
   static const Tunables t = [] {
@@ -105,6 +107,9 @@ const Tunables& tun() {
     v.prep_twice = getenv("RS_PREP_TWICE") != nullptr;
     v.debug_algo = geti("RS_DEBUG_ALGO", -1);
     v.host_trace = getenv("RS_HOST_TRACE") != nullptr;
+    v.small_fuse = geti("RS_SMALL_FUSE", 1);
+    v.est_c0 = geti("RS_EST_C0", 0);
+    v.est_c1 = geti("RS_EST_C1", 0);
     return v;
   }();
   return t;
@@ -582,6 +587,9 @@ int run_powersort(K* keys, void* tags, int64_t n, int w, int classic, unsigned c
   PA.CA = classify_args<K, TB>(V, L, n, w, classic, msuper, 0);
   PA.CA.la = V.la;  // the grid path's classification derives the depths
   PA.CA.ra = V.ra;
+  PA.CA.small_fuse = tun().small_fuse;
+  if (tun().est_c0 > 0) PA.CA.est_c0 = tun().est_c0;
+  if (tun().est_c1 > 0) PA.CA.est_c1 = tun().est_c1;
   PA.jobs = SmallJobs::at(V.jobs);
   int grid_p;
   void* kprep = ct == 1024 ? (void*)k_prep<K, 1024> : ct == 2560 ? (void*)k_prep<K, 2560> : (void*)k_prep<K, 2048>;
