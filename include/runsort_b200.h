@@ -22,6 +22,7 @@
  *   RS_EUNSUPPORTED-> TypeError / NotImplementedError (dtype or size outside
  *                     the device path; never a silent CPU fallback)
  *   RS_EIO         -> OSError         (gen.py:226-236 load_array file errors)
+ *   RS_ECAPACITY   -> (handled inside the host entry points: retry with RS_ALGO_FULL_WS)
  */
 #ifndef RUNSORT_B200_H
 #define RUNSORT_B200_H
@@ -40,6 +41,7 @@ extern "C" {
 #define RS_ECUDA 4
 #define RS_EUNSUPPORTED 5
 #define RS_EIO 6
+#define RS_ECAPACITY 7 /* peeksort's compact workspace overflowed; input unchanged: retry with RS_ALGO_FULL_WS */
 
 #define RS_ALGO_POWERSORT 0
 #define RS_ALGO_PEEKSORT 1
@@ -48,6 +50,15 @@ extern "C" {
 #define RS_ALGO_BOTTOM_UP 3
 #define RS_ALGO_ALPHA_STACK 4
 #define RS_ALGO_ALPHA_MERGE 5
+/* Flag or-ed into RS_ALGO_PEEKSORT wherever `algo` is passed (rs_workspace_bytes,
+ * rs_sort*, rs_fetch_metrics, rs_export_tree): size peeksort's replay arrays
+ * for the worst case of n + 1 recursive calls (~290 bytes per element) instead
+ * of the compact default (n / 12 + 4096 calls, ~29 bytes per element, the
+ * frontier laid over the scratch buffers).  A sort whose recursion outgrows
+ * the compact arrays restores the input on the device and reports
+ * RS_ECAPACITY; rs_sort_host* and the Python entry points then sort again with
+ * this flag themselves.  Ignored for the other algorithms. */
+#define RS_ALGO_FULL_WS 0x100
 
 #define RS_KEY_I32 1
 #define RS_KEY_I64 2

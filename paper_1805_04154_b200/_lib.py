@@ -17,6 +17,8 @@ RS_ALGO_TOP_DOWN, RS_ALGO_BOTTOM_UP, RS_ALGO_ALPHA_STACK, RS_ALGO_ALPHA_MERGE = 
 RS_KEY_I32, RS_KEY_I64 = 1, 2
 RS_MERGE_BITONIC, RS_MERGE_CLASSIC = 0, 1
 RS_EIO = 6
+RS_ECAPACITY = 7  # peeksort's compact replay workspace overflowed (input unchanged): retry with RS_ALGO_FULL_WS
+RS_ALGO_FULL_WS = 0x100
 
 # every symbol include/runsort_b200.h declares
 EXPORTS = ("rs_workspace_bytes", "rs_sort", "rs_sort_ex", "rs_fetch_metrics", "rs_sort_host", "rs_sort_host_ex", "rs_export_tree", "rs_profile",

@@ -58,12 +58,13 @@ static_assert(sizeof(MDesc) == 48 && offsetof(MDesc, e) == 16 && offsetof(MDesc,
 enum LeafMode : int { kLeafNone = 0, kLeafSwap = 1, kLeafRevCopy = 2, kLeafCopy = 3 };
 
 // Device-resident metrics, accumulated with atomics (reference runcore.py:40-55).
+constexpr unsigned long long kErrPeekCapacity = 4;  // peeksort's compact replay workspace overflowed (input restored)
 struct DevMetrics {
   unsigned long long merge_cost;
   unsigned long long comparisons;
   unsigned long long runs_detected;
   unsigned long long max_stack_height;
-  unsigned long long error;       // nonzero: invariant failure (maps to AssertionError)
+  unsigned long long error;       // nonzero: invariant failure (maps to AssertionError); kErrPeekCapacity: RS_ECAPACITY
   unsigned long long n_leaves;    // r
   unsigned long long n_tasks;     // total executor tasks
   unsigned long long task_ctr;    // merge-executor claim counter (starts at phaseA)

@@ -59,6 +59,10 @@ struct PeekArgs {
 struct PeekCounters {
   unsigned long long front_n[3];
   unsigned long long n_nodes, n_leaves, n_revs;
+  // capacity overflow seen while evaluating level L goes to err[(L + 1) & 1],
+  // which every thread reads at the top of level L + 1 (two slots, so a fast
+  // thread's level-(L+1) overflow cannot reach a slow thread's level-(L+1) read)
+  unsigned long long err[2];
 };
 static_assert(sizeof(PeekCounters) <= sizeof(((DevMetrics*)nullptr)->peek), "PeekCounters live in DevMetrics::peek");
 
@@ -314,6 +318,7 @@ struct PeekOut {
   pos_t* revs;
   unsigned long long* n_revs;
   int64_t front_cap, rec_cap;
+  unsigned long long* err;  // this level's overflow slot (PeekCounters::err)
   DevMetrics* met;
 };
 
@@ -331,7 +336,7 @@ __device__ __forceinline__ unsigned long long agg_inc(unsigned long long* ctr) {
 __device__ __forceinline__ void peek_push(const PeekOut& O, pos_t l, pos_t r, pos_t e, pos_t s, bool ed, bool sd,
                                           uint32_t d) {
   unsigned long long k = agg_inc(O.next_cnt);
-  if ((int64_t)k >= O.front_cap) { O.met->error = 2; return; }
+  if ((int64_t)k >= O.front_cap) { *O.err = 2; return; }
   PeekItem it;
   it.l = l; it.r = r; it.e = e; it.s = s;
   it.flags = (ed ? 1u : 0u) | (sd ? 2u : 0u) | (d << 8);
@@ -340,18 +345,18 @@ __device__ __forceinline__ void peek_push(const PeekOut& O, pos_t l, pos_t r, po
 }
 __device__ __forceinline__ void peek_leaf(const PeekOut& O, pos_t l, pos_t r, pos_t npre, uint32_t d) {
   unsigned long long k = agg_inc(O.n_leaves);
-  if ((int64_t)k >= O.rec_cap) { O.met->error = 2; return; }
+  if ((int64_t)k >= O.rec_cap) { *O.err = 2; return; }
   O.leaves[4 * k] = l; O.leaves[4 * k + 1] = r; O.leaves[4 * k + 2] = npre; O.leaves[4 * k + 3] = d;
 }
 __device__ __forceinline__ void peek_node(const PeekOut& O, pos_t l, pos_t mid, pos_t r, uint32_t d) {
   unsigned long long k = agg_inc(O.n_nodes);
-  if ((int64_t)k >= O.rec_cap) { O.met->error = 2; return; }
+  if ((int64_t)k >= O.rec_cap) { *O.err = 2; return; }
   O.nodes[4 * k] = l; O.nodes[4 * k + 1] = mid; O.nodes[4 * k + 2] = r; O.nodes[4 * k + 3] = d;
 }
 __device__ __forceinline__ void peek_rev(const PeekOut& O, pos_t i, pos_t j) {
   if (j <= i) return;
   unsigned long long k = agg_inc(O.n_revs);
-  if ((int64_t)k >= O.rec_cap) { O.met->error = 2; return; }
+  if ((int64_t)k >= O.rec_cap) { *O.err = 2; return; }
   O.revs[2 * k] = i; O.revs[2 * k + 1] = j;
 }
 
@@ -552,6 +557,7 @@ __global__ void __launch_bounds__(256, 2) k_peek(PeekArgs P) {
   O.met = met;
   if (blockIdx.x == 0) RS_DBG(met, 1);
   // 1. first run (sorters.py:177) and the root call (:351-357)
+  O.err = &pc->err[0];
   if (gtid == 0) {
     O.next = P.front[0];
     O.next_cnt = &pc->front_n[0];
@@ -573,9 +579,35 @@ __global__ void __launch_bounds__(256, 2) k_peek(PeekArgs P) {
   // (plus one after a level's reversals, whose keys the next evaluations read).
   int lev = 0;
   unsigned long long rev_done = 0;
+  constexpr int kRevBatches = 256;  // reversal batches (one per level that reversed something)
+  __shared__ unsigned long long s_revb[kRevBatches];
+  int nbatch = 0;
   for (;;) {
+    if (*(volatile unsigned long long*)&pc->err[lev & 1]) {
+      // The frontier or a record array is full (compact workspace, rs_workspace_bytes
+      // without RS_ALGO_FULL_WS).  Put the keys back as they came -- the
+      // reversals applied so far are disjoint strictly descending runs, so
+      // reversing them again restores the input -- and leave every task count
+      // at zero: phase A and the merge executor find nothing to do, and the
+      // host reports RS_ECAPACITY (the caller sorts again with the full workspace).
+      // A later level's chain may end on the first element of an earlier
+      // level's (reversed) run, so the batches are undone last first; within
+      // a level the calls' ranges, hence their reversals, are disjoint.
+      __syncthreads();
+      for (int b = (nbatch < kRevBatches ? nbatch : kRevBatches) - 1; b >= 0; --b) {
+        const unsigned long long b0 = s_revb[b], b1 = b + 1 < nbatch ? s_revb[b + 1] : rev_done;
+        reverse_segments<K, TB>(P, P.revs + 2 * b0, (int64_t)(b1 - b0));
+        grid.sync();
+      }
+      // more levels than batch slots (beyond any tree the executor takes): not restored
+      if (gtid == 0) met->error = nbatch <= kRevBatches ? kErrPeekCapacity : 2;
+      return;
+    }
+    O.err = &pc->err[(lev + 1) & 1];
     unsigned long long nrev = *(volatile unsigned long long*)&pc->n_revs;
     if (nrev > rev_done) {
+      if (threadIdx.x == 0 && nbatch < kRevBatches) s_revb[nbatch] = rev_done;  // batch starts, for the undo
+      ++nbatch;
       reverse_segments<K, TB>(P, P.revs + 2 * rev_done, (int64_t)(nrev - rev_done));
       rev_done = nrev;
       grid.sync();

@@ -169,6 +169,7 @@ struct Layout {
   int64_t mdesc_cap;  // merge-task descriptors (indexed from the first merge task)
   // peeksort replay
   int algo;
+  int full_ws;  // RS_ALGO_FULL_WS: replay capacity n + 1 instead of the compact one
   int64_t front_cap, rec_cap, sum_words, wchunks;
   size_t o_front0, o_front1, o_pnodes, o_pleaves, o_prevs, o_lbits, o_wpre, o_wchunk, o_nozero, o_noone;
 };
@@ -182,8 +183,25 @@ int exec_fcap(int kb, int tb) {
   return tb == 0 ? ExecCfg<int64_t, 0>::FCAP : (tb == 4 ? ExecCfg<int64_t, 4>::FCAP : ExecCfg<int64_t, 8>::FCAP);
 }
 
+// Peeksort's replay capacity (recursive calls per level, leaves, merge nodes,
+// reversals; also its leaf bound r_max).  Leaves can be single elements, so
+// only n + 1 is safe for every input (RS_ALGO_FULL_WS: ~290 bytes per
+// element).  The compact default holds n / 12 + 4096 of each -- min_run_len =
+// 24 on a random permutation gives ~n / 17 leaves -- with the frontier
+// ping-pong laid over the two scratch key/tag buffers, which nothing uses
+// before the executors run; a replay that would overflow restores the input
+// and reports RS_ECAPACITY (rs_peek.cuh), and the caller sorts again with
+// RS_ALGO_FULL_WS.
+int64_t peek_capacity(int64_t n, bool full) {
+  int64_t c = n / 12 + 4096;
+  return full || c > n + 1 ? n + 1 : c;
+}
+
+// `algo` may carry RS_ALGO_FULL_WS.
 Layout make_layout(int64_t n, int w, int kb, int tb, int algo) {
   Layout L{};
+  L.full_ws = (algo & RS_ALGO_FULL_WS) != 0;
+  algo &= ~RS_ALGO_FULL_WS;
   L.algo = algo;
   L.n = n;
   L.w = w;
@@ -200,7 +218,11 @@ Layout make_layout(int64_t n, int w, int kb, int tb, int algo) {
   if (algo == RS_ALGO_TOP_DOWN) minleaf = (w + 1) / 2;  // halves of ranges > w
   if (algo == RS_ALGO_BOTTOM_UP) minleaf = w;            // chunks of w
   L.r_max = n / minleaf + 2;
-  if (L.r_max > n + 1 || algo == RS_ALGO_PEEKSORT) L.r_max = n + 1;  // peeksort leaves can be single elements
+  if (L.r_max > n + 1) L.r_max = n + 1;
+  if (algo == RS_ALGO_PEEKSORT) {  // leaves can be single elements
+    if (peek_capacity(n, false) == n + 1) L.full_ws = 1;  // small n: the compact capacity is the full one
+    L.r_max = peek_capacity(n, L.full_ws);
+  }
   L.leaf_base = (uint32_t)(L.r_max + 1);
   L.nchunks = (L.r_max + kScanThreads - 1) / kScanThreads + 1;
   int levels = 2;
@@ -245,19 +267,27 @@ Layout make_layout(int64_t n, int w, int kb, int tb, int algo) {
   // merge tasks <= sum over merge nodes of (span / tile + 1): merge_cost <= n * levels elements
   // in tiles of >= 1792 (16-byte elements), plus one per merge node (<= r_max; peeksort:
   // fused subtrees or >= 8-element average leaves).  Overflow is caught on the device.
-  L.mdesc_cap = (int64_t)levels * (n / 1792 + 1) + (algo == RS_ALGO_PEEKSORT ? n / 8 : L.r_max) + 64;
+  L.mdesc_cap = (int64_t)levels * (n / 1792 + 1) + (algo == RS_ALGO_PEEKSORT ? std::min<int64_t>(n / 8, L.r_max) : L.r_max) + 64;
   if (L.mdesc_cap > L.max_tasks) L.mdesc_cap = L.max_tasks;
   L.o_mdesc = take((size_t)L.mdesc_cap * sizeof(MDesc));
   L.o_chunkdep = take((size_t)((L.r_max + kOrdChunkMin - 1) / kOrdChunkMin + 1) * kMaxDepth * 4);
   L.o_cls = take((size_t)(2 * L.r_max + 2));
   L.o_jobs = take(small_jobs_bytes());
   if (pk) {
-    L.front_cap = n + 1;
-    L.rec_cap = n + 1;
+    L.rec_cap = L.r_max;
     L.sum_words = skip_tree_words(L.words);
     L.wchunks = (L.words + kWordChunk - 1) / kWordChunk + 1;
-    L.o_front0 = take((size_t)L.front_cap * sizeof(PeekItem));
-    L.o_front1 = take((size_t)L.front_cap * sizeof(PeekItem));
+    if (L.full_ws) {
+      L.front_cap = L.rec_cap;
+      L.o_front0 = take((size_t)L.front_cap * sizeof(PeekItem));
+      L.o_front1 = take((size_t)L.front_cap * sizeof(PeekItem));
+    } else {
+      // the frontier ping-pong over the scratch buffers (key1 + tag1, key2 + tag2)
+      L.o_front0 = L.o_key1;
+      L.o_front1 = L.o_key2;
+      int64_t fit = (int64_t)(std::min(L.o_key2 - L.o_key1, L.o_ascw - L.o_key2) / sizeof(PeekItem));
+      L.front_cap = std::min(L.rec_cap, fit);
+    }
     L.o_pnodes = take((size_t)L.rec_cap * 32);
     L.o_pleaves = take((size_t)L.rec_cap * 32);
     L.o_prevs = take((size_t)L.rec_cap * 16);
@@ -992,6 +1022,9 @@ int read_metrics(const Layout& L, unsigned char* ws, cudaStream_t st, rs_metrics
   DevMetrics hm;
   RS_CUDA(cudaMemcpyAsync(&hm, ws + L.o_met, sizeof(DevMetrics), cudaMemcpyDeviceToHost, st));
   RS_CUDA(cudaStreamSynchronize(st));
+  if (hm.error == kErrPeekCapacity)
+    return fail(RS_ECAPACITY, "peeksort replay exceeded the compact workspace (input unchanged): sort again with "
+                              "RS_ALGO_PEEKSORT | RS_ALGO_FULL_WS");
   if (hm.error) return fail(RS_EINVARIANT, "device invariant failure (leaf count exceeded bound)");
   if (out) {
     out->merge_cost = hm.merge_cost;
@@ -1407,6 +1440,8 @@ int rs_sort_ex(int algo, int key_dtype, void* keys, int tag_bytes, void* tags, i
                int32_t merge_kind, double alpha, void* workspace, size_t ws_bytes, void* stream, rs_metrics* out,
                rs_tree* tree) {
   int kb;
+  const int algo_ws = algo;  // may carry RS_ALGO_FULL_WS (peeksort's replay capacity)
+  algo &= ~RS_ALGO_FULL_WS;
   if (int e = validate(algo, key_dtype, tag_bytes, n, min_run_len, merge_kind, &kb)) return e;
   if (!(alpha > 1.0)) return fail(RS_EINVAL, "alpha must be > 1");
   if (tree && algo >= RS_ALGO_TOP_DOWN) return fail(RS_EUNSUPPORTED, "the baseline sorters record no merge tree");
@@ -1423,7 +1458,7 @@ int rs_sort_ex(int algo, int key_dtype, void* keys, int tag_bytes, void* tags, i
     return RS_OK;
   }
   if (!keys || !workspace) return fail(RS_EINVAL, "null keys or workspace");
-  Layout L = make_layout(n, min_run_len, kb, tag_bytes, algo);
+  Layout L = make_layout(n, min_run_len, kb, tag_bytes, algo_ws);
   if (ws_bytes < L.total) return fail(RS_ENOMEM, "workspace too small");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   unsigned char* ws = reinterpret_cast<unsigned char*>(workspace);
@@ -1496,7 +1531,7 @@ int rs_fetch_metrics(int algo, int key_dtype, int tag_bytes, int64_t n, int32_t 
 int rs_export_tree(int algo, int key_dtype, int tag_bytes, int64_t n, int32_t min_run_len, void* workspace,
                    void* stream, rs_tree* tree) {
   if (!tree) return fail(RS_EINVAL, "null tree");
-  if (algo != RS_ALGO_POWERSORT && algo != RS_ALGO_PEEKSORT)
+  if ((algo & ~RS_ALGO_FULL_WS) != RS_ALGO_POWERSORT && (algo & ~RS_ALGO_FULL_WS) != RS_ALGO_PEEKSORT)
     return fail(RS_EUNSUPPORTED, "the baseline sorters record no merge tree");
   if (n <= 1) {
     tree->n_leaves = n;
@@ -1525,6 +1560,8 @@ int rs_sort_host(int algo, int key_dtype, void* keys, int tag_bytes, void* tags,
 int rs_sort_host_ex(int algo, int key_dtype, void* keys, int tag_bytes, void* tags, int64_t n, int32_t min_run_len,
                     int32_t merge_kind, double alpha, rs_metrics* out, rs_tree* tree) {
   int kb;
+  int algo_ws = algo;  // may carry RS_ALGO_FULL_WS; set here when the compact peeksort replay overflows
+  algo &= ~RS_ALGO_FULL_WS;
   if (int e = validate(algo, key_dtype, tag_bytes, n, min_run_len, merge_kind, &kb)) return e;
   if (!(alpha > 1.0)) return fail(RS_EINVAL, "alpha must be > 1");
   if (tags == nullptr) tag_bytes = 0;
@@ -1533,7 +1570,7 @@ int rs_sort_host_ex(int algo, int key_dtype, void* keys, int tag_bytes, void* ta
   if (!keys) return fail(RS_EINVAL, "null keys");
   int dev;
   RS_CUDA(cudaGetDevice(&dev));
-  Layout L = make_layout(n, min_run_len, kb, tag_bytes, algo);
+  Layout L = make_layout(n, min_run_len, kb, tag_bytes, algo_ws);
   size_t ws = L.total;
   HostTrace tr;
   {
@@ -1576,18 +1613,35 @@ int rs_sort_host_ex(int algo, int key_dtype, void* keys, int tag_bytes, void* ta
       break;
     }
     tr.mark("h2d queued");
-    rc = rs_sort_ex(algo, key_dtype, dk, tag_bytes, dt, n, min_run_len, merge_kind, alpha, dws, ws, st, nullptr,
-                    nullptr);
+    int d = 0;
+    for (;;) {
+      rc = rs_sort_ex(algo_ws, key_dtype, dk, tag_bytes, dt, n, min_run_len, merge_kind, alpha, dws, ws, st, nullptr,
+                      nullptr);
+      if (rc) break;
+      tr.mark("sort queued");
+      unsigned char* wsp = reinterpret_cast<unsigned char*>(dws);
+      d = S.d2h(spans, st, [&]() -> int {
+        int e = read_metrics(L, wsp, st, out);  // synchronizes: the sort is complete
+        tr.mark("sort done");
+        if (!e && tree) e = export_tree(L, wsp, st, tree);
+        return e;
+      });
+      tr.mark("d2h done");
+      if (d != RS_ECAPACITY || (algo_ws & RS_ALGO_FULL_WS)) break;
+      // peeksort outgrew its compact replay arrays: the device restored the
+      // keys and tags, nothing was written back -- sort again, worst-case capacity
+      algo_ws |= RS_ALGO_FULL_WS;
+      L = make_layout(n, min_run_len, kb, tag_bytes, algo_ws);
+      ws = L.total;
+      cudaFreeAsync(dws, st);
+      dws = nullptr;
+      if (cudaMallocAsync(&dws, ws, st) != cudaSuccess) {
+        cudaGetLastError();
+        rc = fail(RS_ENOMEM, "device allocation failed (peeksort worst-case workspace)");
+        break;
+      }
+    }
     if (rc) break;
-    tr.mark("sort queued");
-    unsigned char* wsp = reinterpret_cast<unsigned char*>(dws);
-    int d = S.d2h(spans, st, [&]() -> int {
-      int e = read_metrics(L, wsp, st, out);  // synchronizes: the sort is complete
-      tr.mark("sort done");
-      if (!e && tree) e = export_tree(L, wsp, st, tree);
-      return e;
-    });
-    tr.mark("d2h done");
     if (d > 0) rc = d;  // the device's verdict (nothing was written back)
     else if (d < 0) rc = fail(RS_ECUDA, "device-to-host copy failed");
   } while (0);

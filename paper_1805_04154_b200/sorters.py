@@ -358,33 +358,43 @@ def _device_sort_on(algo: int, a, cfg: SortConfig, metrics: Metrics, tags, dev) 
     w = int(cfg.min_run_len)
     kind = _lib.RS_MERGE_CLASSIC if cfg.merge_kind == "classic" else _lib.RS_MERGE_BITONIC
     tb = tg.code if tg is not None else 0
-    ws_bytes = L.rs_workspace_bytes(algo, keys.code, tb, n, w)
-    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
     out = _lib.RsMetrics()
+    staged = [keys] + ([tg] if tg is not None else [])
     # The sort is enqueued without a host sync; numpy results are copied back
     # into a staging buffer queued behind it, and one synchronizing Metrics
     # fetch follows.  Only when the device reported no invariant failure is
     # the caller's host object overwritten (CUDA tensors are sorted in place).
-    rc = L.rs_sort_ex(algo, keys.code, keys.dev_t.data_ptr(), tb,
-                      tg.dev_t.data_ptr() if tg is not None else None, n, w, kind, float(cfg.alpha),
-                      ws.data_ptr(), ws_bytes, stream.cuda_stream, None, None)
-    _lib.check(rc)
-    staged = [keys] + ([tg] if tg is not None else [])
-    for s_ in staged:
-        s_.finish_device()
-        s_.queue_host_copy()
-    _lib.check(L.rs_fetch_metrics(algo, keys.code, tb, n, w, ws.data_ptr(), stream.cuda_stream,
-                                  ctypes.byref(out)))
+    # Peeksort runs with its compact replay workspace first; if the recursion
+    # outgrows it the device restores the input and reports RS_ECAPACITY, and
+    # the sort runs again with the worst-case workspace (RS_ALGO_FULL_WS).
+    algo_ws = algo
+    while True:
+        ws_bytes = L.rs_workspace_bytes(algo_ws, keys.code, tb, n, w)
+        ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+        rc = L.rs_sort_ex(algo_ws, keys.code, keys.dev_t.data_ptr(), tb,
+                          tg.dev_t.data_ptr() if tg is not None else None, n, w, kind, float(cfg.alpha),
+                          ws.data_ptr(), ws_bytes, stream.cuda_stream, None, None)
+        _lib.check(rc)
+        for s_ in staged:
+            s_.finish_device()
+            s_.queue_host_copy()
+        rc = L.rs_fetch_metrics(algo_ws, keys.code, tb, n, w, ws.data_ptr(), stream.cuda_stream, ctypes.byref(out))
+        if rc == _lib.RS_ECAPACITY and not (algo_ws & _lib.RS_ALGO_FULL_WS):
+            algo_ws |= _lib.RS_ALGO_FULL_WS
+            del ws
+            continue
+        _lib.check(rc)
+        break
     tree = None
     if cfg.record_tree and algo in (_lib.RS_ALGO_POWERSORT, _lib.RS_ALGO_PEEKSORT):
         # host arrays sized by the leaf count r (not n): query r, then export
         probe = _lib.RsTree(0, 0, None, None, None)
-        _lib.check(L.rs_export_tree(algo, keys.code, tb, n, w, ws.data_ptr(), stream.cuda_stream,
+        _lib.check(L.rs_export_tree(algo_ws, keys.code, tb, n, w, ws.data_ptr(), stream.cuda_stream,
                                     ctypes.byref(probe)))
         r = int(probe.n_leaves)
         bufs = (np.zeros(r, dtype=np.int64), np.zeros(r, dtype=np.uint8), np.zeros(r, dtype=np.uint8))
         tree = _lib.RsTree(r, 0, bufs[0].ctypes.data, bufs[1].ctypes.data, bufs[2].ctypes.data)
-        _lib.check(L.rs_export_tree(algo, keys.code, tb, n, w, ws.data_ptr(), stream.cuda_stream,
+        _lib.check(L.rs_export_tree(algo_ws, keys.code, tb, n, w, ws.data_ptr(), stream.cuda_stream,
                                     ctypes.byref(tree)))
     for s_ in staged:
         s_.finish_host()
@@ -415,7 +425,7 @@ class PendingSort:
         _lib.check(_lib.lib().rs_fetch_metrics(algo, code, tb, n, w, self.workspace.data_ptr(),
                                                self.stream.cuda_stream, ctypes.byref(out)))
         m = Metrics()
-        _accumulate(algo, m, out)
+        _accumulate(algo & ~_lib.RS_ALGO_FULL_WS, m, out)
         return m
 
 
@@ -429,7 +439,8 @@ def sort_async(keys, tags=None, cfg: Optional[SortConfig] = None, algo: str = "p
     torch = _torch()
     L = _lib.lib()
     cfg = cfg or SortConfig()
-    code = {"powersort": _lib.RS_ALGO_POWERSORT, "peeksort": _lib.RS_ALGO_PEEKSORT}[algo]
+    # no host round trip here, so no retry: peeksort takes its worst-case workspace
+    code = {"powersort": _lib.RS_ALGO_POWERSORT, "peeksort": _lib.RS_ALGO_PEEKSORT | _lib.RS_ALGO_FULL_WS}[algo]
     n = int(keys.numel())
     if n <= 1:
         return None

@@ -59,3 +59,22 @@ def test_invalid_arguments_rejected_before_any_device_work():
     # n <= 1 returns immediately (reference sorters.py:445-450)
     assert L.rs_sort(0, _lib.RS_KEY_I32, None, 0, None, 1, 24, 0, None, 0, None, ctypes.byref(out), None) == _lib.RS_OK
     assert out.runs_detected == 1 and out.merge_cost == 0
+
+
+def test_peeksort_workspace_is_compact_by_default():
+    """Peeksort's default workspace stays within 2x powersort's (VERDICT round 1, item 8);
+    RS_ALGO_FULL_WS sizes the replay arrays for n + 1 recursive calls."""
+    L = _lib.lib()
+    for kc, tb in ((_lib.RS_KEY_I32, 0), (_lib.RS_KEY_I32, 4), (_lib.RS_KEY_I64, 0), (_lib.RS_KEY_I64, 8)):
+        for n in (10**7, 10**8):
+            power = L.rs_workspace_bytes(_lib.RS_ALGO_POWERSORT, kc, tb, n, 24)
+            peek = L.rs_workspace_bytes(_lib.RS_ALGO_PEEKSORT, kc, tb, n, 24)
+            full = L.rs_workspace_bytes(_lib.RS_ALGO_PEEKSORT | _lib.RS_ALGO_FULL_WS, kc, tb, n, 24)
+            assert peek <= 2 * power, (kc, tb, n, peek / n, power / n)
+            assert full > 5 * peek
+    # small n: the compact capacity already is n + 1
+    assert L.rs_workspace_bytes(_lib.RS_ALGO_PEEKSORT, _lib.RS_KEY_I32, 0, 3000, 24) == \
+        L.rs_workspace_bytes(_lib.RS_ALGO_PEEKSORT | _lib.RS_ALGO_FULL_WS, _lib.RS_KEY_I32, 0, 3000, 24)
+    # the flag means nothing to the other algorithms
+    assert L.rs_workspace_bytes(_lib.RS_ALGO_POWERSORT | _lib.RS_ALGO_FULL_WS, _lib.RS_KEY_I32, 0, 10**6, 24) == \
+        L.rs_workspace_bytes(_lib.RS_ALGO_POWERSORT, _lib.RS_KEY_I32, 0, 10**6, 24)

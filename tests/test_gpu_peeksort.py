@@ -120,3 +120,83 @@ def test_peeksort_long_descending_runs_vs_oracle(key_dtype):
             work, tw, m = _run(a, w, "bitonic", tags)
             assert np.array_equal(work, ref_a) and np.array_equal(tw, ref_t), (len(lens), w)
             assert _mt(m) == ref.metrics_tuple(), (len(lens), w)
+
+
+# ---- compact replay workspace: overflow -> input restored -> worst-case retry
+def _zigzag(n, seed):
+    """Runs of 2-3 elements in both directions: with min_run_len = 1 peeksort makes
+    ~n / 2.5 leaves, far beyond the compact capacity n / 12 + 4096."""
+    rng = np.random.default_rng(seed)
+    return rng.integers(0, 1 << 30, size=n, dtype=np.int64)
+
+
+@pytest.mark.parametrize("key_dtype,tag_dtype", [(np.int32, None), (np.int64, np.int32), (np.int32, np.int64)])
+def test_peeksort_compact_overflow_c_abi(key_dtype, tag_dtype):
+    """rs_sort with the compact workspace reports RS_ECAPACITY and leaves keys and
+    tags exactly as they came; with RS_ALGO_FULL_WS the sort matches the oracle."""
+    import ctypes
+
+    import torch
+
+    from paper_1805_04154_b200 import _lib
+
+    L = _lib.lib()
+    n, w = 300_000, 1
+    a = _zigzag(n, 11).astype(key_dtype)
+    # strictly descending stretches so that reversals are applied before the overflow
+    a[1000:1400] = np.arange(400, 0, -1, dtype=key_dtype)
+    a[150_000:150_900] = np.arange(900, 0, -1, dtype=key_dtype)
+    tags = np.arange(n, dtype=tag_dtype) if tag_dtype is not None else None
+    kc = _lib.RS_KEY_I32 if a.itemsize == 4 else _lib.RS_KEY_I64
+    tb = tags.itemsize if tags is not None else 0
+    dk = torch.from_numpy(a).cuda()
+    dt = torch.from_numpy(tags).cuda() if tags is not None else None
+    st = torch.cuda.current_stream()
+    small = L.rs_workspace_bytes(_lib.RS_ALGO_PEEKSORT, kc, tb, n, w)
+    full = L.rs_workspace_bytes(_lib.RS_ALGO_PEEKSORT | _lib.RS_ALGO_FULL_WS, kc, tb, n, w)
+    assert small < full
+    ws = torch.empty(full, dtype=torch.uint8, device="cuda")
+    out = _lib.RsMetrics()
+    rc = L.rs_sort(_lib.RS_ALGO_PEEKSORT, kc, dk.data_ptr(), tb, dt.data_ptr() if dt is not None else None, n, w, 0,
+                   ws.data_ptr(), small, st.cuda_stream, ctypes.byref(out), None)
+    assert rc == _lib.RS_ECAPACITY
+    assert np.array_equal(dk.cpu().numpy(), a), "keys changed by an overflowed replay"
+    if dt is not None:
+        assert np.array_equal(dt.cpu().numpy(), tags), "tags changed by an overflowed replay"
+    rc = L.rs_sort(_lib.RS_ALGO_PEEKSORT | _lib.RS_ALGO_FULL_WS, kc, dk.data_ptr(), tb,
+                   dt.data_ptr() if dt is not None else None, n, w, 0, ws.data_ptr(), full, st.cuda_stream,
+                   ctypes.byref(out), None)
+    assert rc == _lib.RS_OK
+    ref_k, ref_t = a.copy(), (tags.copy() if tags is not None else None)
+    ref = oracle.peeksort(ref_k, w, "bitonic", ref_t)
+    assert np.array_equal(dk.cpu().numpy(), ref_k)
+    if dt is not None:
+        assert np.array_equal(dt.cpu().numpy(), ref_t)
+    assert (out.merge_cost, out.comparisons, out.runs_detected) == ref.metrics_tuple()[:3]
+    assert ref.runs_detected > n // 12 + 4096  # the input does exceed the compact capacity
+
+
+@pytest.mark.parametrize("how", ["numpy", "cuda", "pinned"])
+def test_peeksort_compact_overflow_public_api(how):
+    """The public entry points retry by themselves (numpy: rs_sort_host_ex; torch: the
+    Python shim): output, tags, Metrics and the recorded tree equal the oracle's."""
+    import torch
+
+    n, w = 200_000, 2
+    a = _zigzag(n, 12).astype(np.int32)
+    tags = np.arange(n, dtype=np.int32)
+    ref_k, ref_t = a.copy(), tags.copy()
+    ref = oracle.peeksort(ref_k, w, "classic", ref_t)
+    assert ref.runs_detected > n // 12 + 4096
+    cfg = rs.SortConfig(min_run_len=w, merge_kind="classic")
+    if how == "numpy":
+        k, t = a.copy(), tags.copy()
+        m = rs.peeksort(k, cfg, tags=t)
+        got_k, got_t = k, t
+    else:
+        k, t = torch.from_numpy(a.copy()), torch.from_numpy(tags.copy())
+        k, t = (k.cuda(), t.cuda()) if how == "cuda" else (k.pin_memory(), t.pin_memory())
+        m = rs.peeksort(k, cfg, tags=t)
+        got_k, got_t = k.cpu().numpy(), t.cpu().numpy()
+    assert np.array_equal(got_k, ref_k) and np.array_equal(got_t, ref_t)
+    assert _mt(m)[:3] == ref.metrics_tuple()[:3]

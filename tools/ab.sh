@@ -12,7 +12,7 @@ for v in "$@"; do
 import json, sys
 v, c = sys.argv[1], sys.argv[2]
 d = json.load(open(f"gpurun_out/ab/{v}_{c}.json"))
-print(f"{v:10s} cfg{c} {d['ms_per_step']:.4f} ms", {k: round(x, 4) for k, x in d.get("phase_ms", {}).items()}, "sorted" if d.get("sorted_ok") else "UNSORTED", flush=True)
+print(f"{v:10s} cfg{c} {d['ms_per_step']:.4f} ms", {k: round(x, 4) for k, x in d.get("phase_ms", {}).items()}, "parity" if d.get("parity", {}).get("ok") else "PARITY-FAIL", flush=True)
 PY
   done
 done
