@@ -716,6 +716,9 @@ def main():
         import torch.distributed as dist
 
         torch.cuda.set_device(local_rank)
+        # stdout carries the one JSON line: NCCL's own "NCCL version ..." banner
+        # (printed to stdout when NCCL_DEBUG is VERSION or WARN) goes to stderr
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         if world == 1:
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
             os.environ.setdefault("MASTER_PORT", str(_free_port()))
