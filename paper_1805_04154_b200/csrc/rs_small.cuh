@@ -363,44 +363,54 @@ __device__ void small_tree(const TreeArrays& T, ClassifyArgs A, unsigned char* s
   if ((tid & 31) == 0 && maxd) atomicMax(&s_maxd, maxd);
   RS_TS(met, 8);
   __syncthreads();  // A.need / A.cls / T.child of every item written (descriptors read them)
-  // ---- job list: phase-A jobs by position, then merge jobs by (depth desc, position).
+  // ---- job list: phase-A jobs -- the fused ones first (a fused subtree runs for
+  // tens of thousands of cycles, a leaf tile for ~6K: claimed last it would end
+  // the phase), then the leaf tiles, each group by position -- then merge jobs.
   // Each job's first task slot and its own index come from one packed scan
-  // (jobs << 32 | tasks); merge jobs carry their node's descriptor.
+  // (fused jobs << 45 | leaf jobs << 32 | leaf tasks; a fused job is one task);
+  // merge jobs carry their node's descriptor.
   unsigned long long vA = 0;
   for (int q = 0; q < per; ++q) {
     const int64_t i = i0 + q;
     if (i >= r) break;
-    uint32_t tl = s_aof[i] - (s_nc[i] == 1 ? 1u : 0u);  // the leaf's own tasks
-    uint32_t jobs = (s_lc[i] == 1 || (s_lc[i] == 2 && tl > 0) ? 1u : 0u) + (s_nc[i] == 1 ? 1u : 0u);
-    vA += ((unsigned long long)jobs << 32) | s_aof[i];
+    const uint32_t tl = s_aof[i] - (s_nc[i] == 1 ? 1u : 0u);  // the leaf's own tasks
+    const unsigned long long jf = (s_lc[i] == 1 ? 1u : 0u) + (s_nc[i] == 1 ? 1u : 0u);
+    const unsigned long long jl = (s_lc[i] == 2 && tl > 0) ? 1u : 0u;
+    vA += (jf << 45) | (jl << 32) | (jl ? tl : 0u);
   }
   unsigned long long totv;
   RS_TSD(met, 0);
   unsigned long long ex = block_excl_scan_u64(vA, sred, &totv);
   RS_TSD(met, 1);
-  const uint32_t totA = (uint32_t)totv;
+  const uint32_t totF = (uint32_t)(totv >> 45), totJL = (uint32_t)(totv >> 32) & 0x1fffu;
+  const uint32_t totA = totF + (uint32_t)totv;
   {
-    uint32_t slot = (uint32_t)ex, jb = (uint32_t)(ex >> 32);
+    uint32_t jf = (uint32_t)(ex >> 45);                       // fused job index = its slot
+    uint32_t jl = totF + ((uint32_t)(ex >> 32) & 0x1fffu);    // leaf job index
+    uint32_t slot = totF + (uint32_t)ex;                      // leaf job's first slot
     for (int q = 0; q < per; ++q) {
       int64_t i = i0 + q;
       if (i >= r) break;
       uint32_t lid = A.leaf_base + (uint32_t)i;
       const uint8_t lc = s_lc[i], nc = s_nc[i];
       uint32_t tl = s_aof[i] - (nc == 1 ? 1u : 0u);
-      if (lc == 1 || (lc == 2 && tl > 0)) {
-        uint32_t kind = lc == 1 ? (uint32_t)kTaskFuse : (uint32_t)kTaskLeaf;
-        J.slot[jb] = slot;
-        J.id[jb] = lid;
-        J.cnt[jb] = tl | (kind << 30);
-        ++jb;
+      if (lc == 1) {
+        J.slot[jf] = jf;
+        J.id[jf] = lid;
+        J.cnt[jf] = 1u | ((uint32_t)kTaskFuse << 30);
+        ++jf;
+      } else if (lc == 2 && tl > 0) {
+        J.slot[jl] = slot;
+        J.id[jl] = lid;
+        J.cnt[jl] = tl | ((uint32_t)kTaskLeaf << 30);
+        ++jl;
         slot += tl;
       }
       if (nc == 1) {
-        J.slot[jb] = slot;
-        J.id[jb] = (uint32_t)i;
-        J.cnt[jb] = 1u | ((uint32_t)kTaskFuse << 30);
-        ++jb;
-        slot += 1;
+        J.slot[jf] = jf;
+        J.id[jf] = (uint32_t)i;
+        J.cnt[jf] = 1u | ((uint32_t)kTaskFuse << 30);
+        ++jf;
       }
     }
   }
@@ -409,7 +419,7 @@ __device__ void small_tree(const TreeArrays& T, ClassifyArgs A, unsigned char* s
   for (int64_t i = 1 + tid; i < r; i += nt)
     if (A.cls[i] == 2) J.md[i] = load_mdesc(A, (uint32_t)i);
   RS_TSD(met, 2);
-  uint32_t jbase = (uint32_t)(totv >> 32);
+  uint32_t jbase = totF + totJL;
   uint64_t base = totA;
   const int dmax = (int)s_maxd;
   RS_TSD(met, 3);

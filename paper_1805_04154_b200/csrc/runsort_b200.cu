@@ -137,7 +137,9 @@ size_t prep_smem_bytes(int w, int kb, int ct) {
   return sm;
 }
 
-// Positions per chain tile (k_prep is instantiated for 1024, 2048 and 2560):
+// Positions per chain tile (k_prep is instantiated for 512, 1024, 2048 and 2560):
+// up to 2^22 keys 512 (short leaves make the per-tile walks and the leaf emission serial chains of
+// tile / min_run_len steps; measured on random permutations and config-2-shaped inputs);
 // below ~7M keys 2048-position tiles leave most prep warps without a tile and
 // 1024 is faster (cfg1, n = 2^20: -9%); above that 2560 (fewer tiles for
 // the group/emit phases; 2048 remains the shared-memory fallback).  A function of n only, so every layout agrees.
@@ -145,7 +147,8 @@ size_t prep_smem_bytes(int w, int kb, int ct) {
 // windows fit in shared memory (a function of (n, w, key bytes) only).
 inline int chain_tile_for(int64_t n, int w, int kb) {
   int ct;
-  if (int v = tun().chain_tile) ct = v >= 2560 ? 2560 : (v >= 2048 ? 2048 : 1024);  // tuning override
+  if (int v = tun().chain_tile) ct = v >= 2560 ? 2560 : (v >= 2048 ? 2048 : (v >= 1024 ? 1024 : 512));  // tuning override
+  else if (n <= ((int64_t)1 << 22) && w <= 64) ct = 512;  // round 2: cfg1 (2^20) -17 us vs 1024, random 4M -13 us, cfg2-shaped 2M equal
   else if (n < (int64_t)2048 * 3552) ct = 1024;
   else ct = 2560;  // round 2: cfg2 (1e7) -2.8 us vs 2048 (3 repeats), cfg3 -4 us, cfg4 -30 us
   while (ct > 1024 && prep_smem_bytes(w, kb, ct) > kMaxSmemPerBlock) ct = ct == 2560 ? 2048 : 1024;
@@ -622,8 +625,12 @@ int run_powersort(K* keys, void* tags, int64_t n, int w, int classic, unsigned c
   if (tun().est_c1 > 0) PA.CA.est_c1 = tun().est_c1;
   PA.jobs = SmallJobs::at(V.jobs);
   int grid_p;
-  void* kprep = ct == 1024 ? (void*)k_prep<K, 1024> : ct == 2560 ? (void*)k_prep<K, 2560> : (void*)k_prep<K, 2048>;
-  if (int e = (ct == 1024   ? prep_grid<K, 1024>(sms, sm, &grid_p)
+  void* kprep = ct == 512    ? (void*)k_prep<K, 512>
+                : ct == 1024 ? (void*)k_prep<K, 1024>
+                : ct == 2560 ? (void*)k_prep<K, 2560>
+                             : (void*)k_prep<K, 2048>;
+  if (int e = (ct == 512    ? prep_grid<K, 512>(sms, sm, &grid_p)
+               : ct == 1024 ? prep_grid<K, 1024>(sms, sm, &grid_p)
                : ct == 2560 ? prep_grid<K, 2560>(sms, sm, &grid_p)
                             : prep_grid<K, 2048>(sms, sm, &grid_p)))
     return e;
