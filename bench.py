@@ -716,9 +716,12 @@ def main():
         import torch.distributed as dist
 
         torch.cuda.set_device(local_rank)
-        # stdout carries the one JSON line: NCCL's own "NCCL version ..." banner
-        # (printed to stdout when NCCL_DEBUG is VERSION or WARN) goes to stderr
-        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+        # stdout carries the one JSON line: anything a library writes to file
+        # descriptor 1 while the ranks run (NCCL prints a "NCCL version ..."
+        # banner there on this image) goes to stderr instead
+        sys.stdout.flush()
+        json_fd = os.dup(1)
+        os.dup2(2, 1)
         if world == 1:
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
             os.environ.setdefault("MASTER_PORT", str(_free_port()))
@@ -732,7 +735,7 @@ def main():
         if rank == 0:
             if world == 1 and not args.no_cpu_baseline and args.config != 5:
                 out["cpu_baseline"] = run_cpu_reference(args)
-            print(json.dumps(out))
+            os.write(json_fd, (json.dumps(out) + "\n").encode())
         dist.destroy_process_group()
         return 0
 
