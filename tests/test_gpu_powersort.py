@@ -158,3 +158,67 @@ def test_baseline_configs_full_size(cfg):
     if tags is not None:
         assert np.array_equal(tw, ref_t)
     assert _mt(m) == ref.metrics_tuple()
+
+
+# ---- thresholds of the device path: every size rule has a case on each side
+def _segments(r, seg_len, rng, desc_every=0, dtype=np.int32):
+    """r natural runs of seg_len keys (>= min_run_len, so exactly r leaves): each
+    segment ascends over the same value range, so every boundary is a descent;
+    every desc_every-th segment is strictly descending instead."""
+    out = np.empty(r * seg_len, dtype=dtype)
+    for k in range(r):
+        seg = np.sort(rng.choice(1 << 20, size=seg_len, replace=False)).astype(dtype)
+        if desc_every and k % desc_every == desc_every - 1:
+            seg = seg[::-1] + (1 << 21)  # strictly descending, above its neighbours
+        out[k * seg_len:(k + 1) * seg_len] = seg
+    return out
+
+
+@pytest.mark.parametrize("r", [2047, 2048, 2049, 2050])
+@pytest.mark.parametrize("desc_every", [0, 3])
+def test_small_tree_threshold(r, desc_every):
+    """Trees of <= 2048 leaves are built by one CTA out of shared memory (ready-time
+    job order, fused >= 3-leaf subtrees), larger ones by the grid phases."""
+    rng = np.random.default_rng(100 + r + desc_every)
+    a = _segments(r, 40, rng, desc_every)
+    tags = np.arange(len(a), dtype=np.int32)
+    for mk in ("bitonic", "classic"):
+        work, tw, m = _run_gpu(a, 24, mk, tags)
+        rk, rt = a.copy(), tags.copy()
+        ref = oracle.powersort(rk, 24, mk, rt)
+        assert np.array_equal(work, rk) and np.array_equal(tw, rt)
+        assert _mt(m) == ref.metrics_tuple()
+        if desc_every == 0:
+            assert m.runs_detected == r
+
+
+@pytest.mark.parametrize("n", [(1 << 22) - 1, 1 << 22, (1 << 22) + 1, 2048 * 3552 - 1, 2048 * 3552])
+def test_chain_tile_thresholds(n):
+    """The chain-tile size is chosen from n (512 / 1024 / 2560 positions)."""
+    keys = workloads.config2(n, seed=3, mean=700.0)
+    work, _, m = _run_gpu(keys, 24, "bitonic")
+    ref_k = keys.copy()
+    ref = oracle.powersort(ref_k, 24, "bitonic")
+    assert np.array_equal(work, ref_k)
+    assert _mt(m) == ref.metrics_tuple()
+
+
+def test_long_leaves_small_tree_fuses_three_leaf_subtrees():
+    """Long leaves on average (n >= 256 r) with clusters of short runs: the small-tree
+    path fuses the clusters (>= 3 leaves within 4096 elements) and leaves pairs to the
+    executor; output, payload and Metrics equal the oracle either way."""
+    rng = np.random.default_rng(77)
+    parts = []
+    for k in range(40):
+        parts.append(np.sort(rng.integers(0, 1 << 30, size=200_000, dtype=np.int64)).astype(np.int32))
+        for length in rng.integers(25, 900, size=int(rng.integers(1, 6))):
+            seg = np.sort(rng.integers(0, 1 << 30, size=int(length), dtype=np.int64)).astype(np.int32)
+            parts.append(seg[::-1].copy() if k % 2 else seg)
+    a = np.concatenate(parts)
+    tags = np.arange(len(a), dtype=np.int64)
+    work, tw, m = _run_gpu(a, 24, "classic", tags)
+    rk, rt = a.copy(), tags.copy()
+    ref = oracle.powersort(rk, 24, "classic", rt)
+    assert np.array_equal(work, rk) and np.array_equal(tw, rt)
+    assert _mt(m) == ref.metrics_tuple()
+    assert len(a) >= 256 * m.runs_detected
