@@ -85,6 +85,7 @@ struct DevMetrics {
   unsigned long long prep_dbg[32];           // RS_INSTR: finer timestamps inside prep phases
   unsigned int last_ctr[8];                  // 'last block done' counters of the prep kernel
   unsigned long long peek[8];                // peeksort replay counters (frontier sizes, records)
+  unsigned long long peek_lev;               // peeksort: the level at which block 0 handed the replay to the grid
 };
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {

@@ -577,7 +577,68 @@ __global__ void __launch_bounds__(256, 2) k_peek(PeekArgs P) {
   // front[(L+1) & 1] / front_n[(L+1) % 3]; front_n[(L+2) % 3] was last read at
   // level L-1, so thread 0 clears it now and one barrier per level suffices
   // (plus one after a level's reversals, whose keys the next evaluations read).
-  int lev = 0;
+  // The first levels hold a handful of calls each and are pure latency: block 0
+  // replays them alone, one call per thread, with the frontier ping-pong, its
+  // counters and the record counters in shared memory (the same peek_item, its
+  // PeekOut pointing at shared memory) behind __syncthreads instead of grid
+  // barriers, until a level has more calls than the block has threads, a
+  // reversal is pending (all blocks share the swaps) or a record array is
+  // full.  Then it writes frontier and counters back and the grid continues.
+  {
+    constexpr int kTopCap = 512;  // calls per shared-memory frontier (a level of <= 256 pushes <= 512)
+    extern __shared__ __align__(16) unsigned char smem_peek[];  // k_peek's dynamic shared memory (kFillSmem), free until the task fill
+    static_assert(2 * kTopCap * sizeof(PeekItem) <= (size_t)kFillSmem, "shared-memory frontier fits the fill staging area");
+    __shared__ unsigned long long s_fn[2], s_nn, s_nl, s_nr, s_err2[2];
+    if (blockIdx.x == 0) {
+      PeekItem* sf[2] = {reinterpret_cast<PeekItem*>(smem_peek), reinterpret_cast<PeekItem*>(smem_peek) + kTopCap};
+      const unsigned long long c0 = *(volatile unsigned long long*)&pc->front_n[0];
+      if (threadIdx.x == 0) {
+        s_fn[0] = c0;
+        s_fn[1] = 0;
+        s_nn = pc->n_nodes;
+        s_nl = pc->n_leaves;
+        s_nr = pc->n_revs;
+        s_err2[0] = pc->err[0];
+        s_err2[1] = 0;
+      }
+      for (unsigned long long x = threadIdx.x; x < c0 && x < (unsigned long long)kTopCap; x += blockDim.x) sf[0][x] = P.front[0][x];
+      __syncthreads();
+      PeekOut T = O;
+      T.n_nodes = &s_nn;
+      T.n_leaves = &s_nl;
+      T.n_revs = &s_nr;
+      T.front_cap = kTopCap;
+      int tl = 0;
+      for (;;) {
+        const unsigned long long cnt = s_fn[tl & 1];
+        if (cnt == 0 || cnt > (unsigned long long)blockDim.x || s_nr != 0 || s_err2[tl & 1] != 0) break;
+        T.next = sf[(tl + 1) & 1];
+        T.next_cnt = &s_fn[(tl + 1) & 1];
+        T.err = &s_err2[(tl + 1) & 1];
+        if (threadIdx.x < cnt) peek_item<K>(V, sf[tl & 1][threadIdx.x], P.w, T);
+        __syncthreads();
+        if (threadIdx.x == 0) s_fn[tl & 1] = 0;  // this level's slot is the one after next
+        ++tl;
+        __syncthreads();
+      }
+      // hand over level tl: frontier, its counters (the next two slots empty), records, errors
+      const unsigned long long cnt = s_fn[tl & 1];
+      for (unsigned long long x = threadIdx.x; x < cnt; x += blockDim.x) P.front[tl & 1][x] = sf[tl & 1][x];
+      if (threadIdx.x == 0) {
+        pc->front_n[tl % 3] = cnt;
+        pc->front_n[(tl + 1) % 3] = 0;
+        pc->front_n[(tl + 2) % 3] = 0;
+        pc->n_nodes = s_nn;
+        pc->n_leaves = s_nl;
+        pc->n_revs = s_nr;
+        pc->err[tl & 1] = s_err2[tl & 1];
+        pc->err[(tl + 1) & 1] = 0;
+        met->peek_lev = (unsigned long long)tl;
+      }
+    }
+    grid.sync();
+  }
+  int lev = (int)*(volatile unsigned long long*)&met->peek_lev;
   unsigned long long rev_done = 0;
   constexpr int kRevBatches = 256;  // reversal batches (one per level that reversed something)
   __shared__ unsigned long long s_revb[kRevBatches];
