@@ -377,7 +377,14 @@ __device__ void d_task_fill(ClassifyArgs A, const uint32_t* __restrict__ chunk_d
   const int64_t oc = ord_chunk(r);
   int64_t nch = (r + oc - 1) / oc;
   int lane = threadIdx.x & 31;
-  for (int64_t ch = blockIdx.x; ch < nch; ch += gridDim.x) {
+  // Few chunks (config 2: 13 for 3,230 leaves) would leave the record writes of
+  // the tree's top -- thousands of tiles in one chunk -- to a handful of
+  // blocks: every chunk is taken by `slices` blocks, which all rank its nodes
+  // (cheap, redundant) and each write one slice of its task records.
+  const int64_t slices = nch > 0 && (int64_t)gridDim.x / nch > 1 ? (int64_t)gridDim.x / nch : 1;
+  for (int64_t vb = blockIdx.x; vb < nch * slices; vb += gridDim.x) {
+    const int64_t ch = vb / slices;
+    const uint32_t sl = (uint32_t)(vb % slices);
     __syncthreads();
     for (int d = threadIdx.x; d < kMaxDepth; d += blockDim.x) run[d] = chunk_depth[ch * kMaxDepth + d];
     int64_t i0 = ch * oc, i1 = (ch + 1) * oc < r ? (ch + 1) * oc : r;
@@ -451,7 +458,7 @@ __device__ void d_task_fill(ClassifyArgs A, const uint32_t* __restrict__ chunk_d
       __syncthreads();
       RS_DBG(A.met, 23);
       const int ny = cnt_i - g < (int64_t)blockDim.x ? (int)(cnt_i - g) : (int)blockDim.x;
-      for (uint32_t q = threadIdx.x; q < tot; q += blockDim.x) {
+      for (uint32_t q = sl * blockDim.x + threadIdx.x; q < tot; q += (uint32_t)slices * blockDim.x) {
         int lo = 0, hi = ny - 1;  // last node y with s_pre[y] <= q
         while (lo < hi) {
           int md = (lo + hi + 1) >> 1;
