@@ -200,3 +200,23 @@ def test_peeksort_compact_overflow_public_api(how):
         got_k, got_t = k.cpu().numpy(), t.cpu().numpy()
     assert np.array_equal(got_k, ref_k) and np.array_equal(got_t, ref_t)
     assert _mt(m)[:3] == ref.metrics_tuple()[:3]
+
+
+def test_peeksort_compact_overflow_recorded_tree():
+    """record_tree after the worst-case retry: the exported tree is the oracle's."""
+    import sys
+
+    n, w = 60_000, 2
+    a = _zigzag(n, 14).astype(np.int64)
+    ref_k = a.copy()
+    ref = oracle.peeksort(ref_k, w, "bitonic", want_tree=True)
+    assert ref.runs_detected > n // 12 + 4096
+    work, _, m = _run(a, w, "bitonic", record=True)
+    assert np.array_equal(work, ref_k)
+    assert _mt(m)[:3] == ref.metrics_tuple()[:3]
+    old = sys.getrecursionlimit()
+    sys.setrecursionlimit(10000)
+    try:
+        assert _shape(m.merge_tree) == oracle.peek_tree_from_merges(n, ref.merges)
+    finally:
+        sys.setrecursionlimit(old)
